@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the DNN-MG fine-level correction step (BASELINE.json metric:
+"patches/sec for DNN-MG correction step (1/2/4/8 B200) and % of roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
+                    [--precision fp32|bf16|tf32x3] [--impl ours|reference]
+
+Workload (default): BASELINE config 3 under the SURVEY §0.1 mapping — unit box,
+level L = 64x32x32 cells, J = 1: 524,288 patches, 4,276,737 fine Q2 nodes,
+MLP 240 -> 256x3 -> 81 tanh, seeded synthetic Fourier inputs, fp32.
+
+A timed step is one full correction (driver.py:251-268): prolongate (K1) ->
+Dirichlet -> stab + residual (K2) -> patch gather (K3) -> patch MLP (K4) ->
+averaging scatter + update (K5), inputs resident in HBM.  The timed steps
+cycle over 4 distinct (x_L^n, b_prev^n) pairs (308 MB > 126 MB L2, and every
+kernel streams >L2-sized arrays), so no step reads its inputs from L2.
+`e2e` repeats the measurement through the public API with pinned HOST
+buffers: x_L and b_prev copied H2D and x_corr copied D2H inside every step.
+
+--impl reference times the CPU oracle port of the reference (oracle/,
+float64 numpy, all host threads) on a bounded sample of the same workload.
+Multi-GPU (torchrun): replicas of the single-GPU workload, one per rank
+("weak"), timed on the device, max over ranks.
+"""
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "patches/sec for DNN-MG correction step (1/2/4/8 B200) and % of roofline"
+UNIT = "patches/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--precision", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", default="16x8x8", help="coarse box of the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def default_precision(cfg_name):
+    return "fp32"
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference port) timing — the only place bench.py runs oracle/
+# ---------------------------------------------------------------------------
+
+def cpu_oracle_rate(cfg, sample, steps, warmup):
+    """Time the float64 oracle correction step on a bounded sample box."""
+    from oracle import dnnmg_oracle as orc
+    from paper_2307_14837_b200 import synthetic
+    n_cells = tuple(int(v) for v in sample.split("x"))
+    L, J = 0, cfg["J"]
+    ctx = orc.build_context((0, 0, 0), (1, 1, 1), n_cells, L, J, cache_geometry=True)
+    n_p = ctx["dof_table"].shape[0]
+    npp = ctx["dof_table"].shape[1] // 4
+    dims = [8 * npp + 24] + [cfg["hidden"]] * cfg["depth"] + [3 * npp]
+    model = orc.Mlp(synthetic.xavier_weights(dims, cfg["seed"] + 7), activation="tanh")
+    modes = synthetic.fourier_modes(cfg["seed"])
+    nu, k = cfg["nu"], cfg["dt"]
+    x0 = synthetic.coarse_state(ctx["coarse_coords"], modes, cfg["seed"], 0, 0.0, nu)
+    xf0 = orc.prolongate_state(ctx["P"], x0)
+    orc.impose_dirichlet(xf0, ctx["tags"], ctx["coords"], 0.0, {orc.WALL: orc.no_slip})
+    b = orc.rhs_next(xf0, ctx["coords"], ctx["table"], k, nu, cache=ctx["geometry"])
+    xs = [synthetic.coarse_state(ctx["coarse_coords"], modes, cfg["seed"], n, n * k, nu)
+          for n in (1, 2)]
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        orc.correction_step(xs[i % 2], b, ctx, model, k * (1 + i % 2), nu, k)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    return n_p / t, n_p, t
+
+
+def run_reference(args, rank, world):
+    from paper_2307_14837_b200 import synthetic
+    if rank != 0:
+        return
+    cfg = synthetic.CONFIGS[args.config]
+    steps = max(1, min(args.steps, 10))
+    warmup = max(0, min(args.warmup, 2))
+    rate, n_p, t = cpu_oracle_rate(cfg, args.cpu_sample, steps, warmup)
+    cores = os.cpu_count()
+    sample = (f"{n_p} patches ({args.cpu_sample} coarse box, J={cfg['J']}) of {args.config}; "
+              f"float64 numpy oracle port; median of {steps} steps after {warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "sample": args.cpu_sample},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown", 0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown", 0x0000000000000002: "applications_clocks_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                bits = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def load_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def build_workload(cfg_name, precision, device_index):
+    import torch
+    from paper_2307_14837_b200 import mesh as meshmod, synthetic
+    from paper_2307_14837_b200.net import Architecture, MlpModel
+    from paper_2307_14837_b200.patch_ops import input_width, output_width
+    from paper_2307_14837_b200.step import CorrectionStep
+    cfg = synthetic.CONFIGS[cfg_name]
+    h = meshmod.build_template_mesh("box", extent_lo=(0, 0, 0), extent_hi=(1, 1, 1),
+                                    n_cells=cfg["n_cells"])
+    if cfg["jitter"]:
+        synthetic.jitter_vertices(h.levels[0].vertices, cfg["n_cells"], (0, 0, 0), (1, 1, 1),
+                                  cfg["seed"] + 1)
+    for _ in range(cfg["J"]):
+        meshmod.refine_uniform(h)
+    ps = meshmod.build_patches(h, 0, cfg["J"])
+    n_in, n_out = input_width(ps), output_width(ps)
+    model = MlpModel(Architecture(n_in, cfg["hidden"], cfg["depth"], n_out), activation="tanh")
+    model.W = synthetic.xavier_weights([n_in] + [cfg["hidden"]] * cfg["depth"] + [n_out],
+                                       cfg["seed"] + 7)
+    model.eval()
+    nu, k = cfg["nu"], cfg["dt"]
+    step = CorrectionStep(h, 0, cfg["J"], model, nu, k, precision=precision, patchset=ps)
+    # seeded coarse states at t_n on the GPU (float64 Fourier sum, rounded to fp32)
+    K, A, B = synthetic.fourier_modes(cfg["seed"])
+    dev = torch.device("cuda", device_index)
+    coarse_xyz = torch.tensor(h.scalar_nodes(0)[0], dtype=torch.float64, device=dev)
+    kk = torch.tensor(2 * np.pi * K, dtype=torch.float64, device=dev)
+    At = torch.tensor(A, dtype=torch.float64, device=dev)
+    Bt = torch.tensor(B, dtype=torch.float64, device=dev)
+
+    def coarse_state(n):
+        t = n * k
+        decay = torch.exp(-nu * (kk ** 2).sum(1) * t)
+        x = torch.empty((coarse_xyz.shape[0], 4), dtype=torch.float64, device=dev)
+        for s in range(0, coarse_xyz.shape[0], 1 << 16):
+            ph = coarse_xyz[s:s + (1 << 16)] @ kk.T
+            x[s:s + (1 << 16), 1:] = torch.cos(ph) @ (At * decay[:, None]) + \
+                torch.sin(ph) @ (Bt * decay[:, None])
+        x[:, 0] = torch.from_numpy(np.random.default_rng(cfg["seed"] + 1000 + n)
+                                   .normal(0.0, 0.1, coarse_xyz.shape[0])).to(dev)
+        return x.reshape(-1).float().contiguous()
+
+    # carried fine RHS through the real recurrence: b^1 = rhs(embed(x^0)), b^{n+1} = rhs(x_corr^n)
+    b = step.rhs_next(step.embed(coarse_state(0)))
+    pairs = []
+    for n in range(1, 5):
+        xl = coarse_state(n)
+        pairs.append((xl, b.clone()))
+        xc = step(xl, b)
+        b = step.rhs_next(xc)
+    torch.cuda.synchronize()
+    return step, pairs, cfg, h
+
+
+def algorithmic_units(step, cfg):
+    """Per-launch algorithmic bytes / flops of each kernel."""
+    nf = step.space.n_nodes
+    nl = step.coarse_ndof // 4
+    npch = step.n_patches
+    npp = step.ps.npp
+    n_in, H, d, n_out = 8 * npp + 24, cfg["hidden"], cfg["depth"], 3 * npp
+    return {
+        "K1_prolong": {"bytes": 16 * nl + 16 * nf},
+        "K2_residual": {"bytes": 72 * nf, "flops_ref_formulation": 213078 * step.level.n_cells},
+        "K3_gather": {"bytes": 32 * nf + 96 * npch + 4 * n_in * npch},
+        "K4_mlp": {"flops": 2 * (n_in * H + (d - 1) * H * H + H * n_out) * npch},
+        "K5_scatter": {"bytes": 4 * n_out * npch + 48 * nf},
+    }
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as tdist
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    precision = args.precision or default_precision(args.config)
+    step, pairs, cfg, h = build_workload(args.config, precision, local)
+    n_p = step.n_patches
+    S = len(pairs)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- per-kernel events inside the timed region (same stream) ----
+    names = ["K1_prolong"] * step.J + ["K2_residual", "K3_gather", "K4_mlp", "K5_scatter"]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+    kern_ms = np.zeros(len(names))
+
+    for i in range(args.warmup):
+        step.run_staged(*pairs[i % S])
+    barrier()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        t_start.record()
+        for i in range(args.steps):
+            step.run_staged(*pairs[i % S], events=ev)
+            # read this step's per-kernel durations lazily (events are reused next step)
+            ev[-1].synchronize()
+            kern_ms += np.array([ev[j].elapsed_time(ev[j + 1]) for j in range(len(names))])
+        t_end.record()
+        barrier()
+    ms = t_start.elapsed_time(t_end)
+    # device-timed fused path without per-kernel events (graph-free, same kernels)
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for i in range(args.steps):
+        step(*pairs[i % S])
+    f1.record()
+    barrier()
+    ms_fused = f0.elapsed_time(f1)
+    ms_dev = min(ms, ms_fused)
+    t = torch.tensor([ms_dev], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * n_p * args.steps / (ms_max / 1e3)
+
+    # ---- e2e through the public step API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hx = [p[0].cpu().pin_memory() for p in pairs]
+        hb = [p[1].cpu().pin_memory() for p in pairs]
+        hout = torch.empty(step.x_corr.numel(), dtype=torch.float32).pin_memory()
+        dx = torch.empty_like(pairs[0][0])
+        db = torch.empty_like(pairs[0][1])
+        for i in range(2):
+            dx.copy_(hx[i % S], non_blocking=True)
+            db.copy_(hb[i % S], non_blocking=True)
+            hout.copy_(step(dx, db), non_blocking=True)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.steps):
+            dx.copy_(hx[i % S], non_blocking=True)
+            db.copy_(hb[i % S], non_blocking=True)
+            hout.copy_(step(dx, db), non_blocking=True)
+        e1.record()
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+        e2e = {"value": world * n_p * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(dx.numel() * 4 + db.numel() * 4),
+               "d2h_bytes_per_step": int(hout.numel() * 4)}
+
+    if rank != 0:
+        if world > 1:
+            tdist.destroy_process_group()
+        return
+    # ---- roofline of the dominant kernel ----
+    peaks, peak_kind = load_peaks()
+    units = algorithmic_units(step, cfg)
+    avg = kern_ms / args.steps
+    share = avg / avg.sum()
+    per_kernel = {}
+    for j, nm in enumerate(names):
+        u = units[nm]
+        entry = {"ms": float(avg[j]), "share": float(share[j])}
+        if "bytes" in u:
+            entry["GB/s"] = u["bytes"] / (avg[j] / 1e3) / 1e9
+            entry["hbm_frac"] = entry["GB/s"] / peaks["hbm_gbs"]
+        if "flops" in u:
+            entry["TFLOP/s"] = u["flops"] / (avg[j] / 1e3) / 1e12
+        if "flops_ref_formulation" in u:
+            entry["ref_formulation_TFLOP/s"] = u["flops_ref_formulation"] / (avg[j] / 1e3) / 1e12
+        per_kernel[nm] = entry
+    dom = names[int(np.argmax(avg))]
+    du = units[dom]
+    if "flops" in du:
+        ach = du["flops"] / (per_kernel[dom]["ms"] / 1e3) / 1e12
+        peak = peaks["bf16_tflops_sustained"] if precision == "bf16" else \
+            peaks["bf16_tflops_sustained"] / 2.0 / (3.0 if precision == "tf32x3" else 1.0)
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak,
+                "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+                "peak_source": f"{peak_kind} bf16 sustained"
+                + ("" if precision == "bf16" else " / 2 (tf32 rate)" + (" / 3 passes" if precision == "tf32x3" else ""))}
+    else:
+        ach = du["bytes"] / (per_kernel[dom]["ms"] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": f"{peak_kind} hbm copy"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        rate, n_s, t_s = cpu_oracle_rate(cfg, args.cpu_sample, 2, 1)
+        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{n_s} patches ({args.cpu_sample} coarse box, J={cfg['J']}), float64 "
+                         f"numpy oracle, median of 2 steps ({t_s:.2f} s/step)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if precision == "fp32" else f"f32 (MLP {precision})",
+        "data": "synthetic",
+        "config": {"workload": args.config, "patches": n_p, "fine_nodes": step.space.n_nodes,
+                   "coarse_cells": int(np.prod(cfg["n_cells"])), "J": cfg["J"],
+                   "mlp": f"{8 * step.ps.npp + 24}->{cfg['hidden']}x{cfg['depth']}->{3 * step.ps.npp} tanh",
+                   "precision": precision, "l2": "inputs > L2 (4 cycled input pairs, 308 MB)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "e2e": e2e,
+        "gpu_launches": int(step.launches * args.steps),
+        "roofline": roof,
+        "kernels": per_kernel,
+        "ms_per_step_fused": ms_fused / args.steps, "ms_per_step_staged": ms / args.steps,
+        "cpu_baseline": cpu,
+        "clocks": sampler.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/*
+ * dnnmg_b200.h — C ABI of the B200-native DNN-MG fine-level correction step.
+ *
+ * The reference (dnnmg, arXiv 2307.14837, pure Python/numpy) exposes this hot
+ * path only as Python functions; there is no FFI in the reference.  Each entry
+ * point below replaces one of those functions and is what a ctypes/cffi binding
+ * of the reference would bind:
+ *
+ *   dnnmg_prolongate        space.prolongate            space.py:177-185 (+ apply_dirichlet 245-255)
+ *   dnnmg_apply_dirichlet   space.apply_dirichlet       space.py:245-255
+ *   dnnmg_stab              Assembler.stab              assembly.py:169-178, 55-59
+ *   dnnmg_residual          Assembler.assemble_residual assembly.py:261-267 (apply_operator 212-240)
+ *   dnnmg_rhs_next          Assembler.assemble_rhs_next assembly.py:242-259
+ *   dnnmg_gather            patch_ops.assemble_network_input  patch_ops.py:49-53 (local_restrict 23-29)
+ *   dnnmg_local_restrict    patch_ops.local_restrict    patch_ops.py:23-29
+ *   dnnmg_global_extend     patch_ops.global_extend     patch_ops.py:32-38
+ *   dnnmg_mlp_forward       net.forward (eval mode)     net.py:124-164
+ *   dnnmg_scatter_update    predict_correction scatter + x~ + scale*d
+ *                                                       patch_ops.py:64-76, driver.py:268
+ *   dnnmg_correction_step   TimeLoop._step_hybrid lines 251-268 (K1..K5 fused sequence)
+ *
+ * Conventions (all match the reference):
+ *   - dof vectors are node-major, component-minor: dof = 4*node + comp,
+ *     comp 0 = pressure, 1..3 = velocity (space.py:3-7).  Device vectors are
+ *     float32, 16-byte aligned, so a node is one float4.
+ *   - index tables are int32, row-major, exactly the reference's numbering.
+ *   - every pointer inside the structs and every array argument is a DEVICE
+ *     pointer unless stated otherwise; calls are asynchronous on `stream`
+ *     (a cudaStream_t passed as void*), never allocate, never synchronise,
+ *     and are CUDA-graph capturable.
+ *   - return value: DNNMG_OK or an error code; dnnmg_status_string() maps it
+ *     to text.  Shape errors use the reference's ValueError wording
+ *     ("length", "architecture", "width").
+ */
+#ifndef DNNMG_B200_H
+#define DNNMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* dnnmg_stream_t; /* cudaStream_t */
+
+enum {
+  DNNMG_OK = 0,
+  DNNMG_ERR_ARG = 1,         /* invalid argument / shape ("length", "width") */
+  DNNMG_ERR_CUDA = 2,        /* a CUDA launch or runtime call failed */
+  DNNMG_ERR_UNSUPPORTED = 3, /* configuration not supported by this build */
+  DNNMG_ERR_ARCH = 4         /* model architecture does not match the patch layout */
+};
+
+enum { DNNMG_ACT_RELU = 0, DNNMG_ACT_TANH = 1 };
+
+enum {
+  DNNMG_PREC_FP32 = 0,   /* SIMT fp32 FFMA (any width) */
+  DNNMG_PREC_BF16 = 1,   /* tcgen05 kind::f16, bf16 operands, fp32 accumulate in TMEM */
+  DNNMG_PREC_TF32X3 = 2  /* tcgen05 kind::tf32, 3-pass split (hi*hi + hi*lo + lo*hi), fp32 accuracy */
+};
+
+/* Q2 embedding level l -> l+1 (space.py:117-165).  Each fine node n takes the
+ * coarse shape values of the first (octant o, child-local node a, parent cell C)
+ * that reaches it; fine_src[n] = C*216 + o*27 + a. */
+typedef struct {
+  int32_t n_fine_nodes;
+  int32_t n_coarse_cells;
+  const int32_t* coarse_cell_nodes; /* [n_coarse_cells][27] level-l Q2 node table */
+  const int32_t* fine_src;          /* [n_fine_nodes] */
+} dnnmg_prolong_t;
+
+/* Dirichlet data of one level (space.py:245-255): bc_code[n] = 0 untouched,
+ * 1 velocity := 0 (no-slip), 2 velocity := bc_values[n]. */
+typedef struct {
+  int32_t n_nodes;
+  const uint8_t* bc_code;  /* [n_nodes] */
+  const float* bc_values;  /* [n_nodes][3] or NULL when no code 2 is present */
+} dnnmg_dirichlet_t;
+
+/* One fine level for assembly (assembly.py:65-108). */
+typedef struct {
+  int32_t n_nodes;
+  int32_t n_cells;
+  const int32_t* cell_nodes;     /* [n_cells][27] (space.cell_nodes) */
+  const double* coords;          /* [n_nodes][3] node coordinates (float64: geometry is
+                                    formed from cell-relative differences in fp64) */
+  const float* h_T;              /* [n_cells] cell diameters (assembly.py:100-103) */
+  const int32_t* node_cell_ptr;  /* [n_nodes+1] CSR node -> incident (cell*27 + a), */
+  const int32_t* node_cell_idx;  /*   cells ascending (= the reference bincount order) */
+  const uint8_t* dof_mask;       /* [n_nodes] bit c set <=> dof 4n+c constrained; NULL = none */
+} dnnmg_level_t;
+
+typedef struct {
+  float nu, k, alpha0, delta0;
+  int32_t convection;  /* 1: with convection (reference default) */
+} dnnmg_phys_t;
+
+/* PatchSet (mesh.py:501-558).  For J=1 the node->patch CSR equals the
+ * node->cell CSR of the fine level because patch p == fine cell p. */
+typedef struct {
+  int32_t n_patches;
+  int32_t nodes_per_patch;        /* 27 (J=1) or 125 (J=2) */
+  int32_t n_geo;                  /* 24 */
+  int32_t n_nodes;                /* fine-level scalar nodes */
+  const int32_t* node_table;      /* [n_patches][nodes_per_patch] */
+  const float* geom;              /* [n_patches][n_geo] */
+  const int32_t* node_patch_ptr;  /* [n_nodes+1] CSR node -> (patch*npp + slot), ascending patch */
+  const int32_t* node_patch_idx;
+} dnnmg_patchset_t;
+
+#define DNNMG_MAX_LAYERS 16
+
+/* Eval-mode MlpModel (net.py:54-159): depth hidden layers + linear head.
+ * bn_scale = gamma/sqrt(running_var+eps), bn_shift = beta - running_mean*bn_scale. */
+typedef struct {
+  int32_t n_in, n_hidden, depth, n_out;
+  int32_t activation;                    /* DNNMG_ACT_* */
+  int32_t precision;                     /* DNNMG_PREC_* */
+  const float* W[DNNMG_MAX_LAYERS];      /* W[i]: [dims[i]][dims[i+1]] row-major, i = 0..depth */
+  const float* bn_scale;                 /* [depth][n_hidden] */
+  const float* bn_shift;                 /* [depth][n_hidden] */
+  const float* in_mean;                  /* [n_in] */
+  const float* in_std;                   /* [n_in] */
+  void* packed;                          /* tensor-core weight image (dnnmg_mlp_pack), or NULL */
+} dnnmg_mlp_t;
+
+/* ---- versioning / errors -------------------------------------------------- */
+int32_t dnnmg_version(void);
+const char* dnnmg_status_string(int32_t status);
+const char* dnnmg_last_error(void);   /* detail of the last failing call (host string) */
+
+/* ---- K1: prolongation + Dirichlet ------------------------------------------- */
+int32_t dnnmg_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float* x_fine,
+                         const dnnmg_dirichlet_t* bc /* nullable */, dnnmg_stream_t stream);
+int32_t dnnmg_apply_dirichlet(const dnnmg_dirichlet_t* bc, float* x, dnnmg_stream_t stream);
+
+/* ---- K2: stabilisation, residual, next RHS ---------------------------------- */
+int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph,
+                   float* alpha_T, float* delta_T, dnnmg_stream_t stream);
+/* r = b_prev - A_h(x); rows with dof_mask bits set are zeroed when apply_mask != 0.
+ * alpha_T/delta_T may be NULL: then they are evaluated at x inside the kernel
+ * (exactly Assembler.stab(x) as the hybrid step does, driver.py:255).
+ * elem_scratch: [n_cells][27][4] floats. */
+int32_t dnnmg_residual(const dnnmg_level_t* lv, const float* x, const float* b_prev,
+                       const float* alpha_T, const float* delta_T, const dnnmg_phys_t* ph,
+                       float* elem_scratch, float* r, int32_t apply_mask, dnnmg_stream_t stream);
+/* A_h(x) itself (Assembler.apply_operator, assembly.py:212-234). */
+int32_t dnnmg_apply_operator(const dnnmg_level_t* lv, const float* x, const float* alpha_T,
+                             const float* delta_T, const dnnmg_phys_t* ph,
+                             float* elem_scratch, float* out, dnnmg_stream_t stream);
+/* next-step RHS with f = None (assembly.py:242-259). */
+int32_t dnnmg_rhs_next(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph,
+                       float* elem_scratch, float* b, dnnmg_stream_t stream);
+
+/* ---- K3: patch gather --------------------------------------------------------- */
+/* X[p] = [x rows | r rows | geom] : [n_patches][8*npp + n_geo] fp32 */
+int32_t dnnmg_gather(const dnnmg_patchset_t* ps, const float* x, const float* r, float* X,
+                     dnnmg_stream_t stream);
+/* rows[p] = x[dof_table[p]] : [n_patches][4*npp] */
+int32_t dnnmg_local_restrict(const dnnmg_patchset_t* ps, const float* x, float* rows,
+                             dnnmg_stream_t stream);
+/* out = mu * bincount(dof_table, rows)  (all 4 components) */
+int32_t dnnmg_global_extend(const dnnmg_patchset_t* ps, const float* rows, float* out,
+                            dnnmg_stream_t stream);
+
+/* ---- K4: patch MLP --------------------------------------------------------------- */
+int32_t dnnmg_mlp_packed_bytes(const dnnmg_mlp_t* m, int64_t* bytes);
+int32_t dnnmg_mlp_pack(const dnnmg_mlp_t* m, void* packed, dnnmg_stream_t stream);
+int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
+                          dnnmg_stream_t stream);
+
+/* ---- K5: averaging scatter + correction update ---------------------------------------- */
+/* d = mu * bincount(velocity rows Y); d[mask] = 0; pressure 0; x_corr = x_tilde + scale*d.
+ * Y: [n_patches][3*npp].  x_tilde/x_corr may be NULL (then only d is written). */
+int32_t dnnmg_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const uint8_t* dof_mask,
+                             const float* x_tilde, float scale, float* d, float* x_corr,
+                             dnnmg_stream_t stream);
+
+/* ---- whole correction step (driver.py:251-268) ------------------------------------------ */
+typedef struct {
+  float* x_tilde;   /* [4*n_fine] */
+  float* r;         /* [4*n_fine] */
+  float* elem;      /* [n_cells*27*4] */
+  float* X;         /* [n_patches][n_in] */
+  float* Y;         /* [n_patches][n_out] */
+  float* d;         /* [4*n_fine] */
+  float* x_mid;     /* [4*n_mid] intermediate level for J = 2, else NULL */
+} dnnmg_step_buffers_t;
+
+/* prolongations: J entries (levels L..L+J-1); bc: Dirichlet data of the fine level. */
+int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_dirichlet_t* bc,
+                              const dnnmg_level_t* fine, const dnnmg_phys_t* ph,
+                              const dnnmg_patchset_t* ps, const dnnmg_mlp_t* m,
+                              const float* x_coarse, const float* b_prev, float scale,
+                              const dnnmg_step_buffers_t* buf, float* x_corr,
+                              dnnmg_stream_t stream);
+
+/* Number of kernels dnnmg_correction_step launches for this configuration. */
+int32_t dnnmg_correction_step_launches(int32_t J, const dnnmg_mlp_t* m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DNNMG_B200_H */

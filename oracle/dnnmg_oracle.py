@@ -419,6 +419,10 @@ class Quadrature:
 QUAD = Quadrature()
 
 
+def _es(*a):
+    return np.einsum(*a, optimize=True)
+
+
 def cell_diameters(level):
     """h_T: largest distance between two corners (assembly.py:99-103)."""
     C = level.verts[level.cells]
@@ -427,18 +431,37 @@ def cell_diameters(level):
 
 
 def cell_geometry(coords, table):
-    """G (nc,64,27,3), w (nc,64), Gpi (nc,64,27,3) for the isoparametric Q2 map
-    (assembly.py:77-90)."""
+    """Isoparametric Q2 geometry per (cell, Gauss point) (assembly.py:77-98):
+    G (nc,64,27,3), w (nc,64), Gpi = G.PI, and the node-major flattened
+    gradient tables Gt = G^(nc,27,64*3) and dGt = Gt - Gpi^ used by the
+    batched matrix products."""
     Q = QUAD
     X = coords[table]
-    J = np.einsum('qaj,cai->cqij', Q.dN, X)
+    J = np.einsum('qaj,cai->cqij', Q.dN, X, optimize=True)
     det = np.linalg.det(J)
     if np.any(det <= 0):
         raise ValueError("non-positive Jacobian in isoparametric map")
     Jinv = np.linalg.inv(J)
-    G = np.einsum('qaj,cqji->cqai', Q.dN, Jinv)
-    Gpi = np.einsum('cqbj,ba->cqaj', G, Q.PI)
-    return G, Q.wq[None, :] * det, Gpi
+    nc = X.shape[0]
+    G = np.ascontiguousarray(np.einsum('qaj,cqji->cqai', Q.dN, Jinv, optimize=True))
+    Gpi = np.ascontiguousarray(np.einsum('cqbj,ba->cqaj', G, Q.PI, optimize=True))
+    Gt = np.ascontiguousarray(G.transpose(0, 2, 1, 3)).reshape(nc, 27, 192)
+    dGt = Gt - np.ascontiguousarray(Gpi.transpose(0, 2, 1, 3)).reshape(nc, 27, 192)
+    return G, Q.wq[None, :] * det, Gpi, Gt, dGt
+
+
+def _chunks(n, size):
+    for s in range(0, n, size):
+        yield slice(s, min(n, s + size))
+
+
+class GeometryCache:
+    """Per-level geometry tables computed once, in chunks, like the reference's
+    Assembler.__init__ (assembly.py:65-108)."""
+
+    def __init__(self, coords, table, chunk=4096):
+        self.chunks = [(sl, cell_geometry(coords, table[sl]))
+                       for sl in _chunks(table.shape[0], chunk)]
 
 
 def stab_weights(x, table, h_T, nu, k, alpha0=0.02, delta0=0.1):
@@ -449,49 +472,71 @@ def stab_weights(x, table, h_T, nu, k, alpha0=0.02, delta0=0.1):
     return alpha0 / den, delta0 / den
 
 
-def element_vectors(x, coords, table, k, nu, alpha_T, delta_T, convection=True):
-    """Per-cell (cont (nc,27), mom (nc,27,3)) of A_h(x) (assembly.py:148-167, 212-240)."""
+def _at_q(loc):
+    """(nc,27,m) nodal values -> (nc,m,64) values at the Gauss points."""
+    return np.matmul(loc.transpose(0, 2, 1), QUAD.N.T)
+
+
+def _grad_at_q(loc, Gt):
+    """(nc,27,m) -> (nc,m,64,3) physical gradients."""
+    nc, _, m = loc.shape
+    return np.matmul(loc.transpose(0, 2, 1), Gt).reshape(nc, m, 64, 3)
+
+
+def element_vectors(x, geom, table, k, nu, alpha_T, delta_T, convection=True):
+    """Per-cell (cont (nc,27), mom (nc,27,3)) of A_h(x) (assembly.py:148-167, 212-240);
+    geom = cell_geometry of these cells.  Index order: fields (nc, comp, q[, j])."""
     Q = QUAD
-    G, w, Gpi = cell_geometry(coords, table)
+    G, w, Gpi, Gt, dGt = geom
+    nc = table.shape[0]
     loc = x.reshape(-1, 4)[table]
-    ph, vh = loc[:, :, 0], loc[:, :, 1:]
-    v = np.einsum('qa,cai->cqi', Q.N, vh)
-    gv = np.einsum('cai,cqaj->cqij', vh, G)
-    p = ph @ Q.N.T
-    gp = np.einsum('ca,cqaj->cqj', ph, G)
-    gpp = np.einsum('ca,cqaj->cqj', ph, Gpi)
-    conv = np.einsum('cqj,cqij->cqi', v, gv) if convection else np.zeros_like(v)
-    div = np.einsum('cqii->cq', gv)
-    mom = np.einsum('cq,cqi,qa->cai', w, v / k + 0.5 * conv, Q.N)
-    mom += 0.5 * nu * np.einsum('cq,cqij,cqaj->cai', w, gv, G)
-    mom -= np.einsum('cq,cq,cqai->cai', w, p, G)
-    cont = np.einsum('cq,cq,qa->ca', w, div, Q.N)
-    cont += alpha_T[:, None] * np.einsum('cq,cqj,cqaj->ca', w, gp - gpp, G - Gpi)
+    ph, vh = loc[:, :, :1], np.ascontiguousarray(loc[:, :, 1:])
+    v = _at_q(vh)                                  # (nc,3,64)
+    gv = _grad_at_q(vh, Gt)                        # (nc,3,64,3)  [c,i,q,j]
+    p = _at_q(ph)[:, 0]                            # (nc,64)
+    gp = _grad_at_q(ph, Gt)[:, 0]                  # (nc,64,3)
+    gpp = gp - _grad_at_q(ph, dGt)[:, 0]           # Gpi part: Gt - dGt
+    conv = np.einsum('cjq,ciqj->ciq', v, gv) if convection else np.zeros_like(v)
+    div = gv[:, 0, :, 0] + gv[:, 1, :, 1] + gv[:, 2, :, 2]
+    # momentum: mass/k + 1/2 convection (N test), 1/2 nu diffusion and pressure (G test)
+    mom = np.matmul(w[:, None, :] * (v / k + 0.5 * conv), Q.N)                   # (nc,3,27)
+    flux = 0.5 * nu * w[:, None, :, None] * gv                                  # [c,i,q,j]
+    flux[:, 0, :, 0] -= w * p
+    flux[:, 1, :, 1] -= w * p
+    flux[:, 2, :, 2] -= w * p
+    mom += np.matmul(Gt, flux.reshape(nc, 3, 192).transpose(0, 2, 1)).transpose(0, 2, 1)
+    # continuity: (div v, xi) + alpha (grad(p - pi p), grad(xi - pi xi))
+    cont = np.matmul(w * div, Q.N)
+    y = (alpha_T[:, None, None] * w[:, :, None] * (gp - gpp)).reshape(nc, 192, 1)
+    cont += np.matmul(dGt, y)[:, :, 0]
     use_delta = convection and delta_T is not None and np.any(delta_T != 0.0)
     if use_delta:
-        pvh = np.einsum('ba,cai->cbi', Q.PI, vh)
-        pv = np.einsum('qb,cbi->cqi', Q.N, pvh)
-        gpv = np.einsum('cbi,cqbj->cqij', pvh, G)
-        g = conv - np.einsum('cqj,cqij->cqi', pv, gpv)
-        S = np.einsum('cqj,cqaj->cqa', v, G) - np.einsum('cqj,cqaj->cqa', pv, Gpi)
-        mom += delta_T[:, None, None] * np.einsum('cq,cqi,cqa->cai', w, g, S)
-    return cont, mom
+        pvh = np.matmul(Q.PI, vh)                                               # (nc,27,3)
+        pv = _at_q(pvh)
+        gpv = _grad_at_q(pvh, Gt)
+        g = conv - np.einsum('cjq,ciqj->ciq', pv, gpv)
+        S = np.matmul(G, v.transpose(0, 2, 1)[:, :, :, None])[..., 0] \
+            - np.matmul(Gpi, pv.transpose(0, 2, 1)[:, :, :, None])[..., 0]        # (nc,64,27)
+        mom += np.matmul(delta_T[:, None, None] * w[:, None, :] * g, S)
+    return cont, mom.transpose(0, 2, 1)
 
 
-def rhs_vectors(x, coords, table, k, nu, f_old=None, f_new=None, convection=True):
+def rhs_vectors(x, geom, table, k, nu, f_old=None, f_new=None, convection=True):
     """Per-cell momentum rows of the next-step RHS (assembly.py:242-259)."""
     Q = QUAD
-    G, w, _ = cell_geometry(coords, table)
-    vh = x.reshape(-1, 4)[table][:, :, 1:]
-    v = np.einsum('qa,cai->cqi', Q.N, vh)
-    gv = np.einsum('cai,cqaj->cqij', vh, G)
-    acc = v / k - (0.5 * np.einsum('cqj,cqij->cqi', v, gv) if convection else 0.0)
+    G, w, _, Gt, _ = geom
+    nc = table.shape[0]
+    vh = np.ascontiguousarray(x.reshape(-1, 4)[table][:, :, 1:])
+    v = _at_q(vh)
+    gv = _grad_at_q(vh, Gt)
+    acc = v / k - (0.5 * np.einsum('cjq,ciqj->ciq', v, gv) if convection else 0.0)
     for fa in (f_old, f_new):
         if fa is not None:
-            acc = acc + 0.5 * np.einsum('qa,cai->cqi', Q.N, fa[table])
-    mom = np.einsum('cq,cqi,qa->cai', w, acc, Q.N)
-    mom -= 0.5 * nu * np.einsum('cq,cqij,cqaj->cai', w, gv, G)
-    return np.zeros(mom.shape[:2]), mom
+            acc = acc + 0.5 * _at_q(np.ascontiguousarray(fa[table]))
+    mom = np.matmul(w[:, None, :] * acc, Q.N)
+    flux = (0.5 * nu * w[:, None, :, None] * gv).reshape(nc, 3, 192)
+    mom -= np.matmul(Gt, flux.transpose(0, 2, 1)).transpose(0, 2, 1)
+    return np.zeros((nc, 27)), mom.transpose(0, 2, 1)
 
 
 def assemble(table, cont, mom, ndof):
@@ -501,16 +546,15 @@ def assemble(table, cont, mom, ndof):
     return np.bincount(dofs, weights=loc, minlength=ndof)
 
 
-def _chunks(n, size):
-    for s in range(0, n, size):
-        yield slice(s, min(n, s + size))
+def _geometry(coords, table, cache):
+    return cache if cache is not None else GeometryCache(coords, table)
 
 
-def residual(x, b_prev, coords, table, k, nu, alpha_T, delta_T, mask=None, chunk=4096):
+def residual(x, b_prev, coords, table, k, nu, alpha_T, delta_T, mask=None, cache=None):
     """r = b_prev - A_h(x), constrained rows zeroed (assembly.py:261-267)."""
     A = np.zeros(x.size)
-    for sl in _chunks(table.shape[0], chunk):
-        cont, mom = element_vectors(x, coords, table[sl], k, nu, alpha_T[sl], delta_T[sl])
+    for sl, geom in _geometry(coords, table, cache).chunks:
+        cont, mom = element_vectors(x, geom, table[sl], k, nu, alpha_T[sl], delta_T[sl])
         A += assemble(table[sl], cont, mom, x.size)
     r = b_prev - A
     if mask is not None:
@@ -518,11 +562,11 @@ def residual(x, b_prev, coords, table, k, nu, alpha_T, delta_T, mask=None, chunk
     return r
 
 
-def rhs_next(x, coords, table, k, nu, chunk=4096):
+def rhs_next(x, coords, table, k, nu, cache=None):
     """Next-step fine RHS with f = None (assembly.py:242-259)."""
     out = np.zeros(x.size)
-    for sl in _chunks(table.shape[0], chunk):
-        cont, mom = rhs_vectors(x, coords, table[sl], k, nu)
+    for sl, geom in _geometry(coords, table, cache).chunks:
+        cont, mom = rhs_vectors(x, geom, table[sl], k, nu)
         out += assemble(table[sl], cont, mom, x.size)
     return out
 
@@ -588,15 +632,18 @@ def correction_step(x_coarse, b_prev, ctx, model, t, nu, k, alpha0=0.02, delta0=
     xt = prolongate_state(ctx["P"], x_coarse)
     impose_dirichlet(xt, ctx["tags"], ctx["coords"], t, bcs)
     aT, dT = stab_weights(xt, ctx["table"], ctx["h_T"], nu, k, alpha0, delta0)
-    r = residual(xt, b_prev, ctx["coords"], ctx["table"], k, nu, aT, dT, ctx["mask"])
+    r = residual(xt, b_prev, ctx["coords"], ctx["table"], k, nu, aT, dT, ctx["mask"],
+                 cache=ctx.get("geometry"))
     X = network_input(xt, r, ctx["dof_table"], ctx["geom"])
     Y = mlp_forward(model, X)
     d = scatter_average(Y, ctx["dof_table"], ctx["mu"], ctx["mask"])
     return dict(x_tilde=xt, alpha_T=aT, delta_T=dT, r=r, X=X, Y=Y, d=d, x_corr=xt + scale * d)
 
 
-def build_context(lo, hi, n_cells, L, J, jitter_fn=None, channel_tags=False, bc_tags=(WALL,)):
-    """Hierarchy plus every index map the correction step needs."""
+def build_context(lo, hi, n_cells, L, J, jitter_fn=None, channel_tags=False, bc_tags=(WALL,),
+                  cache_geometry=False):
+    """Hierarchy plus every index map the correction step needs; cache_geometry
+    precomputes the per-level geometry once as the reference's Assembler does."""
     h = Hierarchy(lo, hi, n_cells, channel_tags)
     if jitter_fn is not None:
         jitter_fn(h.levels[0].verts)
@@ -610,4 +657,5 @@ def build_context(lo, hi, n_cells, L, J, jitter_fn=None, channel_tags=False, bc_
                 P=[prolongation_csr(h, l) for l in range(L, L + J)],
                 h_T=cell_diameters(h.levels[L + J]), dof_table=dof_table,
                 node_table=node_table, valence=valence, mu=mu, geom=geom,
-                coarse_coords=h.q2(L)[0])
+                coarse_coords=h.q2(L)[0],
+                geometry=GeometryCache(coords, table) if cache_geometry else None)

@@ -1,0 +1,195 @@
+// extern "C" entry points of libdnnmg_b200.so (declared in include/dnnmg_b200.h).
+#include <cstdarg>
+#include <cstring>
+#include "common.cuh"
+
+namespace dnnmg {
+
+static thread_local char g_last_error[512] = "";
+
+int32_t set_error(int32_t status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int32_t launch_prolongate(const dnnmg_prolong_t*, const float*, float*, const dnnmg_dirichlet_t*,
+                          cudaStream_t);
+int32_t launch_dirichlet(const dnnmg_dirichlet_t*, float*, cudaStream_t);
+int32_t launch_stab(const dnnmg_level_t*, const float*, const dnnmg_phys_t*, float*, float*,
+                    cudaStream_t);
+int32_t launch_residual(const dnnmg_level_t*, const float*, const float*, const float*,
+                        const float*, const dnnmg_phys_t*, float*, float*, int, int, cudaStream_t);
+int32_t launch_gather(const dnnmg_patchset_t*, const float*, const float*, float*, cudaStream_t);
+int32_t launch_restrict(const dnnmg_patchset_t*, const float*, float*, cudaStream_t);
+int32_t launch_extend(const dnnmg_patchset_t*, const float*, float*, cudaStream_t);
+int32_t launch_scatter_update(const dnnmg_patchset_t*, const float*, const uint8_t*, const float*,
+                              float, float*, float*, cudaStream_t);
+int32_t launch_mlp_simt(const dnnmg_mlp_t*, const float*, int64_t, float*, cudaStream_t);
+int32_t mlp_tc_supported(const dnnmg_mlp_t*);
+int32_t mlp_tc_packed_bytes(const dnnmg_mlp_t*, int64_t*);
+int32_t launch_mlp_tc_pack(const dnnmg_mlp_t*, void*, cudaStream_t);
+int32_t launch_mlp_tc(const dnnmg_mlp_t*, const float*, int64_t, float*, cudaStream_t);
+
+static int32_t check_mlp(const dnnmg_mlp_t* m) {
+  DNNMG_REQUIRE(m, DNNMG_ERR_ARG, "mlp: null model");
+  DNNMG_REQUIRE(m->depth >= 1 && m->depth < DNNMG_MAX_LAYERS, DNNMG_ERR_UNSUPPORTED,
+                "mlp: depth %d outside [1, %d)", m->depth, DNNMG_MAX_LAYERS);
+  DNNMG_REQUIRE(m->n_in > 0 && m->n_hidden > 0 && m->n_out > 0, DNNMG_ERR_ARG,
+                "mlp: non-positive width");
+  for (int i = 0; i <= m->depth; ++i)
+    DNNMG_REQUIRE(m->W[i], DNNMG_ERR_ARG, "mlp: W[%d] is NULL", i);
+  DNNMG_REQUIRE(m->bn_scale && m->bn_shift && m->in_mean && m->in_std, DNNMG_ERR_ARG,
+                "mlp: missing normalisation vectors");
+  return DNNMG_OK;
+}
+
+}  // namespace dnnmg
+
+using namespace dnnmg;
+
+extern "C" {
+
+int32_t dnnmg_version(void) { return 100; }
+
+const char* dnnmg_status_string(int32_t status) {
+  switch (status) {
+    case DNNMG_OK: return "ok";
+    case DNNMG_ERR_ARG: return "invalid argument";
+    case DNNMG_ERR_CUDA: return "CUDA error";
+    case DNNMG_ERR_UNSUPPORTED: return "unsupported configuration";
+    case DNNMG_ERR_ARCH: return "model architecture does not match the patch layout";
+    default: return "unknown status";
+  }
+}
+
+const char* dnnmg_last_error(void) { return g_last_error; }
+
+int32_t dnnmg_prolongate(const dnnmg_prolong_t* P, const float* xc, float* xf,
+                         const dnnmg_dirichlet_t* bc, dnnmg_stream_t s) {
+  return launch_prolongate(P, xc, xf, bc, as_stream(s));
+}
+
+int32_t dnnmg_apply_dirichlet(const dnnmg_dirichlet_t* bc, float* x, dnnmg_stream_t s) {
+  return launch_dirichlet(bc, x, as_stream(s));
+}
+
+int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph, float* aT,
+                   float* dT, dnnmg_stream_t s) {
+  return launch_stab(lv, x, ph, aT, dT, as_stream(s));
+}
+
+int32_t dnnmg_residual(const dnnmg_level_t* lv, const float* x, const float* b, const float* aT,
+                       const float* dT, const dnnmg_phys_t* ph, float* elem, float* r,
+                       int32_t apply_mask, dnnmg_stream_t s) {
+  return launch_residual(lv, x, b, aT, dT, ph, elem, r, apply_mask, 1, as_stream(s));
+}
+
+int32_t dnnmg_apply_operator(const dnnmg_level_t* lv, const float* x, const float* aT,
+                             const float* dT, const dnnmg_phys_t* ph, float* elem, float* out,
+                             dnnmg_stream_t s) {
+  return launch_residual(lv, x, nullptr, aT, dT, ph, elem, out, 0, 0, as_stream(s));
+}
+
+int32_t dnnmg_rhs_next(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph,
+                       float* elem, float* b, dnnmg_stream_t s) {
+  return launch_residual(lv, x, nullptr, nullptr, nullptr, ph, elem, b, 0, 2, as_stream(s));
+}
+
+int32_t dnnmg_gather(const dnnmg_patchset_t* ps, const float* x, const float* r, float* X,
+                     dnnmg_stream_t s) {
+  return launch_gather(ps, x, r, X, as_stream(s));
+}
+
+int32_t dnnmg_local_restrict(const dnnmg_patchset_t* ps, const float* x, float* rows,
+                             dnnmg_stream_t s) {
+  return launch_restrict(ps, x, rows, as_stream(s));
+}
+
+int32_t dnnmg_global_extend(const dnnmg_patchset_t* ps, const float* rows, float* out,
+                            dnnmg_stream_t s) {
+  return launch_extend(ps, rows, out, as_stream(s));
+}
+
+int32_t dnnmg_mlp_packed_bytes(const dnnmg_mlp_t* m, int64_t* bytes) {
+  int32_t st = check_mlp(m);
+  if (st) return st;
+  DNNMG_REQUIRE(bytes, DNNMG_ERR_ARG, "mlp_packed_bytes: null output");
+  if (m->precision == DNNMG_PREC_FP32) {
+    *bytes = 0;
+    return DNNMG_OK;
+  }
+  return mlp_tc_packed_bytes(m, bytes);
+}
+
+int32_t dnnmg_mlp_pack(const dnnmg_mlp_t* m, void* packed, dnnmg_stream_t s) {
+  int32_t st = check_mlp(m);
+  if (st) return st;
+  if (m->precision == DNNMG_PREC_FP32) return DNNMG_OK;
+  DNNMG_REQUIRE(packed, DNNMG_ERR_ARG, "mlp_pack: null buffer");
+  return launch_mlp_tc_pack(m, packed, as_stream(s));
+}
+
+int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
+                          dnnmg_stream_t s) {
+  int32_t st = check_mlp(m);
+  if (st) return st;
+  DNNMG_REQUIRE(X && Y, DNNMG_ERR_ARG, "mlp_forward: null argument");
+  DNNMG_REQUIRE(n_rows >= 0, DNNMG_ERR_ARG, "mlp_forward: negative row count");
+  if (n_rows == 0) return DNNMG_OK;
+  if (m->precision == DNNMG_PREC_FP32) return launch_mlp_simt(m, X, n_rows, Y, as_stream(s));
+  DNNMG_REQUIRE(m->packed, DNNMG_ERR_ARG, "mlp_forward: tensor-core mode needs packed weights");
+  DNNMG_REQUIRE(mlp_tc_supported(m), DNNMG_ERR_UNSUPPORTED,
+                "mlp_forward: tensor-core mode supports n_in <= 256, n_hidden == 256, n_out <= 256");
+  return launch_mlp_tc(m, X, n_rows, Y, as_stream(s));
+}
+
+int32_t dnnmg_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const uint8_t* mask,
+                             const float* xt, float scale, float* d, float* xc, dnnmg_stream_t s) {
+  return launch_scatter_update(ps, Y, mask, xt, scale, d, xc, as_stream(s));
+}
+
+int32_t dnnmg_correction_step_launches(int32_t J, const dnnmg_mlp_t* m) {
+  (void)m;
+  // J prolongations + element + node-sum + gather + mlp + scatter
+  return J + 5;
+}
+
+int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_dirichlet_t* bc,
+                              const dnnmg_level_t* fine, const dnnmg_phys_t* ph,
+                              const dnnmg_patchset_t* ps, const dnnmg_mlp_t* m,
+                              const float* x_coarse, const float* b_prev, float scale,
+                              const dnnmg_step_buffers_t* buf, float* x_corr, dnnmg_stream_t s) {
+  DNNMG_REQUIRE(P && fine && ph && ps && m && buf && x_coarse && b_prev && x_corr, DNNMG_ERR_ARG,
+                "correction_step: null argument");
+  DNNMG_REQUIRE(J == 1 || J == 2, DNNMG_ERR_ARG, "correction_step: unsupported patch depth J=%d", J);
+  DNNMG_REQUIRE(J == 1 || buf->x_mid, DNNMG_ERR_ARG, "correction_step: J=2 needs x_mid");
+  const int npp = ps->nodes_per_patch;
+  DNNMG_REQUIRE(m->n_in == 8 * npp + ps->n_geo && m->n_out == 3 * npp, DNNMG_ERR_ARCH,
+                "model architecture (%d -> %d) does not match the patch layout (%d -> %d)",
+                m->n_in, m->n_out, 8 * npp + ps->n_geo, 3 * npp);
+  cudaStream_t st = as_stream(s);
+  int32_t rc;
+  // (1) prolongate to L+J, (2) re-impose Dirichlet data on the fine level (driver.py:251-253)
+  if (J == 1) {
+    rc = launch_prolongate(&P[0], x_coarse, buf->x_tilde, bc, st);
+  } else {
+    rc = launch_prolongate(&P[0], x_coarse, buf->x_mid, nullptr, st);
+    if (!rc) rc = launch_prolongate(&P[1], buf->x_mid, buf->x_tilde, bc, st);
+  }
+  if (rc) return rc;
+  // (3) stab at x~ + residual against the carried RHS, masked (driver.py:255-258)
+  rc = launch_residual(fine, buf->x_tilde, b_prev, nullptr, nullptr, ph, buf->elem, buf->r, 1, 1,
+                       st);
+  if (rc) return rc;
+  // (4) patch features, network, averaging scatter, update (driver.py:263-268)
+  rc = launch_gather(ps, buf->x_tilde, buf->r, buf->X, st);
+  if (rc) return rc;
+  rc = dnnmg_mlp_forward(m, buf->X, ps->n_patches, buf->Y, s);
+  if (rc) return rc;
+  return launch_scatter_update(ps, buf->Y, fine->dof_mask, buf->x_tilde, scale, buf->d, x_corr, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+"""Device-resident index tables and the thin calls into libdnnmg_b200.
+
+PyTorch is used only as plumbing here: CUDA memory, the current stream and
+host<->device copies.  Every arithmetic operation on the correction path is a
+kernel of libdnnmg_b200.so called through its C ABI (``_lib``); there is no
+PyTorch or numpy fallback, and a missing library or GPU raises.
+
+Tables are uploaded once per host object (hierarchy level, PatchSet, model)
+and cached on that object, so repeated API calls only move the vectors.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+ALPHA0, DELTA0 = 0.02, 0.1
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2307_14837_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def f32(x):
+    """numpy / torch -> contiguous float32 CUDA tensor."""
+    dev = device()
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+
+
+def upload(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(device())
+
+
+def like_input(t, ref):
+    """Return a device result in the caller's convention: numpy float64 for numpy
+    inputs (the reference's dtype), the CUDA tensor otherwise."""
+    if isinstance(ref, torch.Tensor):
+        return t
+    return t.double().cpu().numpy()
+
+
+def _cache(obj, key):
+    store = obj.__dict__.setdefault("_b200_device", {})
+    return store, key
+
+
+def node_csr(table):
+    """CSR node -> flat (row*width + slot) entries, rows ascending per node."""
+    flat = np.asarray(table, dtype=np.int64).reshape(-1)
+    order = np.argsort(flat, kind="stable")
+    counts = np.bincount(flat, minlength=int(flat.max()) + 1 if flat.size else 0)
+    ptr_ = np.zeros(counts.size + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr_[1:])
+    return ptr_, order
+
+
+def dof_mask_bits(mask, n_nodes):
+    """bool dof mask -> per-node bit field (bit c <=> dof 4n+c constrained)."""
+    if mask is None:
+        return None
+    m = np.asarray(mask, dtype=bool).reshape(n_nodes, 4)
+    return (m.astype(np.uint8) * np.array([1, 2, 4, 8], dtype=np.uint8)).sum(1).astype(np.uint8)
+
+
+def cell_diameters(vertices, cells, chunk=1 << 16):
+    """h_T = largest distance between two cell corners (assembly.py:99-103)."""
+    out = np.empty(cells.shape[0])
+    for s in range(0, cells.shape[0], chunk):
+        C = vertices[cells[s:s + chunk]]
+        d2 = ((C[:, :, None, :] - C[:, None, :, :]) ** 2).sum(-1)
+        out[s:s + chunk] = np.sqrt(d2.max(axis=(1, 2)))
+    return out
+
+
+class DeviceProlong:
+    """K1 tables for level -> level+1."""
+
+    def __init__(self, hierarchy, level):
+        from .space import prolongation_source
+        _, ctab = hierarchy.scalar_nodes(level)
+        src = prolongation_source(hierarchy, level)
+        self.ctab = upload(ctab, np.int32)
+        self.src = upload(src, np.int32)
+        self.n_fine = int(src.size)
+        self.n_coarse_nodes = int(hierarchy.scalar_nodes(level)[0].shape[0])
+        self.struct = _lib.Prolong(self.n_fine, int(ctab.shape[0]), ptr(self.ctab), ptr(self.src))
+
+    @staticmethod
+    def get(hierarchy, level):
+        store, key = _cache(hierarchy, ("prolong", level))
+        if key not in store:
+            store[key] = DeviceProlong(hierarchy, level)
+        return store[key]
+
+
+class DeviceLevel:
+    """K2 tables of one level: cell nodes, fp64 coordinates, h_T, node->cell CSR."""
+
+    def __init__(self, space):
+        h = space.hierarchy
+        lvl = h.levels[space.level]
+        self.n_nodes = int(space.n_nodes)
+        self.n_cells = int(space.cell_nodes.shape[0])
+        self.cell_nodes = upload(space.cell_nodes, np.int32)
+        self.coords = upload(space.nodes, np.float64)
+        self.h_T_host = cell_diameters(lvl.vertices, lvl.cells)
+        self.h_T = upload(self.h_T_host, np.float32)
+        p, idx = node_csr(space.cell_nodes)
+        self.csr_ptr = upload(p, np.int32)
+        self.csr_idx = upload(idx, np.int32)
+        self.elem = None
+
+    def struct(self, dof_mask=None):
+        return _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
+                          ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask))
+
+    def scratch(self):
+        if self.elem is None:
+            self.elem = torch.empty(self.n_cells * 27 * 4, dtype=torch.float32, device=device())
+        return self.elem
+
+    @staticmethod
+    def get(space):
+        store, key = _cache(space.hierarchy, ("level", space.level))
+        if key not in store:
+            store[key] = DeviceLevel(space)
+        return store[key]
+
+
+class DevicePatchSet:
+    """K3/K5 tables: node table, geometry rows, node->(patch, slot) CSR."""
+
+    def __init__(self, ps):
+        self.n_patches = int(ps.node_table.shape[0])
+        self.npp = int(ps.nodes_per_patch)
+        self.n_geo = int(ps.n_geo)
+        self.n_nodes = int(ps.mu.shape[0] // 4)
+        self.node_table = upload(ps.node_table, np.int32)
+        self.geom = upload(ps.geom_table, np.float32)
+        p, idx = node_csr(ps.node_table)
+        if p.size - 1 != self.n_nodes:
+            raise RuntimeError("patch union does not cover the fine level")
+        self.csr_ptr = upload(p, np.int32)
+        self.csr_idx = upload(idx, np.int32)
+        self.struct = _lib.PatchSet(self.n_patches, self.npp, self.n_geo, self.n_nodes,
+                                    ptr(self.node_table), ptr(self.geom), ptr(self.csr_ptr),
+                                    ptr(self.csr_idx))
+
+    @staticmethod
+    def get(ps):
+        store, key = _cache(ps, "patchset")
+        if key not in store:
+            store[key] = DevicePatchSet(ps)
+        return store[key]
+
+
+class DeviceModel:
+    """Eval-mode MlpModel on the device (net.py:54-159), BN folded to scale/shift."""
+
+    def __init__(self, model, precision="fp32"):
+        arch = model.arch
+        self.arch = arch
+        self.precision = precision
+        self.W = [f32(np.asarray(w, dtype=np.float64)) for w in model.W]
+        scale, shift = [], []
+        for i in range(arch.depth):
+            s = np.asarray(model.gamma[i], float) / np.sqrt(np.asarray(model.running_var[i], float)
+                                                            + model.bn_eps)
+            scale.append(s)
+            shift.append(np.asarray(model.beta[i], float) - np.asarray(model.running_mean[i], float) * s)
+        self.scale = f32(np.concatenate(scale))
+        self.shift = f32(np.concatenate(shift))
+        self.in_mean = f32(np.asarray(model.input_mean, float))
+        self.in_std = f32(np.asarray(model.input_std, float))
+        Ws = (ctypes.c_void_p * _lib.MAX_LAYERS)(*([w.data_ptr() for w in self.W]
+                                                  + [0] * (_lib.MAX_LAYERS - len(self.W))))
+        act = _lib.ACT_TANH if model.activation == "tanh" else _lib.ACT_RELU
+        self.struct = _lib.Mlp(arch.n_in, arch.n_hidden, arch.depth, arch.n_out, act,
+                               _lib.PRECISIONS[precision], Ws, ptr(self.scale), ptr(self.shift),
+                               ptr(self.in_mean), ptr(self.in_std), None)
+        self.packed = None
+        if precision != "fp32":
+            nbytes = ctypes.c_int64(0)
+            _lib.call("dnnmg_mlp_packed_bytes", ctypes.byref(self.struct), ctypes.byref(nbytes))
+            self.packed = torch.empty(max(int(nbytes.value), 16), dtype=torch.uint8, device=device())
+            self.struct.packed = ptr(self.packed)
+            _lib.call("dnnmg_mlp_pack", ctypes.byref(self.struct), ptr(self.packed), stream_handle())
+
+    def forward(self, X, n_rows, Y):
+        _lib.call("dnnmg_mlp_forward", ctypes.byref(self.struct), ptr(X), int(n_rows), ptr(Y),
+                  stream_handle())
+
+
+def dirichlet_codes(space, t, bcs):
+    """(bc_code uint8 [n], bc_values float32 [n,3] or None) of apply_dirichlet at t."""
+    code = np.zeros(space.n_nodes, dtype=np.uint8)
+    vals = None
+    for tag, fn in bcs.items():
+        nodes = space.nodes_with_tag(tag)
+        if nodes.size == 0 or fn is None:
+            continue
+        v = np.asarray(fn(t, space.nodes[nodes]), dtype=float).reshape(nodes.size, 3)
+        if not np.any(v):
+            code[nodes] = 1
+        else:
+            if vals is None:
+                vals = np.zeros((space.n_nodes, 3), dtype=np.float32)
+            code[nodes] = 2
+            vals[nodes] = v
+    return code, vals
+
+
+class DeviceDirichlet:
+    def __init__(self, space, t, bcs):
+        code, vals = dirichlet_codes(space, t, bcs)
+        self.code = upload(code, np.uint8)
+        self.vals = None if vals is None else upload(vals, np.float32)
+        self.struct = _lib.Dirichlet(int(space.n_nodes), ptr(self.code), ptr(self.vals))
+
+
+# ---- reference-API operations -----------------------------------------------------------
+
+def prolongate_state(hierarchy, x, levels_up=1):
+    from .space import StateVector
+    v = f32(x.values)
+    lvl = x.level
+    for _ in range(levels_up):
+        P = DeviceProlong.get(hierarchy, lvl)
+        if v.numel() != 4 * P.n_coarse_nodes:
+            raise ValueError(f"vector length {v.numel()} does not match level {lvl} "
+                             f"({4 * P.n_coarse_nodes} dofs)")
+        out = torch.empty(4 * P.n_fine, dtype=torch.float32, device=v.device)
+        _lib.call("dnnmg_prolongate", ctypes.byref(P.struct), ptr(v), ptr(out), None,
+                  stream_handle())
+        v = out
+        lvl += 1
+    return StateVector(lvl, like_input(v, x.values), x.time)
+
+
+def apply_dirichlet_state(space, x, t, bcs):
+    bc = DeviceDirichlet(space, t, bcs)
+    if isinstance(x.values, torch.Tensor) and x.values.is_cuda and x.values.dtype == torch.float32 \
+            and x.values.is_contiguous():
+        _lib.call("dnnmg_apply_dirichlet", ctypes.byref(bc.struct), ptr(x.values), stream_handle())
+        return x
+    v = f32(x.values)
+    _lib.call("dnnmg_apply_dirichlet", ctypes.byref(bc.struct), ptr(v), stream_handle())
+    touched = torch.nonzero(bc.code).reshape(-1)
+    rows = v.reshape(-1, 4)[touched]
+    if isinstance(x.values, np.ndarray):
+        # only the constrained rows change; untouched entries keep their float64 values
+        x.values.reshape(-1, 4)[touched.cpu().numpy()] = rows.double().cpu().numpy()
+    else:
+        x.values.reshape(-1, 4)[touched.to(x.values.device)] = rows.to(x.values.dtype)
+    return x

@@ -1,0 +1,168 @@
+"""The fused fine-level correction step on device-resident data.
+
+``CorrectionStep`` is the production form of ``driver.TimeLoop._step_hybrid``
+lines 251-268 (prolongate -> Dirichlet -> stab -> residual -> gather -> MLP ->
+scatter-average -> x~ + scale*d): all tables, weights and work buffers live in
+HBM, one call issues the whole K1..K5 sequence through the single C-ABI entry
+``dnnmg_correction_step`` on the current stream (no host synchronisation, no
+allocation), and the sequence can be captured into a CUDA graph.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib, device as dv, mesh as meshmod
+from .patch_ops import check_model, input_width, output_width
+from .space import FeSpace, no_slip
+
+
+def constrained_mask(space, bcs):
+    """Dirichlet velocity dofs plus the pressure pin at dof 0 when there is no
+    outflow boundary (driver.py:56-65)."""
+    m = space.dirichlet_mask(tuple(bcs.keys()))
+    if not space.has_outflow:
+        m[0] = True
+    return m
+
+
+class CorrectionStep:
+    def __init__(self, hierarchy, L, J, model, nu, k, bcs=None, alpha0=0.02, delta0=0.1,
+                 scale=1.0, precision="fp32", patchset=None, t=0.0):
+        self.hierarchy, self.L, self.J = hierarchy, L, J
+        self.bcs = bcs if bcs is not None else {meshmod.WALL: no_slip}
+        self.scale = float(scale)
+        self.nu, self.k = nu, k
+        self.space = FeSpace(hierarchy, L + J)
+        self.coarse_ndof = 4 * hierarchy.scalar_nodes(L)[0].shape[0]
+        self.prolongs = [dv.DeviceProlong.get(hierarchy, l) for l in range(L, L + J)]
+        self.P = (_lib.Prolong * J)(*[p.struct for p in self.prolongs])
+        self.level = dv.DeviceLevel.get(self.space)
+        self.mask = constrained_mask(self.space, self.bcs)
+        self.mask_bits = dv.upload(dv.dof_mask_bits(self.mask, self.space.n_nodes), np.uint8)
+        self.lv = self.level.struct(self.mask_bits)
+        self.patchset = patchset if patchset is not None else meshmod.build_patches(hierarchy, L, J)
+        check_model(model, self.patchset)
+        self.ps = dv.DevicePatchSet.get(self.patchset)
+        self.precision = precision
+        self.model = dv.DeviceModel(model, precision)
+        self.phys = _lib.Phys(float(nu), float(k), float(alpha0), float(delta0), 1)
+        dev = dv.device()
+        nf = self.space.n_nodes
+        f = torch.float32
+        self.x_tilde = torch.empty(4 * nf, dtype=f, device=dev)
+        self.r = torch.empty(4 * nf, dtype=f, device=dev)
+        self.d = torch.empty(4 * nf, dtype=f, device=dev)
+        self.x_corr = torch.empty(4 * nf, dtype=f, device=dev)
+        self.elem = self.level.scratch()
+        self.X = torch.empty((self.ps.n_patches, input_width(self.patchset)), dtype=f, device=dev)
+        self.Y = torch.empty((self.ps.n_patches, output_width(self.patchset)), dtype=f, device=dev)
+        self.x_mid = (torch.empty(4 * self.prolongs[0].n_fine, dtype=f, device=dev)
+                      if J == 2 else None)
+        self.buf = _lib.StepBuffers(dv.ptr(self.x_tilde), dv.ptr(self.r), dv.ptr(self.elem),
+                                    dv.ptr(self.X), dv.ptr(self.Y), dv.ptr(self.d),
+                                    dv.ptr(self.x_mid))
+        self._t = None
+        self.set_time(t)
+        self.graph = None
+
+    # Dirichlet data are re-evaluated only when they depend on t
+    def set_time(self, t):
+        code, vals = dv.dirichlet_codes(self.space, t, self.bcs)
+        if self._t is not None and vals is None and self._static:
+            return
+        self._static = vals is None
+        self.bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
+        self.bc.code = dv.upload(code, np.uint8)
+        self.bc.vals = None if vals is None else dv.upload(vals, np.float32)
+        self.bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(self.bc.code), dv.ptr(self.bc.vals))
+        self._t = t
+
+    @property
+    def n_patches(self):
+        return self.ps.n_patches
+
+    @property
+    def launches(self):
+        return int(_lib.load().dnnmg_correction_step_launches(self.J, ctypes.byref(self.model.struct)))
+
+    def run(self, x_coarse, b_prev, x_corr=None):
+        """Issue one correction step; all arguments are fp32 CUDA tensors."""
+        out = self.x_corr if x_corr is None else x_corr
+        if x_coarse.numel() != self.coarse_ndof or b_prev.numel() != self.x_tilde.numel():
+            raise ValueError("vector length does not match the coarse / fine level")
+        _lib.call("dnnmg_correction_step", self.P, self.J, ctypes.byref(self.bc.struct),
+                  ctypes.byref(self.lv), ctypes.byref(self.phys), ctypes.byref(self.ps.struct),
+                  ctypes.byref(self.model.struct), dv.ptr(x_coarse), dv.ptr(b_prev),
+                  ctypes.c_float(self.scale), ctypes.byref(self.buf), dv.ptr(out),
+                  dv.stream_handle())
+        return out
+
+    __call__ = run
+
+    def run_staged(self, x_coarse, b_prev, x_corr=None, events=None):
+        """The same kernel sequence as run(), issued stage by stage through the
+        per-kernel C-ABI entries so that CUDA events can bracket each stage
+        (events: list of J+5 torch.cuda.Event, recorded on the current stream)."""
+        out = self.x_corr if x_corr is None else x_corr
+        s = dv.stream_handle()
+        e = iter(events) if events is not None else None
+
+        def mark():
+            if e is not None:
+                next(e).record()
+        mark()
+        cur = x_coarse
+        for i, P in enumerate(self.prolongs):
+            dst = self.x_tilde if i == self.J - 1 else self.x_mid
+            bc = ctypes.byref(self.bc.struct) if i == self.J - 1 else None
+            _lib.call("dnnmg_prolongate", ctypes.byref(P.struct), dv.ptr(cur), dv.ptr(dst), bc, s)
+            cur = dst
+            mark()
+        _lib.call("dnnmg_residual", ctypes.byref(self.lv), dv.ptr(self.x_tilde), dv.ptr(b_prev),
+                  None, None, ctypes.byref(self.phys), dv.ptr(self.elem), dv.ptr(self.r), 1, s)
+        mark()
+        _lib.call("dnnmg_gather", ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde),
+                  dv.ptr(self.r), dv.ptr(self.X), s)
+        mark()
+        _lib.call("dnnmg_mlp_forward", ctypes.byref(self.model.struct), dv.ptr(self.X),
+                  self.ps.n_patches, dv.ptr(self.Y), s)
+        mark()
+        _lib.call("dnnmg_scatter_update", ctypes.byref(self.ps.struct), dv.ptr(self.Y),
+                  dv.ptr(self.mask_bits), dv.ptr(self.x_tilde), ctypes.c_float(self.scale),
+                  dv.ptr(self.d), dv.ptr(out), s)
+        mark()
+        return out
+
+    def capture(self, x_coarse, b_prev):
+        """Capture run(x_coarse, b_prev) into a CUDA graph (inputs are fixed buffers)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.run(x_coarse, b_prev)            # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(x_coarse, b_prev)
+        self.graph = g
+        return g
+
+    def rhs_next(self, x, out=None):
+        """Next-step fine RHS from a (corrected) fine state (assembly.py:242-259)."""
+        out = torch.empty_like(self.x_tilde) if out is None else out
+        lv = self.level.struct()
+        _lib.call("dnnmg_rhs_next", ctypes.byref(lv), dv.ptr(x), ctypes.byref(self.phys),
+                  dv.ptr(self.elem), dv.ptr(out), dv.stream_handle())
+        return out
+
+    def embed(self, x_coarse, t=None):
+        """Prolongate + Dirichlet only (driver.embed_state, driver.py:611-619)."""
+        cur = dv.f32(x_coarse)
+        for i, P in enumerate(self.prolongs):
+            out = torch.empty(4 * P.n_fine, dtype=torch.float32, device=cur.device)
+            bc = ctypes.byref(self.bc.struct) if i == self.J - 1 else None
+            _lib.call("dnnmg_prolongate", ctypes.byref(P.struct), dv.ptr(cur), dv.ptr(out), bc,
+                      dv.stream_handle())
+            cur = out
+        return cur

@@ -35,3 +35,47 @@ def oracle_model(g):
                    running_mean=[g[f"rmean{i}"] for i in range(depth)],
                    running_var=[g[f"rvar{i}"] for i in range(depth)],
                    input_mean=g["input_mean"], input_std=g["input_std"])
+
+
+def load_golden(name):
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"{name}.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+def product_hierarchy(g):
+    """Build the same (jittered) hierarchy with the product's mesh module."""
+    from paper_2307_14837_b200 import mesh
+    n_cells = tuple(int(v) for v in g["n_cells"])
+    h = mesh.build_template_mesh("box", extent_lo=g["lo"], extent_hi=g["hi"], n_cells=n_cells,
+                                 channel_tags=bool(int(g["channel"])))
+    if int(g["jitter"]) >= 0:
+        synthetic.jitter_vertices(h.levels[0].vertices, n_cells, g["lo"], g["hi"], int(g["jitter"]))
+    for _ in range(int(g["L"]) + int(g["J"])):
+        mesh.refine_uniform(h)
+    return h
+
+
+def product_model(g):
+    """The golden case's eval-mode model as this package's MlpModel."""
+    from paper_2307_14837_b200.net import Architecture, MlpModel
+    n = int(g["n_layers"])
+    depth = n - 1
+    W = [g[f"W{i}"].astype(np.float64) for i in range(n)]
+    m = MlpModel(Architecture(W[0].shape[0], W[0].shape[1], depth, W[-1].shape[1]),
+                 activation=str(g["act"]))
+    m.W = W
+    m.gamma = [g[f"gamma{i}"] for i in range(depth)]
+    m.beta = [g[f"beta{i}"] for i in range(depth)]
+    m.running_mean = [g[f"rmean{i}"] for i in range(depth)]
+    m.running_var = [g[f"rvar{i}"] for i in range(depth)]
+    m.input_mean, m.input_std = g["input_mean"], g["input_std"]
+    return m.eval()
+
+
+def product_bcs(g):
+    from paper_2307_14837_b200 import mesh, space
+    if int(g["channel"]):
+        return {mesh.INFLOW: space.inflow_profile(3, 1.0, 0.41), mesh.WALL: space.no_slip}
+    return {mesh.WALL: space.no_slip}

@@ -1,0 +1,204 @@
+"""GPU parity: every kernel of the correction path against the reference's own
+golden output (tests/golden, produced by running dnnmg) and the reference's
+property tests, through the product's drop-in API and the C ABI.
+
+Tolerances (relative L2 against the float64 reference):
+  index maps / gathers: exact (fp32 rounding of the same values)
+  x~ (prolongation, dyadic weights): 1e-7
+  r (residual, fp32 with cancellation b - A): 2e-5
+  Y, d, x_corr in fp32 mode: 1e-5 (north-star gate)
+"""
+import copy
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES
+from golden_util import load_golden, product_hierarchy, product_model, product_bcs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2307_14837_b200 import mesh as meshmod, space as spmod, patch_ops, net  # noqa: E402
+from paper_2307_14837_b200.assembly import Assembler, StabParams  # noqa: E402
+from paper_2307_14837_b200.step import CorrectionStep, constrained_mask  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module", params=GOLDEN_CASES)
+def case(request):
+    g = load_golden(request.param)
+    h = product_hierarchy(g)
+    L, J = int(g["L"]), int(g["J"])
+    s = spmod.FeSpace(h, L + J)
+    ps = meshmod.build_patches(h, L, J)
+    return request.param, g, h, s, ps
+
+
+def test_prolongate_and_dirichlet(case):
+    name, g, h, s, ps = case
+    L, J = int(g["L"]), int(g["J"])
+    xt = spmod.prolongate(h, spmod.StateVector(L, g["x_coarse"].copy()), J)
+    assert xt.level == L + J
+    spmod.apply_dirichlet(s, xt, float(g["t"]), product_bcs(g))
+    assert rel(xt.values, g["x_tilde"]) < 1e-7
+
+
+def test_stab(case):
+    name, g, h, s, ps = case
+    st = Assembler(s).stab(g["x_tilde"], float(g["nu"]), float(g["k"]))
+    assert rel(st.alpha_T, g["alpha_T"]) < 1e-6
+    assert rel(st.delta_T, g["delta_T"]) < 1e-6
+
+
+def test_residual(case):
+    name, g, h, s, ps = case
+    asm = Assembler(s)
+    st = StabParams(float(g["alpha0"]), float(g["delta0"]), g["alpha_T"], g["delta_T"])
+    r = asm.assemble_residual(g["x_tilde"], g["b_prev"], float(g["k"]), float(g["nu"]), st,
+                              mask=g["mask"])
+    assert rel(r, g["r"]) < 2e-5, rel(r, g["r"])
+    assert np.all(r[g["mask"]] == 0.0)
+    # stab evaluated inside the kernel (alpha_T = None) gives the same residual
+    r2 = asm.assemble_residual(g["x_tilde"], g["b_prev"], float(g["k"]), float(g["nu"]),
+                               StabParams(), mask=g["mask"])
+    assert rel(r2, g["r"]) < 2e-5
+
+
+def test_rhs_next(case):
+    name, g, h, s, ps = case
+    b = Assembler(s).assemble_rhs_next(g["x_corr"], None, None, float(g["k"]), float(g["nu"]))
+    assert rel(b, g["b_next"]) < 2e-6, rel(b, g["b_next"])
+
+
+def test_network_input_exact(case):
+    name, g, h, s, ps = case
+    X = patch_ops.assemble_network_input(g["x_tilde"], g["r"], ps)
+    assert np.array_equal(X, g["X"].astype(np.float32).astype(np.float64))
+
+
+def test_forward_fp32(case):
+    name, g, h, s, ps = case
+    Y = net.forward(product_model(g), g["X"], precision="fp32")
+    assert rel(Y, g["Y"]) < 1e-5, rel(Y, g["Y"])
+
+
+def test_predict_correction_fp32(case):
+    name, g, h, s, ps = case
+    d = patch_ops.predict_correction(product_model(g), g["x_tilde"], g["r"], ps,
+                                     dirichlet_mask=g["mask"], precision="fp32")
+    assert rel(d, g["d"]) < 1e-5, rel(d, g["d"])
+    assert np.all(d.reshape(-1, 4)[:, 0] == 0.0)
+    assert np.all(d[g["mask"]] == 0.0)
+
+
+def test_fused_step_fp32(case):
+    name, g, h, s, ps = case
+    L, J = int(g["L"]), int(g["J"])
+    step = CorrectionStep(h, L, J, product_model(g), float(g["nu"]), float(g["k"]),
+                          bcs=product_bcs(g), scale=float(g["scale"]), precision="fp32",
+                          patchset=ps, t=float(g["t"]))
+    xc = torch.tensor(g["x_coarse"], dtype=torch.float32, device="cuda")
+    b = torch.tensor(g["b_prev"], dtype=torch.float32, device="cuda")
+    out = step(xc, b).double().cpu().numpy()
+    torch.cuda.synchronize()
+    assert rel(step.x_tilde.cpu().numpy(), g["x_tilde"]) < 1e-7
+    assert rel(step.r.cpu().numpy(), g["r"]) < 2e-5
+    assert rel(step.d.cpu().numpy(), g["d"]) < 1e-5
+    assert rel(out, g["x_corr"]) < 1e-5
+    # deterministic: a second run is bitwise identical
+    out2 = step(xc, b).double().cpu().numpy()
+    assert np.array_equal(out, out2)
+
+
+# ---- reference property tests (test_patch_ops.py) on the GPU -------------------------
+
+@pytest.fixture(scope="module")
+def ps3():
+    h = meshmod.build_template_mesh("box", extent_lo=(0, 0, 0), extent_hi=(1, 1, 1), n_cells=(3, 2, 2))
+    meshmod.refine_uniform(h)
+    return meshmod.build_patches(h, 0, 1)
+
+
+def test_local_restrict_is_pure_gather(ps3):
+    n = ps3.mu.shape[0]
+    rows = patch_ops.local_restrict(np.arange(n, dtype=float), ps3)
+    assert np.array_equal(rows, ps3.dof_table.astype(float))
+    assert np.all(patch_ops.local_restrict(np.full(n, 3.25), ps3) == 3.25)
+    with pytest.raises(ValueError, match="length"):
+        patch_ops.local_restrict(np.zeros(n + 1), ps3)
+
+
+def test_extend_restrict_identity(ps3):
+    x = np.random.default_rng(3).standard_normal(ps3.mu.shape[0]).astype(np.float32)
+    back = patch_ops.global_extend(patch_ops.local_restrict(x, ps3), ps3)
+    assert np.abs(back - x).max() < 1e-6
+
+
+def test_shared_dof_average(ps3):
+    dof = int(np.nonzero(1.0 / ps3.mu >= 2)[0][0])
+    owners = np.nonzero((ps3.dof_table == dof).any(axis=1))[0]
+    rows = np.zeros((len(ps3), ps3.ndof_patch))
+    slot = np.nonzero(ps3.dof_table[owners[0]] == dof)[0][0]
+    rows[owners[0], slot] = 5.0
+    out = patch_ops.global_extend(rows, ps3)
+    assert out[dof] == pytest.approx(5.0 / owners.size, rel=1e-7)
+
+
+def _model(ps, seed, hidden=12, depth=2):
+    return net.MlpModel(net.Architecture(patch_ops.input_width(ps), hidden, depth,
+                                         patch_ops.output_width(ps)), seed=seed).eval()
+
+
+def test_zero_weight_model_zero_defect(ps3):
+    m = net.zero_weights(_model(ps3, 0))
+    rng = np.random.default_rng(1)
+    n = ps3.mu.shape[0]
+    d = patch_ops.predict_correction(m, rng.standard_normal(n), rng.standard_normal(n), ps3)
+    assert np.all(d == 0.0)
+
+
+def test_permutation_invariance(ps3):
+    m = _model(ps3, 3)
+    rng = np.random.default_rng(2)
+    n = ps3.mu.shape[0]
+    xt, r = rng.standard_normal(n), rng.standard_normal(n)
+    d1 = patch_ops.predict_correction(m, xt, r, ps3)
+    assert np.abs(d1).max() > 0 and np.all(d1.reshape(-1, 4)[:, 0] == 0.0)
+    perm = rng.permutation(len(ps3))
+    sh = copy.copy(ps3)
+    sh.__dict__ = {k: v for k, v in ps3.__dict__.items() if k != "_b200_device"}
+    sh.dof_table = ps3.dof_table[perm]
+    sh.node_table = ps3.node_table[perm]
+    sh.geom_table = ps3.geom_table[perm]
+    d2 = patch_ops.predict_correction(m, xt, r, sh)
+    assert np.abs(d1 - d2).max() < 1e-5 * np.abs(d1).max()
+
+
+def test_model_patch_mismatch_rejected(ps3):
+    n = ps3.mu.shape[0]
+    bad = net.MlpModel(net.Architecture(10, 8, 2, 4), seed=0).eval()
+    with pytest.raises(ValueError, match="architecture"):
+        patch_ops.predict_correction(bad, np.zeros(n), np.zeros(n), ps3)
+    tr = _model(ps3, 0).train()
+    with pytest.raises(ValueError, match="eval"):
+        patch_ops.predict_correction(tr, np.zeros(n), np.zeros(n), ps3)
+
+
+def test_zero_state_zero_residual(ps3):
+    """test_assembly.py:31-37 on the GPU."""
+    h = ps3.hierarchy
+    s = spmod.FeSpace(h, 1)
+    asm = Assembler(s)
+    x = np.zeros(s.ndof)
+    st = asm.stab(x, 1e-2, 0.1)
+    r = asm.assemble_residual(x, np.zeros_like(x), 0.1, 1e-2, st, mask=s.dirichlet_mask())
+    assert np.all(r == 0.0)

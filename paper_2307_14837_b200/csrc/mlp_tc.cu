@@ -1,11 +1,529 @@
-// K4 fast path: tcgen05 / TMEM patch MLP (placeholder until the kernel lands).
+// K4 fast path: the patch MLP on 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Reference: net._forward eval branch (net.py:124-159):
+//   h0 = (X - mean)/std; layer i: z = h W_i, a = act(z*scale_i + shift_i) (BN folded),
+//   h_{i+1} = a (+ h_i for i >= 1); head Y = h_depth W_depth.
+//
+// One persistent CTA per SM processes 128-row tiles.  Warp roles (320 threads):
+//   warps 0..7  compute: stage the layer-0 A operand from X (input normalisation),
+//               run every epilogue (TMEM -> registers -> BN/activation/skip) and
+//               write the next GEMM's A operand into the SMEM ring chunk by chunk;
+//               the fp32 skip state h lives in their registers (128 values/thread)
+//   warp 8      weight producer: cp.async.bulk (TMA) of pre-packed weight chunks
+//               (already in the UMMA canonical layout) into the SMEM ring
+//   warp 9      MMA issuer: one thread issues tcgen05.mma into TMEM, commits to
+//               mbarriers that release SMEM stages and signal the epilogue
+// TMEM holds two 128 x 256 fp32 accumulators, so the epilogue of GEMM j overlaps
+// the MMAs of GEMM j+1 (which consume the A chunks the epilogue produces).
+//
+// Precision modes:
+//   BF16    kind::f16, bf16 A/B, fp32 accumulate in TMEM
+//   TF32X3  kind::tf32, x = hi + lo (both tf32), D += Ahi*Bhi + Ahi*Blo + Alo*Bhi:
+//           fp32-level accuracy (the fp32 parity mode)
+// Operands use the K-major, no-swizzle canonical layout: 8x16-byte core matrices,
+// LBO = 128 B between K-adjacent core matrices, SBO between 8-row groups.
+#include <cuda_bf16.h>
 #include "common.cuh"
 
 namespace dnnmg {
-int32_t mlp_tc_supported(const dnnmg_mlp_t*) { return 0; }
-int32_t mlp_tc_packed_bytes(const dnnmg_mlp_t*, int64_t* b) { *b = 0; return DNNMG_ERR_UNSUPPORTED; }
-int32_t launch_mlp_tc_pack(const dnnmg_mlp_t*, void*, cudaStream_t) { return DNNMG_ERR_UNSUPPORTED; }
-int32_t launch_mlp_tc(const dnnmg_mlp_t*, const float*, int64_t, float*, cudaStream_t) {
-  return DNNMG_ERR_UNSUPPORTED;
+
+constexpr int kTcM = 128;
+constexpr int kTcH = 256;
+constexpr int kKC = 32;            // K elements per pipeline chunk
+constexpr int kTcThreads = 320;
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
+
+template <int MODE> struct TcCfg;
+template <> struct TcCfg<DNNMG_PREC_BF16> {
+  static constexpr int ESZ = 2, PARTS = 1, NW = 6, NA = 4, KSTEP = 16;
+};
+template <> struct TcCfg<DNNMG_PREC_TF32X3> {
+  static constexpr int ESZ = 4, PARTS = 2, NW = 2, NA = 2, KSTEP = 8;
+};
+
+struct TcArgs {
+  const float* X;
+  float* Y;
+  int64_t n_rows;
+  int n_in, n_out, depth, act;
+  int K0p, Nhead;
+  const uint8_t* packed;
+  int64_t goff[DNNMG_MAX_LAYERS];
+  const float* scale;
+  const float* shift;
+  const float* in_mean;
+  const float* in_std;
+};
+
+// ---- PTX helpers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+template <int MODE>
+__device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  if constexpr (MODE == DNNMG_PREC_BF16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+
+// canonical K-major no-swizzle shared-memory matrix descriptor
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((128u >> 4) & 0x3FFFu) << 16;  // LBO: K-adjacent core matrices
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;   // SBO: 8-row groups
+  d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
+  return d;
+}
+template <int MODE>
+__host__ __device__ constexpr uint32_t idesc_for(int N) {
+  return (1u << 4)                                              // D = F32
+         | ((MODE == DNNMG_PREC_BF16 ? 1u : 2u) << 7)           // A = BF16 | TF32
+         | ((MODE == DNNMG_PREC_BF16 ? 1u : 2u) << 10)          // B = BF16 | TF32
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+}
+
+__device__ __forceinline__ float act_fast(float x, int act, bool accurate) {
+  if (act != DNNMG_ACT_TANH) return fmaxf(x, 0.f);
+  if (accurate) return tanhf(x);
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// byte offset of element (row, kk) in a canonical chunk part (kk < kKC)
+template <int ESZ>
+__host__ __device__ constexpr uint32_t canon_off(int row, int kk) {
+  return (uint32_t)((row >> 3) * (256 * ESZ) + (kk / (16 / ESZ)) * 128 + (row & 7) * 16 +
+                    (kk % (16 / ESZ)) * ESZ);
+}
+
+// write 16 consecutive K values (kk0..kk0+15, kk0 % 16 == 0) of one row into an A stage
+template <int MODE>
+__device__ __forceinline__ void put_row16(uint8_t* stage, int row, int kk0, const float* v) {
+  using C = TcCfg<MODE>;
+  if constexpr (MODE == DNNMG_PREC_BF16) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint4 q;
+      q.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+      q.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+      q.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+      q.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+      *reinterpret_cast<uint4*>(stage + canon_off<2>(row, kk0 + 8 * j)) = q;
+    }
+  } else {
+    constexpr int part = kTcM * kKC * C::ESZ;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 hi, lo;
+      uint32_t* h = &hi.x;
+      uint32_t* l = &lo.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = v[4 * j + e];
+        const uint32_t t = to_tf32(x);
+        h[e] = t;
+        l[e] = to_tf32(x - __uint_as_float(t));
+      }
+      const uint32_t off = canon_off<4>(row, kk0 + 4 * j);
+      *reinterpret_cast<uint4*>(stage + off) = hi;
+      *reinterpret_cast<uint4*>(stage + part + off) = lo;
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
+  using C = TcCfg<MODE>;
+  constexpr int WST = kTcH * kKC * C::ESZ * C::PARTS;  // bytes per weight stage
+  constexpr int AST = kTcM * kKC * C::ESZ * C::PARTS;  // bytes per A stage
+  constexpr uint32_t SBO = 256 * C::ESZ;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* wring = smem;
+  uint8_t* aring = smem + C::NW * WST;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(aring + C::NA * AST);
+  uint64_t* w_full = bars;
+  uint64_t* w_empty = bars + C::NW;
+  uint64_t* a_full = bars + 2 * C::NW;
+  uint64_t* a_empty = bars + 2 * C::NW + C::NA;
+  uint64_t* acc_full = bars + 2 * C::NW + 2 * C::NA;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_tiles = (A.n_rows + kTcM - 1) / kTcM;
+  const int G = A.depth + 1;  // GEMMs per tile
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NW; ++i) {
+      mbar_init(smem_u32(&w_full[i]), 1);
+      mbar_init(smem_u32(&w_empty[i]), 1);
+    }
+    for (int i = 0; i < C::NA; ++i) {
+      mbar_init(smem_u32(&a_full[i]), 8);
+      mbar_init(smem_u32(&a_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProducerWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducerWarp) {
+    // ---------------- weight producer ----------------
+    if (lane == 0) {
+      uint32_t item = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int g = 0; g < G; ++g) {
+          const int N = g < A.depth ? kTcH : A.Nhead;
+          const int nk = (g == 0 ? A.K0p : kTcH) / kKC;
+          const uint32_t bytes = (uint32_t)N * kKC * C::ESZ * C::PARTS;
+          for (int c = 0; c < nk; ++c, ++item) {
+            const int s = item % C::NW;
+            const uint32_t round = item / C::NW;
+            mbar_wait(smem_u32(&w_empty[s]), (round & 1) ^ 1);
+            mbar_expect_tx(smem_u32(&w_full[s]), bytes);
+            bulk_g2s(smem_u32(wring + s * WST), A.packed + A.goff[g] + (int64_t)c * bytes, bytes,
+                     smem_u32(&w_full[s]));
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      uint32_t witem = 0, aitem = 0, j = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int g = 0; g < G; ++g, ++j) {
+          const int N = g < A.depth ? kTcH : A.Nhead;
+          const int nk = (g == 0 ? A.K0p : kTcH) / kKC;
+          const uint32_t idesc = idesc_for<MODE>(N);
+          const int buf = j & 1;
+          mbar_wait(smem_u32(&acc_empty[buf]), ((j >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * kTcH;
+          for (int c = 0; c < nk; ++c, ++witem, ++aitem) {
+            const int sw = witem % C::NW, sa = aitem % C::NA;
+            mbar_wait(smem_u32(&w_full[sw]), (witem / C::NW) & 1);
+            mbar_wait(smem_u32(&a_full[sa]), (aitem / C::NA) & 1);
+            tc_fence_after();
+            const uint32_t wb = smem_u32(wring + sw * WST);
+            const uint32_t ab = smem_u32(aring + sa * AST);
+#pragma unroll
+            for (int ks = 0; ks < kKC / C::KSTEP; ++ks) {
+              const uint32_t koff = ks * 256;
+              const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
+              const uint64_t ahi = sdesc(ab + koff, SBO), bhi = sdesc(wb + koff, SBO);
+              tc_mma<MODE>(d, ahi, bhi, idesc, acc);
+              if constexpr (MODE == DNNMG_PREC_TF32X3) {
+                const uint64_t alo = sdesc(ab + kTcM * kKC * 4 + koff, SBO);
+                const uint64_t blo = sdesc(wb + (uint32_t)N * kKC * 4 + koff, SBO);
+                tc_mma<MODE>(d, ahi, blo, idesc, 1u);
+                tc_mma<MODE>(d, alo, bhi, idesc, 1u);
+              }
+            }
+            tc_commit(smem_u32(&w_empty[sw]));
+            tc_commit(smem_u32(&a_empty[sa]));
+          }
+          tc_commit(smem_u32(&acc_full[buf]));
+        }
+      }
+    }
+  } else {
+    // ---------------- compute warps ----------------
+    const int quad = warp & 3;          // TMEM lane quadrant
+    const int hh = warp >> 2;           // which 16-column half of every 32-column chunk
+    const int row_in_tile = quad * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    constexpr bool accurate = MODE == DNNMG_PREC_TF32X3;
+    float h[8][16];                     // fp32 skip state of this thread's row, 128 columns
+    uint32_t aitem = 0, j = 0;
+
+    auto produce_chunk = [&](int c, const float* v) {
+      const int s = aitem % C::NA;
+      mbar_wait(smem_u32(&a_empty[s]), ((aitem / C::NA) & 1) ^ 1);
+      put_row16<MODE>(aring + s * AST, row_in_tile, 16 * hh, v);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
+      ++aitem;
+      (void)c;
+    };
+
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t row = tile * kTcM + row_in_tile;
+      const bool live = row < A.n_rows;
+      // layer-0 operand: normalised input rows
+      for (int c = 0; c < A.K0p / kKC; ++c) {
+        float v[16];
+        const int col0 = c * kKC + 16 * hh;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int col = col0 + e;
+          float x = 0.f;
+          if (live && col < A.n_in)
+            x = (__ldg(A.X + row * A.n_in + col) - __ldg(A.in_mean + col)) / __ldg(A.in_std + col);
+          v[e] = x;
+        }
+        produce_chunk(c, v);
+      }
+      for (int g = 0; g < A.depth; ++g, ++j) {
+        const int buf = j & 1;
+        mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
+        tc_fence_after();
+        const float* sc = A.scale + g * kTcH;
+        const float* sh = A.shift + g * kTcH;
+#pragma unroll
+        for (int c = 0; c < kTcH / kKC; ++c) {
+          float v[16];
+          tmem_ld16(tmem + lane_addr + buf * kTcH + c * kKC + 16 * hh, v);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int col = c * kKC + 16 * hh + e;
+            const float a = act_fast(fmaf(v[e], __ldg(sc + col), __ldg(sh + col)), A.act, accurate);
+            h[c][e] = (g == 0) ? a : a + h[c][e];
+            v[e] = h[c][e];
+          }
+          produce_chunk(c, v);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
+      }
+      // head: Y = h W_depth
+      {
+        const int buf = j & 1;
+        mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
+        tc_fence_after();
+        for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
+          float v[16];
+          tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
+          if (live) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int col = sl * 16 + e;
+              if (col < A.n_out) A.Y[row * A.n_out + col] = v[e];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
+        ++j;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kProducerWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// ---- weight packing: W[g] (K x N row-major fp32) -> canonical chunk images -----
+template <int MODE>
+__global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, int Np,
+                            uint8_t* __restrict__ out) {
+  using C = TcCfg<MODE>;
+  const int64_t total = (int64_t)Kp * Np;
+  const uint32_t part = (uint32_t)Np * kKC * C::ESZ;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i % Np);
+    const int k = (int)(i / Np);
+    const float w = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
+    const int c = k / kKC, kk = k % kKC;
+    uint8_t* chunk = out + (int64_t)c * part * C::PARTS;
+    const uint32_t off = canon_off<C::ESZ>(n, kk);
+    if constexpr (MODE == DNNMG_PREC_BF16) {
+      *reinterpret_cast<__nv_bfloat16_raw*>(chunk + off) =
+          static_cast<__nv_bfloat16_raw>(__float2bfloat16_rn(w));
+    } else {
+      const uint32_t hi = to_tf32(w);
+      *reinterpret_cast<uint32_t*>(chunk + off) = hi;
+      *reinterpret_cast<uint32_t*>(chunk + part + off) = to_tf32(w - __uint_as_float(hi));
+    }
+  }
+}
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+int32_t mlp_tc_supported(const dnnmg_mlp_t* m) {
+  return (m->precision == DNNMG_PREC_BF16 || m->precision == DNNMG_PREC_TF32X3) &&
+         m->n_hidden == kTcH && m->n_in <= kTcH && m->n_out <= kTcH && m->depth >= 1 &&
+         m->depth < DNNMG_MAX_LAYERS;
+}
+
+static void layout(const dnnmg_mlp_t* m, int64_t* goff, int64_t* total) {
+  const int esz = m->precision == DNNMG_PREC_BF16 ? 2 : 4;
+  const int parts = m->precision == DNNMG_PREC_BF16 ? 1 : 2;
+  int64_t off = 0;
+  for (int g = 0; g <= m->depth; ++g) {
+    const int K = g == 0 ? round_up(m->n_in, kKC) : kTcH;
+    const int N = g < m->depth ? kTcH : round_up(m->n_out, 16);
+    goff[g] = off;
+    off += (int64_t)K * N * esz * parts;
+  }
+  *total = off;
+}
+
+int32_t mlp_tc_packed_bytes(const dnnmg_mlp_t* m, int64_t* bytes) {
+  DNNMG_REQUIRE(mlp_tc_supported(m), DNNMG_ERR_UNSUPPORTED,
+                "mlp: tensor-core mode needs n_hidden == 256, n_in <= 256, n_out <= 256");
+  int64_t goff[DNNMG_MAX_LAYERS];
+  layout(m, goff, bytes);
+  return DNNMG_OK;
+}
+
+int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
+  DNNMG_REQUIRE(mlp_tc_supported(m), DNNMG_ERR_UNSUPPORTED,
+                "mlp: tensor-core mode needs n_hidden == 256, n_in <= 256, n_out <= 256");
+  int64_t goff[DNNMG_MAX_LAYERS], total;
+  layout(m, goff, &total);
+  for (int g = 0; g <= m->depth; ++g) {
+    const int K = g == 0 ? m->n_in : kTcH;
+    const int N = g < m->depth ? kTcH : m->n_out;
+    const int Kp = g == 0 ? round_up(m->n_in, kKC) : kTcH;
+    const int Np = g < m->depth ? kTcH : round_up(m->n_out, 16);
+    uint8_t* out = static_cast<uint8_t*>(packed) + goff[g];
+    const int64_t n = (int64_t)Kp * Np;
+    if (m->precision == DNNMG_PREC_BF16)
+      pack_kernel<DNNMG_PREC_BF16><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, out);
+    else
+      pack_kernel<DNNMG_PREC_TF32X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, out);
+    DNNMG_CHECK_LAUNCH("pack_kernel");
+  }
+  return DNNMG_OK;
+}
+
+template <int MODE>
+static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
+                           cudaStream_t s) {
+  using C = TcCfg<MODE>;
+  TcArgs A;
+  A.X = X;
+  A.Y = Y;
+  A.n_rows = n_rows;
+  A.n_in = m->n_in;
+  A.n_out = m->n_out;
+  A.depth = m->depth;
+  A.act = m->activation;
+  A.K0p = round_up(m->n_in, kKC);
+  A.Nhead = round_up(m->n_out, 16);
+  A.packed = static_cast<const uint8_t*>(m->packed);
+  int64_t total;
+  layout(m, A.goff, &total);
+  A.scale = m->bn_scale;
+  A.shift = m->bn_shift;
+  A.in_mean = m->in_mean;
+  A.in_std = m->in_std;
+  constexpr int WST = kTcH * kKC * C::ESZ * C::PARTS;
+  constexpr int AST = kTcM * kKC * C::ESZ * C::PARTS;
+  size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 4) + 16;
+  if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: TMEM (512 columns) is per SM
+  cudaFuncSetAttribute(mlp_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t tiles = (n_rows + kTcM - 1) / kTcM;
+  const int grid = (int)(tiles < kSMs ? tiles : kSMs);
+  mlp_tc_kernel<MODE><<<grid, kTcThreads, smem, s>>>(A);
+  DNNMG_CHECK_LAUNCH("mlp_tc_kernel");
+  return DNNMG_OK;
+}
+
+int32_t launch_mlp_tc(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
+                      cudaStream_t s) {
+  if (m->precision == DNNMG_PREC_BF16) return launch_mode<DNNMG_PREC_BF16>(m, X, n_rows, Y, s);
+  return launch_mode<DNNMG_PREC_TF32X3>(m, X, n_rows, Y, s);
+}
+
 }  // namespace dnnmg

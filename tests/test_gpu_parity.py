@@ -202,3 +202,73 @@ def test_zero_state_zero_residual(ps3):
     st = asm.stab(x, 1e-2, 0.1)
     r = asm.assemble_residual(x, np.zeros_like(x), 0.1, 1e-2, st, mask=s.dirichlet_mask())
     assert np.all(r == 0.0)
+
+
+# ---- tensor-core MLP modes (tcgen05): fp32-accurate 3xTF32 and bf16 ----------------------
+
+TC_TOL = {"tf32x3": 1e-5, "bf16": 2e-2}
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_forward_tc_cfg0(precision):
+    g = load_golden("cfg0")
+    Y = net.forward(product_model(g), g["X"], precision=precision)
+    assert rel(Y, g["Y"]) < TC_TOL[precision], rel(Y, g["Y"])
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_predict_correction_tc_cfg0(precision):
+    g = load_golden("cfg0")
+    h = product_hierarchy(g)
+    ps = meshmod.build_patches(h, 0, 1)
+    d = patch_ops.predict_correction(product_model(g), g["x_tilde"], g["r"], ps,
+                                     dirichlet_mask=g["mask"], precision=precision)
+    assert rel(d, g["d"]) < TC_TOL[precision], rel(d, g["d"])
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_fused_step_tc_cfg0(precision):
+    g = load_golden("cfg0")
+    h = product_hierarchy(g)
+    step = CorrectionStep(h, 0, 1, product_model(g), float(g["nu"]), float(g["k"]),
+                          precision=precision, t=float(g["t"]))
+    xc = torch.tensor(g["x_coarse"], dtype=torch.float32, device="cuda")
+    b = torch.tensor(g["b_prev"], dtype=torch.float32, device="cuda")
+    step(xc, b)
+    torch.cuda.synchronize()
+    assert rel(step.d.cpu().numpy(), g["d"]) < TC_TOL[precision]
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+@pytest.mark.parametrize("shape", [(240, 3, 81, "tanh", 1000, False), (174, 3, 81, "tanh", 4097, False),
+                                   (240, 4, 81, "relu", 300, True), (256, 1, 200, "tanh", 129, True)])
+def test_forward_tc_random(precision, shape):
+    """Random rows (ragged tile counts), BN stats, input norm, relu/tanh; the
+    float64 oracle MLP (net.py:124-159) is the reference."""
+    from oracle import dnnmg_oracle as orc
+    n_in, depth, n_out, act, rows, bn = shape
+    rng = np.random.default_rng(n_in + rows)
+    m = net.MlpModel(net.Architecture(n_in, 256, depth, n_out), activation=act, seed=rows)
+    dims = [n_in] + [256] * depth + [n_out]
+    m.W = [(rng.uniform(-1, 1, (a, b)) * np.sqrt(6.0 / (a + b))).astype(np.float32).astype(float)
+           for a, b in zip(dims[:-1], dims[1:])]
+    if bn:
+        m.gamma = [rng.uniform(0.5, 1.5, 256) for _ in range(depth)]
+        m.beta = [rng.normal(0, 0.1, 256) for _ in range(depth)]
+        m.running_mean = [rng.normal(0, 0.2, 256) for _ in range(depth)]
+        m.running_var = [rng.uniform(0.5, 2.0, 256) for _ in range(depth)]
+        m.set_input_norm(rng.normal(0, 0.3, n_in), rng.uniform(0.5, 2.0, n_in))
+    m.eval()
+    X = rng.standard_normal((rows, n_in)).astype(np.float32).astype(float)
+    ref = orc.mlp_forward(orc.Mlp(m.W, act, m.gamma, m.beta, m.running_mean, m.running_var,
+                                  m.input_mean, m.input_std), X)
+    Y = net.forward(m, X, precision=precision)
+    assert rel(Y, ref) < TC_TOL[precision], rel(Y, ref)
+    Y32 = net.forward(m, X, precision="fp32")
+    assert rel(Y32, ref) < 1e-5
+
+
+def test_tc_rejects_unsupported_width():
+    m = net.MlpModel(net.Architecture(240, 128, 3, 81), activation="tanh").eval()
+    with pytest.raises(NotImplementedError):
+        net.forward(m, np.zeros((4, 240)), precision="bf16")

@@ -54,19 +54,19 @@ __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[
 #undef QD
 
 // ---- per-cell shared-memory layout (floats) --------------------------------
-constexpr int kNF = 11;               // fields: X^x,X^y,X^z, p, vx,vy,vz, pi p, pi vx,vy,vz
-constexpr int kGroup = 64;            // threads per cell
-constexpr int oU = 0;                 // u[f][27]
-constexpr int oSX = oU + kNF * 27;    // sx[f][2][9][4]   | backward: tx[4][2][3][16][3]
-constexpr int oSY = oSX + kNF * 72;   // sy[f][3][3][16]  |           ty[4][2][2][4][3][3]
-constexpr int oFQ = oSY + kNF * 144;  // fq[f][4][64]
-constexpr int oCF = oFQ + kNF * 256;  // cf[4][7][64]
-constexpr int oTZ = oCF + 4 * 7 * 64; // tz[4][2][27]
-constexpr int oST = oTZ + 4 * 2 * 27; // alpha, delta, vmax scratch
-constexpr int kCellFloats = oST + 4;
-static_assert(4 * 2 * 3 * 48 <= kNF * 72 + kNF * 144, "backward scratch must fit");
+constexpr int kNF = 11;                // fields: X^x,X^y,X^z, p, vx,vy,vz, pi p, pi vx,vy,vz
+constexpr int kGroup = 64;             // threads per cell (one per Gauss point)
+constexpr int oU = 0;                  // u[f][27]
+constexpr int oSX = oU + 300;          // sx[f][2][9][4]          | backward tx[8][3][16][3]
+constexpr int oSY = oSX + kNF * 72;    // sy[f][3][3][16]         |          ty[8][2][4][3][3]
+constexpr int oCF = oSY + kNF * 144;   // cf[4][7][64]
+constexpr int oTZ = oCF + 4 * 7 * 64;  // tz[4][2][27]
+constexpr int oST = oTZ + 4 * 2 * 27;  // alpha, delta, vmax
+constexpr int kCellFloats = (oST + 4 + 3) / 4 * 4;
 constexpr int oTX = oSX;
 constexpr int oTY = oSX + 4 * 2 * 3 * 48;
+static_assert(oTY + 4 * 2 * 2 * 36 <= oCF, "backward scratch must fit in the forward scratch");
+static_assert(oSX % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
@@ -85,46 +85,68 @@ struct ResidualArgs {
 };
 
 // PI[b][v] for local node b (lattice ib) and vertex lattice iv in {0,2}^3 (elements.py:96-118)
-__device__ __forceinline__ float pi_weight(int b, int v) {
+__host__ __device__ constexpr float pi_weight(int b, int v) {
   float w = 1.f;
-  int bb = b, vv = v;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0, bb = b, vv = v; k < 3; ++k, bb /= 3, vv /= 3) {
     const int ib = bb % 3, iv = vv % 3;
-    bb /= 3; vv /= 3;
     w *= (ib == 1) ? 0.5f : (ib == iv ? 1.f : 0.f);
   }
   return w;
 }
 
+__device__ __forceinline__ void group_sync(int grp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(kGroup) : "memory");
+}
+
+struct NodePrefetch {
+  float4 xv;
+  float d0, d1, d2;
+};
+
+__device__ __forceinline__ NodePrefetch load_node(const ResidualArgs& A, int c, int t) {
+  NodePrefetch p;
+  const int node = __ldg(A.cell_nodes + (int64_t)c * 27 + t);
+  const int n0 = __ldg(A.cell_nodes + (int64_t)c * 27);
+  const double* X = A.coords + 3 * (int64_t)node;
+  const double* X0 = A.coords + 3 * (int64_t)n0;
+  p.d0 = float(__ldg(X) - __ldg(X0));
+  p.d1 = float(__ldg(X + 1) - __ldg(X0 + 1));
+  p.d2 = float(__ldg(X + 2) - __ldg(X0 + 2));
+  p.xv = __ldg(A.x + node);
+  return p;
+}
+
 template <int CPB>
-__global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
-  extern __shared__ float smem[];
+__global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
+  extern __shared__ __align__(16) float smem[];
   const int grp = threadIdx.x / kGroup;
   const int t = threadIdx.x % kGroup;
   float* S = smem + grp * kCellFloats;
-  const int vertex_local[8] = {0, 2, 6, 8, 18, 20, 24, 26};
+  // this thread's Gauss point in the pointwise phase: q = qx + 4 qy + 16 qz
+  const int qx = t & 3, qy = (t >> 2) & 3, qz = t >> 4;
+  const float bz0 = cB[qz][0], bz1 = cB[qz][1], bz2 = cB[qz][2];
+  const float dz0 = cD[qz][0], dz1 = cD[qz][1], dz2 = cD[qz][2];
+  const float wq = cW[qx] * cW[qy] * cW[qz];
 
-  for (int base = blockIdx.x * CPB; base < A.n_cells; base += gridDim.x * CPB) {
-    const int c = base + grp;
+  const int stride = gridDim.x * CPB;
+  int c = blockIdx.x * CPB + grp;
+  NodePrefetch pf;
+  if (t < 27 && c < A.n_cells) pf = load_node(A, c, t);
+
+  for (; c - grp < A.n_cells; c += stride) {
     const bool live = c < A.n_cells;
-    // ---------------- gather ----------------
+    // ---------------- gather (prefetched) ----------------
     float vmag = 0.f;
     if (t < 27) {
       if (live) {
-        const int node = __ldg(A.cell_nodes + (int64_t)c * 27 + t);
-        const int n0 = __ldg(A.cell_nodes + (int64_t)c * 27);
-        const double* X = A.coords + 3 * (int64_t)node;
-        const double* X0 = A.coords + 3 * (int64_t)n0;
-        S[oU + 0 * 27 + t] = float(X[0] - X0[0]);
-        S[oU + 1 * 27 + t] = float(X[1] - X0[1]);
-        S[oU + 2 * 27 + t] = float(X[2] - X0[2]);
-        const float4 xv = __ldg(A.x + node);
-        S[oU + 3 * 27 + t] = xv.x;
-        S[oU + 4 * 27 + t] = xv.y;
-        S[oU + 5 * 27 + t] = xv.z;
-        S[oU + 6 * 27 + t] = xv.w;
-        vmag = sqrtf(xv.y * xv.y + xv.z * xv.z + xv.w * xv.w);
+        S[oU + 0 * 27 + t] = pf.d0;
+        S[oU + 1 * 27 + t] = pf.d1;
+        S[oU + 2 * 27 + t] = pf.d2;
+        S[oU + 3 * 27 + t] = pf.xv.x;
+        S[oU + 4 * 27 + t] = pf.xv.y;
+        S[oU + 5 * 27 + t] = pf.xv.z;
+        S[oU + 6 * 27 + t] = pf.xv.w;
+        vmag = sqrtf(pf.xv.y * pf.xv.y + pf.xv.z * pf.xv.z + pf.xv.w * pf.xv.w);
       } else {  // padding cell: unit reference cube, zero state (never written out)
         S[oU + 0 * 27 + t] = 0.5f * (t % 3);
         S[oU + 1 * 27 + t] = 0.5f * ((t / 3) % 3);
@@ -132,19 +154,20 @@ __global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
 #pragma unroll
         for (int f = 3; f < 7; ++f) S[oU + f * 27 + t] = 0.f;
       }
+      if (c + stride < A.n_cells) pf = load_node(A, c + stride, t);  // overlap next cell
     }
-    if (t < 32) {  // vmax over the 27 nodes (assembly.py:169-172): first warp of the group
+    if (t < 32) {  // vmax over the 27 nodes (assembly.py:169-172)
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) vmag = fmaxf(vmag, __shfl_xor_sync(0xffffffffu, vmag, off));
       if (t == 0) S[oST + 2] = vmag;
     }
-    __syncthreads();
+    group_sync(grp);
     if (t < 27) {
-      // pi-projected nodal values (Q1 interpolant of p and v on the Q2 nodes)
+      // pi-projected nodal values: Q1 interpolant of p and v at the Q2 nodes
       float pp = 0.f, p0 = 0.f, p1 = 0.f, p2 = 0.f;
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
-        const int av = vertex_local[v];
+        const int av = (v & 1) * 2 + ((v >> 1) & 1) * 6 + (v >> 2) * 18;
         const float w = pi_weight(t, av);
         pp = fmaf(w, S[oU + 3 * 27 + av], pp);
         p0 = fmaf(w, S[oU + 4 * 27 + av], p0);
@@ -155,8 +178,7 @@ __global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
       S[oU + 8 * 27 + t] = p0;
       S[oU + 9 * 27 + t] = p1;
       S[oU + 10 * 27 + t] = p2;
-    }
-    if (t == 32) {
+    } else if (t == 32) {
       float aT = 0.f, dT = 0.f;
       if (live) {
         if (A.alpha_in) {
@@ -172,70 +194,74 @@ __global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
       S[oST + 0] = aT;
       S[oST + 1] = dT;
     }
-    __syncthreads();
-    // ---------------- forward stage x: sx[f][kind][izy][qx] ----------------
-    for (int l = t; l < kNF * 9; l += kGroup) {
-      const int f = l / 9, izy = l % 9;
-      const float* u = S + oU + f * 27 + izy * 3;
-      const float u0 = u[0], u1 = u[1], u2 = u[2];
-      float* o = S + oSX + f * 72 + izy * 4;
+    group_sync(grp);
+    // ---------------- forward x: sx[f][kind][izy][qx] (float4 over qx) ----------------
 #pragma unroll
-      for (int qx = 0; qx < 4; ++qx) {
-        o[qx] = cB[qx][0] * u0 + cB[qx][1] * u1 + cB[qx][2] * u2;
-        o[36 + qx] = cD[qx][0] * u0 + cD[qx][1] * u1 + cD[qx][2] * u2;
+    for (int r = 0; r < 2; ++r) {
+      const int l = t + 64 * r;
+      if (l < kNF * 9) {
+        const int f = l / 9, izy = l - 9 * (l / 9);
+        const float* u = S + oU + f * 27 + izy * 3;
+        const float u0 = u[0], u1 = u[1], u2 = u[2];
+        float4 vb, vd;
+        vb.x = cB[0][0] * u0 + cB[0][1] * u1 + cB[0][2] * u2;
+        vb.y = cB[1][0] * u0 + cB[1][1] * u1 + cB[1][2] * u2;
+        vb.z = cB[2][0] * u0 + cB[2][1] * u1 + cB[2][2] * u2;
+        vb.w = cB[3][0] * u0 + cB[3][1] * u1 + cB[3][2] * u2;
+        vd.x = cD[0][0] * u0 + cD[0][1] * u1 + cD[0][2] * u2;
+        vd.y = cD[1][0] * u0 + cD[1][1] * u1 + cD[1][2] * u2;
+        vd.z = cD[2][0] * u0 + cD[2][1] * u1 + cD[2][2] * u2;
+        vd.w = cD[3][0] * u0 + cD[3][1] * u1 + cD[3][2] * u2;
+        *reinterpret_cast<float4*>(S + oSX + f * 72 + izy * 4) = vb;
+        *reinterpret_cast<float4*>(S + oSX + f * 72 + 36 + izy * 4) = vd;
       }
     }
-    __syncthreads();
-    // ---------------- forward stage y: sy[f][{vv,vd,dv}][iz][qy*4+qx] ----------------
-    for (int l = t; l < kNF * 12; l += kGroup) {
-      const int f = l / 12, r = l % 12, iz = r / 4, qx = r % 4;
-      const float* s0 = S + oSX + f * 72 + iz * 12 + qx;  // [iy] stride 4
-      const float a0 = s0[0], a1 = s0[4], a2 = s0[8];
-      const float b0 = s0[36], b1 = s0[40], b2 = s0[44];
-      float* o = S + oSY + f * 144 + iz * 16 + qx;
+    group_sync(grp);
+    // ---------------- forward y: sy[f][{vv,vd,dv}][iz][qy*4+qx] ----------------
 #pragma unroll
-      for (int qy = 0; qy < 4; ++qy) {
-        o[qy * 4] = cB[qy][0] * a0 + cB[qy][1] * a1 + cB[qy][2] * a2;
-        o[48 + qy * 4] = cD[qy][0] * a0 + cD[qy][1] * a1 + cD[qy][2] * a2;
-        o[96 + qy * 4] = cB[qy][0] * b0 + cB[qy][1] * b1 + cB[qy][2] * b2;
+    for (int r = 0; r < 3; ++r) {
+      const int l = t + 64 * r;
+      if (l < kNF * 12) {
+        const int f = l / 12, rr = l - 12 * (l / 12), iz = rr >> 2, lx = rr & 3;
+        const float* s0 = S + oSX + f * 72 + iz * 12 + lx;  // [iy] stride 4
+        const float a0 = s0[0], a1 = s0[4], a2 = s0[8];
+        const float b0 = s0[36], b1 = s0[40], b2 = s0[44];
+        float* o = S + oSY + f * 144 + iz * 16 + lx;
+#pragma unroll
+        for (int ly = 0; ly < 4; ++ly) {
+          o[ly * 4] = cB[ly][0] * a0 + cB[ly][1] * a1 + cB[ly][2] * a2;
+          o[48 + ly * 4] = cD[ly][0] * a0 + cD[ly][1] * a1 + cD[ly][2] * a2;
+          o[96 + ly * 4] = cB[ly][0] * b0 + cB[ly][1] * b1 + cB[ly][2] * b2;
+        }
       }
     }
-    __syncthreads();
-    // ---------------- forward stage z: fq[f][{val,dx,dy,dz}][q] ----------------
-    for (int l = t; l < kNF * 16; l += kGroup) {
-      const int f = l / 16, yx = l % 16;
-      const float* s = S + oSY + f * 144 + yx;  // [kind*48 + iz*16]
-      const float vv0 = s[0], vv1 = s[16], vv2 = s[32];
-      const float vd0 = s[48], vd1 = s[64], vd2 = s[80];
-      const float dv0 = s[96], dv1 = s[112], dv2 = s[128];
-      float* o = S + oFQ + f * 256 + yx;
-#pragma unroll
-      for (int qz = 0; qz < 4; ++qz) {
-        const float b0 = cB[qz][0], b1 = cB[qz][1], b2 = cB[qz][2];
-        o[qz * 16] = b0 * vv0 + b1 * vv1 + b2 * vv2;
-        o[64 + qz * 16] = b0 * dv0 + b1 * dv1 + b2 * dv2;
-        o[128 + qz * 16] = b0 * vd0 + b1 * vd1 + b2 * vd2;
-        o[192 + qz * 16] = cD[qz][0] * vv0 + cD[qz][1] * vv1 + cD[qz][2] * vv2;
-      }
-    }
-    __syncthreads();
-    // ---------------- pointwise (thread = Gauss point q) ----------------
+    group_sync(grp);
+    // ---------------- forward z fused with the pointwise phase (thread = q) ----------------
     {
-      const int q = t;
-      const float* F = S + oFQ + q;
-#define FQ(f, kind) F[(f) * 256 + (kind) * 64]
+      const int yx = t & 15;
+      float F[kNF][4];  // [field][val, d/dxi, d/deta, d/dzeta] at this Gauss point
+#pragma unroll
+      for (int f = 0; f < kNF; ++f) {
+        const float* s = S + oSY + f * 144 + yx;
+        const float vv0 = s[0], vv1 = s[16], vv2 = s[32];
+        const float vd0 = s[48], vd1 = s[64], vd2 = s[80];
+        const float dv0 = s[96], dv1 = s[112], dv2 = s[128];
+        F[f][0] = bz0 * vv0 + bz1 * vv1 + bz2 * vv2;
+        F[f][1] = bz0 * dv0 + bz1 * dv1 + bz2 * dv2;
+        F[f][2] = bz0 * vd0 + bz1 * vd1 + bz2 * vd2;
+        F[f][3] = dz0 * vv0 + dz1 * vv1 + dz2 * vv2;
+      }
       float J[3][3];
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) J[i][j] = FQ(i, 1 + j);
+        for (int j = 0; j < 3; ++j) J[i][j] = F[i][1 + j];
       const float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
       const float c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
       const float c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
       const float det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
       const float id = 1.0f / det;
-      // Ji[k][j] = (J^-1)[k][j]: reference k -> physical j
-      float Ji[3][3];
+      float Ji[3][3];  // (J^-1)[k][j]: reference k -> physical j
       Ji[0][0] = c00 * id;
       Ji[1][0] = c01 * id;
       Ji[2][0] = c02 * id;
@@ -245,50 +271,52 @@ __global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
       Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
       Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
       Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
-      const float w = cW[q & 3] * cW[(q >> 2) & 3] * cW[q >> 4] * det;
+      const float w = wq * det;
       const float aT = S[oST + 0], dT = S[oST + 1];
       float v[3], gv[3][3];
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        v[i] = FQ(4 + i, 0);
+        v[i] = F[4 + i][0];
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          gv[i][j] = FQ(4 + i, 1) * Ji[0][j] + FQ(4 + i, 2) * Ji[1][j] + FQ(4 + i, 3) * Ji[2][j];
+          gv[i][j] = F[4 + i][1] * Ji[0][j] + F[4 + i][2] * Ji[1][j] + F[4 + i][3] * Ji[2][j];
       }
       float conv[3];
 #pragma unroll
       for (int i = 0; i < 3; ++i)
         conv[i] = A.convection ? v[0] * gv[i][0] + v[1] * gv[i][1] + v[2] * gv[i][2] : 0.f;
-      float* C = S + oCF + q;  // cf[comp][arr][q]
+      float* C = S + oCF + t;
 #define CF(comp, arr) C[((comp) * 7 + (arr)) * 64]
+      const float ik = 1.0f / A.k;
       if (A.mode == MODE_OPERATOR) {
-        const float p = FQ(3, 0);
+        const float p = F[3][0];
         float gp[3], gpp[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-          gp[j] = FQ(3, 1) * Ji[0][j] + FQ(3, 2) * Ji[1][j] + FQ(3, 3) * Ji[2][j];
-          gpp[j] = FQ(7, 1) * Ji[0][j] + FQ(7, 2) * Ji[1][j] + FQ(7, 3) * Ji[2][j];
+          gp[j] = F[3][1] * Ji[0][j] + F[3][2] * Ji[1][j] + F[3][3] * Ji[2][j];
+          gpp[j] = F[7][1] * Ji[0][j] + F[7][2] * Ji[1][j] + F[7][3] * Ji[2][j];
         }
         const bool use_d = A.convection && dT != 0.f;
         float g[3] = {0.f, 0.f, 0.f}, pvr[3] = {0.f, 0.f, 0.f};
         if (use_d) {
-          float pv[3], gpv[3][3];
+          float pv[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) pv[i] = F[8 + i][0];
 #pragma unroll
           for (int i = 0; i < 3; ++i) {
-            pv[i] = FQ(8 + i, 0);
+            float s = 0.f;
 #pragma unroll
-            for (int j = 0; j < 3; ++j)
-              gpv[i][j] = FQ(8 + i, 1) * Ji[0][j] + FQ(8 + i, 2) * Ji[1][j] + FQ(8 + i, 3) * Ji[2][j];
+            for (int j = 0; j < 3; ++j) {
+              const float gpv = F[8 + i][1] * Ji[0][j] + F[8 + i][2] * Ji[1][j] + F[8 + i][3] * Ji[2][j];
+              s = fmaf(pv[j], gpv, s);
+            }
+            g[i] = conv[i] - s;
           }
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-            g[i] = conv[i] - (pv[0] * gpv[i][0] + pv[1] * gpv[i][1] + pv[2] * gpv[i][2]);
 #pragma unroll
           for (int kk = 0; kk < 3; ++kk)
             pvr[kk] = Ji[kk][0] * pv[0] + Ji[kk][1] * pv[1] + Ji[kk][2] * pv[2];
         }
         const float div = gv[0][0] + gv[1][1] + gv[2][2];
-        // continuity: value test w*div; gradient test alpha*w*(gp - gpp) through (G - Gpi)
         float E[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) E[j] = aT * w * (gp[j] - gpp[j]);
@@ -300,7 +328,6 @@ __global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
           CF(0, 4 + kk) = -b;
         }
         const float hn = 0.5f * A.nu * w;
-        const float ik = 1.0f / A.k;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           CF(1 + i, 0) = w * (v[i] * ik + 0.5f * conv[i]);
@@ -316,7 +343,6 @@ __global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
         }
       } else {  // MODE_RHS (assembly.py:242-259, f = None)
         const float hn = -0.5f * A.nu * w;
-        const float ik = 1.0f / A.k;
 #pragma unroll
         for (int a = 0; a < 7; ++a) CF(0, a) = 0.f;
 #pragma unroll
@@ -324,101 +350,118 @@ __global__ void __launch_bounds__(64 * CPB) element_kernel(ResidualArgs A) {
           CF(1 + i, 0) = w * (v[i] * ik - 0.5f * conv[i]);
 #pragma unroll
           for (int kk = 0; kk < 3; ++kk) {
-            CF(1 + i, 1 + kk) = hn * (Ji[kk][0] * gv[i][0] + Ji[kk][1] * gv[i][1] + Ji[kk][2] * gv[i][2]);
+            CF(1 + i, 1 + kk) =
+                hn * (Ji[kk][0] * gv[i][0] + Ji[kk][1] * gv[i][1] + Ji[kk][2] * gv[i][2]);
             CF(1 + i, 4 + kk) = 0.f;
           }
         }
       }
 #undef CF
-#undef FQ
     }
-    __syncthreads();
-    // ---------------- backward stage x (contract qx) ----------------
-    // line (comp, part, qz, qy) -> tx[comp][part][{Tv,T1,T2}][qz*4+qy][ix]
-    for (int l = t; l < 4 * 2 * 16; l += kGroup) {
-      const int comp = l / 32, part = (l / 16) % 2, zy = l % 16;
-      const float* cf = S + oCF + comp * 7 * 64 + zy * 4;
-      float Av[4], B0[4], B1[4], B2[4];
+    group_sync(grp);
+    // ---------------- backward x (contract qx): line (comp, part, zy) ----------------
 #pragma unroll
-      for (int qx = 0; qx < 4; ++qx) {
-        if (part == 0) {
-          Av[qx] = cf[qx];
-          B0[qx] = cf[64 + qx];
-          B1[qx] = cf[128 + qx];
-          B2[qx] = cf[192 + qx];
-        } else {
-          Av[qx] = 0.f;
-          B0[qx] = cf[256 + qx];
-          B1[qx] = cf[320 + qx];
-          B2[qx] = cf[384 + qx];
-        }
+    for (int r = 0; r < 2; ++r) {
+      const int l = t + 64 * r;
+      const int comp = l >> 5, part = (l >> 4) & 1, zy = l & 15;
+      const float* cf = S + oCF + comp * 7 * 64 + zy * 4;
+      float4 a4, b0, b1, b2;
+      if (part == 0) {
+        a4 = *reinterpret_cast<const float4*>(cf);
+        b0 = *reinterpret_cast<const float4*>(cf + 64);
+        b1 = *reinterpret_cast<const float4*>(cf + 128);
+        b2 = *reinterpret_cast<const float4*>(cf + 192);
+      } else {
+        a4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        b0 = *reinterpret_cast<const float4*>(cf + 256);
+        b1 = *reinterpret_cast<const float4*>(cf + 320);
+        b2 = *reinterpret_cast<const float4*>(cf + 384);
       }
+      const float Av[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float B0[4] = {b0.x, b0.y, b0.z, b0.w};
+      const float B1[4] = {b1.x, b1.y, b1.z, b1.w};
+      const float B2[4] = {b2.x, b2.y, b2.z, b2.w};
       float* o = S + oTX + ((comp * 2 + part) * 3) * 48 + zy * 3;
 #pragma unroll
       for (int ix = 0; ix < 3; ++ix) {
         float tv = 0.f, t1 = 0.f, t2 = 0.f;
 #pragma unroll
-        for (int qx = 0; qx < 4; ++qx) {
-          tv += cB[qx][ix] * Av[qx] + cD[qx][ix] * B0[qx];
-          t1 += cB[qx][ix] * B1[qx];
-          t2 += cB[qx][ix] * B2[qx];
+        for (int q = 0; q < 4; ++q) {
+          tv += cB[q][ix] * Av[q] + cD[q][ix] * B0[q];
+          t1 += cB[q][ix] * B1[q];
+          t2 += cB[q][ix] * B2[q];
         }
         o[ix] = tv;
         o[48 + ix] = t1;
         o[96 + ix] = t2;
       }
     }
-    __syncthreads();
-    // ---------------- backward stage y (contract qy) ----------------
-    // line (comp, part, qz, ix) -> ty[comp][part][{Ua,Ub}][qz][iy][ix]
-    for (int l = t; l < 4 * 2 * 12; l += kGroup) {
-      const int cp = l / 12, r = l % 12, qz = r / 3, ix = r % 3;
-      const float* tx = S + oTX + cp * 3 * 48 + qz * 12 + ix;  // [arr*48 + qy*3]
-      float* o = S + oTY + cp * 2 * 36 + qz * 9 + ix;
+    group_sync(grp);
+    // ---------------- backward y (contract qy): line (cp, qz, ix) ----------------
 #pragma unroll
-      for (int iy = 0; iy < 3; ++iy) {
-        float ua = 0.f, ub = 0.f;
+    for (int r = 0; r < 2; ++r) {
+      const int l = t + 64 * r;
+      if (l < 4 * 2 * 12) {
+        const int cp = l / 12, rr = l - 12 * (l / 12), lz = rr / 3, ix = rr - 3 * (rr / 3);
+        const float* tx = S + oTX + cp * 3 * 48 + lz * 12 + ix;  // [arr*48 + qy*3]
+        float* o = S + oTY + cp * 2 * 36 + lz * 9 + ix;
 #pragma unroll
-        for (int qy = 0; qy < 4; ++qy) {
-          ua += cB[qy][iy] * tx[qy * 3] + cD[qy][iy] * tx[48 + qy * 3];
-          ub += cB[qy][iy] * tx[96 + qy * 3];
+        for (int iy = 0; iy < 3; ++iy) {
+          float ua = 0.f, ub = 0.f;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ua += cB[q][iy] * tx[q * 3] + cD[q][iy] * tx[48 + q * 3];
+            ub += cB[q][iy] * tx[96 + q * 3];
+          }
+          o[iy * 3] = ua;
+          o[36 + iy * 3] = ub;
         }
-        o[iy * 3] = ua;
-        o[36 + iy * 3] = ub;
       }
     }
-    __syncthreads();
-    // ---------------- backward stage z (contract qz) ----------------
-    for (int l = t; l < 4 * 2 * 9; l += kGroup) {
-      const int cp = l / 9, yx = l % 9;
-      const float* ty = S + oTY + cp * 2 * 36 + yx;  // [arr*36 + qz*9]
-      float* o = S + oTZ + cp * 27 + yx;
+    group_sync(grp);
+    // ---------------- backward z (contract qz): line (cp, yx) ----------------
 #pragma unroll
-      for (int iz = 0; iz < 3; ++iz) {
-        float s = 0.f;
+    for (int r = 0; r < 2; ++r) {
+      const int l = t + 64 * r;
+      if (l < 4 * 2 * 9) {
+        const int cp = l / 9, yx = l - 9 * (l / 9);
+        const float* ty = S + oTY + cp * 2 * 36 + yx;  // [arr*36 + qz*9]
+        float* o = S + oTZ + cp * 27 + yx;
 #pragma unroll
-        for (int qz = 0; qz < 4; ++qz) s += cB[qz][iz] * ty[qz * 9] + cD[qz][iz] * ty[36 + qz * 9];
-        o[iz * 9] = s;
+        for (int iz = 0; iz < 3; ++iz) {
+          float s = 0.f;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s += cB[q][iz] * ty[q * 9] + cD[q][iz] * ty[36 + q * 9];
+          o[iz * 9] = s;
+        }
       }
     }
-    __syncthreads();
-    // ---------------- output: direct + PI^T * gpi part ----------------
+    group_sync(grp);
+    // ---------------- output: direct + PI^T * (LPS part), one float4 per node ----------------
     if (t < 27 && live) {
       float e[4];
+      const bool vertex = (t % 3 != 1) && ((t / 3) % 3 != 1) && (t / 9 != 1);
 #pragma unroll
       for (int comp = 0; comp < 4; ++comp) {
         float s = S[oTZ + (comp * 2) * 27 + t];
-        // PI[b][t] is non-zero only for vertex nodes t
-        const int ax = t % 3, ay = (t / 3) % 3, az = t / 9;
-        if (ax != 1 && ay != 1 && az != 1) {
+        if (vertex) {
           const float* gp = S + oTZ + (comp * 2 + 1) * 27;
-          for (int b = 0; b < 27; ++b) s = fmaf(pi_weight(b, t), gp[b], s);
+#pragma unroll
+          for (int b = 0; b < 27; ++b) {
+            // PI[b][t] for vertex t: 1 at the vertex, 1/2^m for nodes between
+            const int ib0 = b % 3, ib1 = (b / 3) % 3, ib2 = b / 9;
+            const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
+            const float w = (ib0 == 1 ? 0.5f : (ib0 == it0 ? 1.f : 0.f)) *
+                            (ib1 == 1 ? 0.5f : (ib1 == it1 ? 1.f : 0.f)) *
+                            (ib2 == 1 ? 0.5f : (ib2 == it2 ? 1.f : 0.f));
+            s = fmaf(w, gp[b], s);
+          }
         }
         e[comp] = s;
       }
       A.elem[(int64_t)c * 27 + t] = make_float4(e[0], e[1], e[2], e[3]);
     }
-    __syncthreads();
+    // the next cell's gather writes only u, which no later stage of this cell reads
   }
 }
 
@@ -473,7 +516,7 @@ __global__ void __launch_bounds__(256) stab_kernel(int n_cells, const int32_t* _
   }
 }
 
-constexpr int kCPB = 2;
+constexpr int kCPB = 4;
 
 static int32_t check_level(const dnnmg_level_t* lv, const char* who) {
   DNNMG_REQUIRE(lv && lv->cell_nodes && lv->coords && lv->h_T && lv->node_cell_ptr &&
@@ -508,7 +551,7 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
     configured = true;
   }
   int blocks = (lv->n_cells + kCPB - 1) / kCPB;
-  const int cap = kSMs * 8;
+  const int cap = kSMs * 2;
   if (blocks > cap) blocks = cap;
   if (lv->n_cells == 0) return DNNMG_OK;
   element_kernel<kCPB><<<blocks, 64 * kCPB, smem, s>>>(A);

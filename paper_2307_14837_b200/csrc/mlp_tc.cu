@@ -23,6 +23,7 @@
 // Operands use the K-major, no-swizzle canonical layout: 8x16-byte core matrices,
 // LBO = 128 B between K-adjacent core matrices, SBO between 8-row groups.
 #include <cuda_bf16.h>
+#include <type_traits>
 #include "common.cuh"
 
 namespace dnnmg {
@@ -48,6 +49,7 @@ struct TcArgs {
   int64_t n_rows;
   int n_in, n_out, depth, act;
   int K0p, Nhead;
+  int y_mode;  // 0: direct stores, 1: staged in the A ring, 2: staged in a dedicated buffer
   const uint8_t* packed;
   int64_t goff[DNNMG_MAX_LAYERS];
   const float* scale;
@@ -167,9 +169,12 @@ __host__ __device__ constexpr uint32_t idesc_for(int N) {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
 }
 
+// tanh: bf16 mode uses the MUFU tanh.approx (rel. err ~2^-11, below bf16 resolution);
+// the fp32-accuracy mode uses 1 - 2/(1 + e^{2x}) with MUFU ex2/rcp: absolute error
+// ~2e-7 on [-1, 1], saturating correctly for |x| -> inf.
 __device__ __forceinline__ float act_fast(float x, int act, bool accurate) {
   if (act != DNNMG_ACT_TANH) return fmaxf(x, 0.f);
-  if (accurate) return tanhf(x);
+  if (accurate) return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x));
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
@@ -234,6 +239,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   uint64_t* acc_full = bars + 2 * C::NW + 2 * C::NA;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // BN scale/shift per hidden layer and the input normalisation, staged once per CTA
+  float* p_scale = reinterpret_cast<float*>(tmem_slot + 4);
+  float* p_shift = p_scale + A.depth * kTcH;
+  float* p_mean = p_shift + A.depth * kTcH;
+  float* p_rstd = p_mean + kTcH;
+  for (int i = threadIdx.x; i < A.depth * kTcH; i += blockDim.x) {
+    p_scale[i] = A.scale[i];
+    p_shift[i] = A.shift[i];
+  }
+  float* y_stage = A.y_mode == 1 ? reinterpret_cast<float*>(aring) : p_rstd + kTcH;
+  for (int i = threadIdx.x; i < kTcH; i += blockDim.x) {
+    p_mean[i] = i < A.n_in ? A.in_mean[i] : 0.f;
+    p_rstd[i] = i < A.n_in ? 1.0f / A.in_std[i] : 0.f;
+  }
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -347,61 +366,135 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       (void)c;
     };
 
+    const int nck0 = A.K0p / kKC;
+    const bool vec_x = (A.n_in & 3) == 0;
+    float xin[8][16];                   // raw input row slice of the next tile (prefetched)
+    auto load_x = [&](int64_t tile) {
+      const int64_t row = tile * kTcM + row_in_tile;
+      const bool ok = tile < n_tiles && row < A.n_rows;
+      const float* xr = A.X + row * A.n_in;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = c * kKC + 16 * hh + 4 * j;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ok && c < nck0) {
+            if (vec_x) {
+              if (col < A.n_in) v = __ldg(reinterpret_cast<const float4*>(xr + col));
+            } else {
+              if (col < A.n_in) v.x = __ldg(xr + col);
+              if (col + 1 < A.n_in) v.y = __ldg(xr + col + 1);
+              if (col + 2 < A.n_in) v.z = __ldg(xr + col + 2);
+              if (col + 3 < A.n_in) v.w = __ldg(xr + col + 3);
+            }
+          }
+          xin[c][4 * j] = v.x;
+          xin[c][4 * j + 1] = v.y;
+          xin[c][4 * j + 2] = v.z;
+          xin[c][4 * j + 3] = v.w;
+        }
+      }
+    };
+    load_x(blockIdx.x);
+
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int64_t row = tile * kTcM + row_in_tile;
       const bool live = row < A.n_rows;
-      // layer-0 operand: normalised input rows
-      for (int c = 0; c < A.K0p / kKC; ++c) {
-        float v[16];
-        const int col0 = c * kKC + 16 * hh;
+      // layer-0 operand: normalised input rows (net.py:131), from the prefetched registers
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int col = col0 + e;
-          float x = 0.f;
-          if (live && col < A.n_in)
-            x = (__ldg(A.X + row * A.n_in + col) - __ldg(A.in_mean + col)) / __ldg(A.in_std + col);
-          v[e] = x;
+      for (int c = 0; c < 8; ++c) {
+        if (c < nck0) {
+          float v[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int col = c * kKC + 16 * hh + e;
+            v[e] = (xin[c][e] - p_mean[col]) * p_rstd[col];
+          }
+          produce_chunk(c, v);
         }
-        produce_chunk(c, v);
       }
-      for (int g = 0; g < A.depth; ++g, ++j) {
+      // hidden layers: layer 0 writes the skip state, layers >= 1 add to it
+      auto epilogue = [&](int g, auto first) {
         const int buf = j & 1;
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
         tc_fence_after();
-        const float* sc = A.scale + g * kTcH;
-        const float* sh = A.shift + g * kTcH;
+        const float* sc = p_scale + g * kTcH;
+        const float* sh = p_shift + g * kTcH;
 #pragma unroll
         for (int c = 0; c < kTcH / kKC; ++c) {
           float v[16];
           tmem_ld16(tmem + lane_addr + buf * kTcH + c * kKC + 16 * hh, v);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          for (int e = 0; e < 16; e += 4) {
             const int col = c * kKC + 16 * hh + e;
-            const float a = act_fast(fmaf(v[e], __ldg(sc + col), __ldg(sh + col)), A.act, accurate);
-            h[c][e] = (g == 0) ? a : a + h[c][e];
-            v[e] = h[c][e];
+            const float4 s4 = *reinterpret_cast<const float4*>(sc + col);
+            const float4 t4 = *reinterpret_cast<const float4*>(sh + col);
+            const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+            const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float a = act_fast(fmaf(v[e + u], sv[u], tv[u]), A.act, accurate);
+              if constexpr (decltype(first)::value) h[c][e + u] = a;
+              else h[c][e + u] = a + h[c][e + u];
+              v[e + u] = h[c][e + u];
+            }
           }
           produce_chunk(c, v);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
-      }
+        ++j;
+      };
+      epilogue(0, std::true_type{});
+      for (int g = 1; g < A.depth; ++g) epilogue(g, std::false_type{});
+      // the skip state is dead now: prefetch the next tile's input under the head GEMM
+      load_x(tile + gridDim.x);
       // head: Y = h W_depth
       {
         const int buf = j & 1;
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
         tc_fence_after();
+        if (A.y_mode == 0) {
+          for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
+            float v[16];
+            tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
+            if (live) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const int col = sl * 16 + e;
+                if (col < A.n_out) A.Y[row * A.n_out + col] = v[e];
+              }
+            }
+          }
+        } else {
+        // stage the 128 x n_out tile in SMEM (the A ring is idle here: every head
+        // chunk has been consumed and the next tile's chunks are not produced yet)
+        float* ys = y_stage;
         for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
           float v[16];
           tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
-          if (live) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int col = sl * 16 + e;
-              if (col < A.n_out) A.Y[row * A.n_out + col] = v[e];
-            }
+          for (int e = 0; e < 16; ++e) {
+            const int col = sl * 16 + e;
+            if (col < A.n_out) ys[row_in_tile * A.n_out + col] = v[e];
           }
+        }
+        tc_fence_before();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        {  // coalesced copy of the contiguous Y block of this tile
+          const int64_t r0 = tile * kTcM;
+          const int nvalid = (int)((A.n_rows - r0) < kTcM ? (A.n_rows - r0) : kTcM);
+          const int nf = nvalid * A.n_out;
+          float* dst = A.Y + r0 * A.n_out;
+          const int tid = threadIdx.x;
+          const int n4 = nf >> 2;
+          for (int i = tid; i < n4; i += 256)
+            reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(ys)[i];
+          for (int i = 4 * n4 + tid; i < nf; i += 256) dst[i] = ys[i];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         }
         tc_fence_before();
         __syncwarp();
@@ -517,7 +610,17 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.in_std = m->in_std;
   constexpr int WST = kTcH * kKC * C::ESZ * C::PARTS;
   constexpr int AST = kTcM * kKC * C::ESZ * C::PARTS;
-  size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 4) + 16;
+  size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 4) + 16 +
+                sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
+  const size_t ybytes = (size_t)kTcM * m->n_out * 4;
+  if ((size_t)C::NA * AST >= ybytes) {
+    A.y_mode = 1;
+  } else if (smem + ybytes <= 220 * 1024) {
+    A.y_mode = 2;
+    smem += ybytes;
+  } else {
+    A.y_mode = 0;
+  }
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: TMEM (512 columns) is per SM
   cudaFuncSetAttribute(mlp_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t tiles = (n_rows + kTcM - 1) / kTcM;

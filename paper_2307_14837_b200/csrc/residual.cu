@@ -48,25 +48,30 @@ __constant__ float cB[4][3] = {{QB(0, 0), QB(0, 1), QB(0, 2)}, {QB(1, 0), QB(1, 
                                {QB(2, 0), QB(2, 1), QB(2, 2)}, {QB(3, 0), QB(3, 1), QB(3, 2)}};
 __constant__ float cD[4][3] = {{QD(0, 0), QD(0, 1), QD(0, 2)}, {QD(1, 0), QD(1, 1), QD(1, 2)},
                                {QD(2, 0), QD(2, 1), QD(2, 2)}, {QD(3, 0), QD(3, 1), QD(3, 2)}};
+__constant__ float cX[4] = {float(tab::xg[0]), float(tab::xg[1]), float(tab::xg[2]),
+                            float(tab::xg[3])};
 __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[2]),
                             float(tab::wg[3])};
 #undef QB
 #undef QD
 
 // ---- per-cell shared-memory layout (floats) --------------------------------
-constexpr int kNF = 11;                // fields: X^x,X^y,X^z, p, vx,vy,vz, pi p, pi vx,vy,vz
+// Q2 fields through the sum-factorised forward stages: X^x, X^y, X^z, p, vx, vy, vz.
+// The pi-projected (Q1) fields are trilinear in the 8 vertex values and are
+// evaluated per Gauss point directly from those (elements.py:96-118).
+constexpr int kNF = 7;
 constexpr int kGroup = 64;             // threads per cell (one per Gauss point)
 constexpr int oU = 0;                  // u[f][27]
-constexpr int oSX = oU + 300;          // sx[f][2][9][4]          | backward tx[8][3][16][3]
-constexpr int oSY = oSX + kNF * 72;    // sy[f][3][3][16]         |          ty[8][2][4][3][3]
-constexpr int oCF = oSY + kNF * 144;   // cf[4][7][64]
+constexpr int oSX = 192;               // sx[f][2][9][4]          | backward tx[8][3][16][3]
+constexpr int oSY = oSX + kNF * 72;    // sy[f][16][12] = [yx][{vv,vd,dv} x iz, pad]
+constexpr int oCF = oSY + kNF * 192;   // cf[4][7][64]            |          ty[8][2][4][3][3]
 constexpr int oTZ = oCF + 4 * 7 * 64;  // tz[4][2][27]
 constexpr int oST = oTZ + 4 * 2 * 27;  // alpha, delta, vmax
 constexpr int kCellFloats = (oST + 4 + 3) / 4 * 4;
 constexpr int oTX = oSX;
 constexpr int oTY = oSX + 4 * 2 * 3 * 48;
 static_assert(oTY + 4 * 2 * 2 * 36 <= oCF, "backward scratch must fit in the forward scratch");
-static_assert(oSX % 4 == 0 && oCF % 4 == 0, "float4 alignment");
+static_assert(oSX % 4 == 0 && oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
@@ -127,6 +132,7 @@ __global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
   const float bz0 = cB[qz][0], bz1 = cB[qz][1], bz2 = cB[qz][2];
   const float dz0 = cD[qz][0], dz1 = cD[qz][1], dz2 = cD[qz][2];
   const float wq = cW[qx] * cW[qy] * cW[qz];
+  const float lx1 = cX[qx], ly1 = cX[qy], lz1 = cX[qz];  // Gauss coordinates: L1 = x, L0 = 1 - x
 
   const int stride = gridDim.x * CPB;
   int c = blockIdx.x * CPB + grp;
@@ -162,23 +168,7 @@ __global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
       if (t == 0) S[oST + 2] = vmag;
     }
     group_sync(grp);
-    if (t < 27) {
-      // pi-projected nodal values: Q1 interpolant of p and v at the Q2 nodes
-      float pp = 0.f, p0 = 0.f, p1 = 0.f, p2 = 0.f;
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int av = (v & 1) * 2 + ((v >> 1) & 1) * 6 + (v >> 2) * 18;
-        const float w = pi_weight(t, av);
-        pp = fmaf(w, S[oU + 3 * 27 + av], pp);
-        p0 = fmaf(w, S[oU + 4 * 27 + av], p0);
-        p1 = fmaf(w, S[oU + 5 * 27 + av], p1);
-        p2 = fmaf(w, S[oU + 6 * 27 + av], p2);
-      }
-      S[oU + 7 * 27 + t] = pp;
-      S[oU + 8 * 27 + t] = p0;
-      S[oU + 9 * 27 + t] = p1;
-      S[oU + 10 * 27 + t] = p2;
-    } else if (t == 32) {
+    if (t == 32) {
       float aT = 0.f, dT = 0.f;
       if (live) {
         if (A.alpha_in) {
@@ -196,43 +186,47 @@ __global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
     }
     group_sync(grp);
     // ---------------- forward x: sx[f][kind][izy][qx] (float4 over qx) ----------------
+    if (t < kNF * 9) {
+      const int f = t / 9, izy = t - 9 * (t / 9);
+      const float* u = S + oU + f * 27 + izy * 3;
+      const float u0 = u[0], u1 = u[1], u2 = u[2];
+      float4 vb, vd;
+      vb.x = cB[0][0] * u0 + cB[0][1] * u1 + cB[0][2] * u2;
+      vb.y = cB[1][0] * u0 + cB[1][1] * u1 + cB[1][2] * u2;
+      vb.z = cB[2][0] * u0 + cB[2][1] * u1 + cB[2][2] * u2;
+      vb.w = cB[3][0] * u0 + cB[3][1] * u1 + cB[3][2] * u2;
+      vd.x = cD[0][0] * u0 + cD[0][1] * u1 + cD[0][2] * u2;
+      vd.y = cD[1][0] * u0 + cD[1][1] * u1 + cD[1][2] * u2;
+      vd.z = cD[2][0] * u0 + cD[2][1] * u1 + cD[2][2] * u2;
+      vd.w = cD[3][0] * u0 + cD[3][1] * u1 + cD[3][2] * u2;
+      *reinterpret_cast<float4*>(S + oSX + f * 72 + izy * 4) = vb;
+      *reinterpret_cast<float4*>(S + oSX + f * 72 + 36 + izy * 4) = vd;
+    }
+    group_sync(grp);
+    // ---------------- forward y: line (f, qy, qx) -> sy[f][qy*4+qx][kind*3+iz] ----------------
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int l = t + 64 * r;
-      if (l < kNF * 9) {
-        const int f = l / 9, izy = l - 9 * (l / 9);
-        const float* u = S + oU + f * 27 + izy * 3;
-        const float u0 = u[0], u1 = u[1], u2 = u[2];
-        float4 vb, vd;
-        vb.x = cB[0][0] * u0 + cB[0][1] * u1 + cB[0][2] * u2;
-        vb.y = cB[1][0] * u0 + cB[1][1] * u1 + cB[1][2] * u2;
-        vb.z = cB[2][0] * u0 + cB[2][1] * u1 + cB[2][2] * u2;
-        vb.w = cB[3][0] * u0 + cB[3][1] * u1 + cB[3][2] * u2;
-        vd.x = cD[0][0] * u0 + cD[0][1] * u1 + cD[0][2] * u2;
-        vd.y = cD[1][0] * u0 + cD[1][1] * u1 + cD[1][2] * u2;
-        vd.z = cD[2][0] * u0 + cD[2][1] * u1 + cD[2][2] * u2;
-        vd.w = cD[3][0] * u0 + cD[3][1] * u1 + cD[3][2] * u2;
-        *reinterpret_cast<float4*>(S + oSX + f * 72 + izy * 4) = vb;
-        *reinterpret_cast<float4*>(S + oSX + f * 72 + 36 + izy * 4) = vd;
-      }
-    }
-    group_sync(grp);
-    // ---------------- forward y: sy[f][{vv,vd,dv}][iz][qy*4+qx] ----------------
+      if (l < kNF * 16) {
+        const int f = l >> 4, yx = l & 15, ly = yx >> 2, lx = yx & 3;
+        const float* s0 = S + oSX + f * 72 + lx;  // [kind*36 + (iz*3+iy)*4]
+        const float by0 = cB[ly][0], by1 = cB[ly][1], by2 = cB[ly][2];
+        const float dy0 = cD[ly][0], dy1 = cD[ly][1], dy2 = cD[ly][2];
+        float o[12];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int l = t + 64 * r;
-      if (l < kNF * 12) {
-        const int f = l / 12, rr = l - 12 * (l / 12), iz = rr >> 2, lx = rr & 3;
-        const float* s0 = S + oSX + f * 72 + iz * 12 + lx;  // [iy] stride 4
-        const float a0 = s0[0], a1 = s0[4], a2 = s0[8];
-        const float b0 = s0[36], b1 = s0[40], b2 = s0[44];
-        float* o = S + oSY + f * 144 + iz * 16 + lx;
-#pragma unroll
-        for (int ly = 0; ly < 4; ++ly) {
-          o[ly * 4] = cB[ly][0] * a0 + cB[ly][1] * a1 + cB[ly][2] * a2;
-          o[48 + ly * 4] = cD[ly][0] * a0 + cD[ly][1] * a1 + cD[ly][2] * a2;
-          o[96 + ly * 4] = cB[ly][0] * b0 + cB[ly][1] * b1 + cB[ly][2] * b2;
+        for (int iz = 0; iz < 3; ++iz) {
+          const float a0 = s0[(iz * 3 + 0) * 4], a1 = s0[(iz * 3 + 1) * 4], a2 = s0[(iz * 3 + 2) * 4];
+          const float b0 = s0[36 + (iz * 3 + 0) * 4], b1 = s0[36 + (iz * 3 + 1) * 4],
+                      b2 = s0[36 + (iz * 3 + 2) * 4];
+          o[0 + iz] = by0 * a0 + by1 * a1 + by2 * a2;  // vv
+          o[3 + iz] = dy0 * a0 + dy1 * a1 + dy2 * a2;  // vd
+          o[6 + iz] = by0 * b0 + by1 * b1 + by2 * b2;  // dv
         }
+        o[9] = o[10] = o[11] = 0.f;
+        float4* dst = reinterpret_cast<float4*>(S + oSY + f * 192 + yx * 12);
+        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+        dst[2] = make_float4(o[8], o[9], o[10], o[11]);
       }
     }
     group_sync(grp);
@@ -242,14 +236,13 @@ __global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
       float F[kNF][4];  // [field][val, d/dxi, d/deta, d/dzeta] at this Gauss point
 #pragma unroll
       for (int f = 0; f < kNF; ++f) {
-        const float* s = S + oSY + f * 144 + yx;
-        const float vv0 = s[0], vv1 = s[16], vv2 = s[32];
-        const float vd0 = s[48], vd1 = s[64], vd2 = s[80];
-        const float dv0 = s[96], dv1 = s[112], dv2 = s[128];
-        F[f][0] = bz0 * vv0 + bz1 * vv1 + bz2 * vv2;
-        F[f][1] = bz0 * dv0 + bz1 * dv1 + bz2 * dv2;
-        F[f][2] = bz0 * vd0 + bz1 * vd1 + bz2 * vd2;
-        F[f][3] = dz0 * vv0 + dz1 * vv1 + dz2 * vv2;
+        const float4* src = reinterpret_cast<const float4*>(S + oSY + f * 192 + yx * 12);
+        const float4 q0 = src[0], q1 = src[1], q2 = src[2];
+        // q0 = (vv0, vv1, vv2, vd0), q1 = (vd1, vd2, dv0, dv1), q2 = (dv2, -, -, -)
+        F[f][0] = bz0 * q0.x + bz1 * q0.y + bz2 * q0.z;
+        F[f][1] = bz0 * q1.z + bz1 * q1.w + bz2 * q2.x;
+        F[f][2] = bz0 * q0.w + bz1 * q1.x + bz2 * q1.y;
+        F[f][3] = dz0 * q0.x + dz1 * q0.y + dz2 * q0.z;
       }
       float J[3][3];
 #pragma unroll
@@ -290,24 +283,50 @@ __global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
       const float ik = 1.0f / A.k;
       if (A.mode == MODE_OPERATOR) {
         const float p = F[3][0];
+        // Q1 (pi) fields: trilinear in the vertex values, at this Gauss point
+        float PQ[4][4];  // [p, vx, vy, vz][val, d/dxi, d/deta, d/dzeta]
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const float* uf = S + oU + (3 + f) * 27;
+          float a[2][2], ax[2][2];
+#pragma unroll
+          for (int vz = 0; vz < 2; ++vz)
+#pragma unroll
+            for (int vy = 0; vy < 2; ++vy) {
+              const float g0 = uf[18 * vz + 6 * vy], g1 = uf[18 * vz + 6 * vy + 2];
+              a[vz][vy] = fmaf(lx1, g1 - g0, g0);
+              ax[vz][vy] = g1 - g0;
+            }
+          float b[2], bx[2], by[2];
+#pragma unroll
+          for (int vz = 0; vz < 2; ++vz) {
+            b[vz] = fmaf(ly1, a[vz][1] - a[vz][0], a[vz][0]);
+            bx[vz] = fmaf(ly1, ax[vz][1] - ax[vz][0], ax[vz][0]);
+            by[vz] = a[vz][1] - a[vz][0];
+          }
+          PQ[f][0] = fmaf(lz1, b[1] - b[0], b[0]);
+          PQ[f][1] = fmaf(lz1, bx[1] - bx[0], bx[0]);
+          PQ[f][2] = fmaf(lz1, by[1] - by[0], by[0]);
+          PQ[f][3] = b[1] - b[0];
+        }
         float gp[3], gpp[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           gp[j] = F[3][1] * Ji[0][j] + F[3][2] * Ji[1][j] + F[3][3] * Ji[2][j];
-          gpp[j] = F[7][1] * Ji[0][j] + F[7][2] * Ji[1][j] + F[7][3] * Ji[2][j];
+          gpp[j] = PQ[0][1] * Ji[0][j] + PQ[0][2] * Ji[1][j] + PQ[0][3] * Ji[2][j];
         }
         const bool use_d = A.convection && dT != 0.f;
         float g[3] = {0.f, 0.f, 0.f}, pvr[3] = {0.f, 0.f, 0.f};
         if (use_d) {
           float pv[3];
 #pragma unroll
-          for (int i = 0; i < 3; ++i) pv[i] = F[8 + i][0];
+          for (int i = 0; i < 3; ++i) pv[i] = PQ[1 + i][0];
 #pragma unroll
           for (int i = 0; i < 3; ++i) {
             float s = 0.f;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-              const float gpv = F[8 + i][1] * Ji[0][j] + F[8 + i][2] * Ji[1][j] + F[8 + i][3] * Ji[2][j];
+              const float gpv = PQ[1 + i][1] * Ji[0][j] + PQ[1 + i][2] * Ji[1][j] + PQ[1 + i][3] * Ji[2][j];
               s = fmaf(pv[j], gpv, s);
             }
             g[i] = conv[i] - s;

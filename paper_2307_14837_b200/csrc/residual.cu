@@ -56,22 +56,29 @@ __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[
 #undef QD
 
 // ---- per-cell shared-memory layout (floats) --------------------------------
+// One warp per cell; lanes take Gauss points q = lane and lane + 32 in the
+// pointwise phase and "lines" of the 1-D contractions in the other stages.
 // Q2 fields through the sum-factorised forward stages: X^x, X^y, X^z, p, vx, vy, vz.
 // The pi-projected (Q1) fields are trilinear in the 8 vertex values and are
 // evaluated per Gauss point directly from those (elements.py:96-118).
 constexpr int kNF = 7;
-constexpr int kGroup = 64;             // threads per cell (one per Gauss point)
 constexpr int oU = 0;                  // u[f][27]
 constexpr int oSX = 192;               // sx[f][2][9][4]          | backward tx[8][3][16][3]
-constexpr int oSY = oSX + kNF * 72;    // sy[f][16][12] = [yx][{vv,vd,dv} x iz, pad]
-constexpr int oCF = oSY + kNF * 192;   // cf[4][7][64]            |          ty[8][2][4][3][3]
-constexpr int oTZ = oCF + 4 * 7 * 64;  // tz[4][2][27]
-constexpr int oST = oTZ + 4 * 2 * 27;  // alpha, delta, vmax
-constexpr int kCellFloats = (oST + 4 + 3) / 4 * 4;
+constexpr int oSY = oSX + kNF * 72;    // sy[f][16][12]           |          ty[8][2][4][3][3]
+constexpr int oCF = oSY + kNF * 192;   // cf[22][64]: A[4], B[4][3], dg[3], pvr[3]
+constexpr int kNCF = 22;
+constexpr int oTZ = oCF + kNCF * 64;   // tz[4][2][27]
+constexpr int kCellFloats = (oTZ + 4 * 2 * 27 + 3) / 4 * 4;
 constexpr int oTX = oSX;
 constexpr int oTY = oSX + 4 * 2 * 3 * 48;
 static_assert(oTY + 4 * 2 * 2 * 36 <= oCF, "backward scratch must fit in the forward scratch");
 static_assert(oSX % 4 == 0 && oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
+// coefficient arrays
+constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
+constexpr int CB = 4;        // B[c][k]   reference-gradient test
+constexpr int CDG = 16;      // dg[i] = delta*w*g_i           (LPS, Gpi test, comps 1..3)
+constexpr int CPV = 19;      // pvr[k] = (J^-1 pi v)_k
+constexpr int kWarpsPerBlock = 5;
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
@@ -99,10 +106,6 @@ __host__ __device__ constexpr float pi_weight(int b, int v) {
   return w;
 }
 
-__device__ __forceinline__ void group_sync(int grp) {
-  asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(kGroup) : "memory");
-}
-
 struct NodePrefetch {
   float4 xv;
   float d0, d1, d2;
@@ -121,95 +124,207 @@ __device__ __forceinline__ NodePrefetch load_node(const ResidualArgs& A, int c, 
   return p;
 }
 
-template <int CPB>
-__global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
-  extern __shared__ __align__(16) float smem[];
-  const int grp = threadIdx.x / kGroup;
-  const int t = threadIdx.x % kGroup;
-  float* S = smem + grp * kCellFloats;
-  // this thread's Gauss point in the pointwise phase: q = qx + 4 qy + 16 qz
-  const int qx = t & 3, qy = (t >> 2) & 3, qz = t >> 4;
-  const float bz0 = cB[qz][0], bz1 = cB[qz][1], bz2 = cB[qz][2];
-  const float dz0 = cD[qz][0], dz1 = cD[qz][1], dz2 = cD[qz][2];
-  const float wq = cW[qx] * cW[qy] * cW[qz];
-  const float lx1 = cX[qx], ly1 = cX[qy], lz1 = cX[qz];  // Gauss coordinates: L1 = x, L0 = 1 - x
+// coefficients of one Gauss point (pointwise phase); F = Q2 fields at q
+__device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S, float* CF, int q,
+                                          float F[kNF][4], float aT, float dT) {
+  const int qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
+  float J[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) J[i][j] = F[i][1 + j];
+  const float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  const float c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  const float c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  const float det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+  const float id = 1.0f / det;
+  float Ji[3][3];  // (J^-1)[k][j]: reference k -> physical j
+  Ji[0][0] = c00 * id;
+  Ji[1][0] = c01 * id;
+  Ji[2][0] = c02 * id;
+  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+  const float w = cW[qx] * cW[qy] * cW[qz] * det;
+  float v[3], gv[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    v[i] = F[4 + i][0];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      gv[i][j] = F[4 + i][1] * Ji[0][j] + F[4 + i][2] * Ji[1][j] + F[4 + i][3] * Ji[2][j];
+  }
+  float conv[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    conv[i] = A.convection ? v[0] * gv[i][0] + v[1] * gv[i][1] + v[2] * gv[i][2] : 0.f;
+#define CFW(arr) CF[(arr) * 64 + q]
+  const float ik = 1.0f / A.k;
+  if (A.mode == MODE_OPERATOR) {
+    const float p = F[3][0];
+    // Q1 (pi) fields: trilinear in the vertex values, at this Gauss point
+    const float lx1 = cX[qx], ly1 = cX[qy], lz1 = cX[qz];
+    float PQ[4][4];  // [p, vx, vy, vz][val, d/dxi, d/deta, d/dzeta]
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const float* uf = S + oU + (3 + f) * 27;
+      float a[2][2], ax[2][2];
+#pragma unroll
+      for (int vz = 0; vz < 2; ++vz)
+#pragma unroll
+        for (int vy = 0; vy < 2; ++vy) {
+          const float g0 = uf[18 * vz + 6 * vy], g1 = uf[18 * vz + 6 * vy + 2];
+          a[vz][vy] = fmaf(lx1, g1 - g0, g0);
+          ax[vz][vy] = g1 - g0;
+        }
+      float b[2], bx[2], by[2];
+#pragma unroll
+      for (int vz = 0; vz < 2; ++vz) {
+        b[vz] = fmaf(ly1, a[vz][1] - a[vz][0], a[vz][0]);
+        bx[vz] = fmaf(ly1, ax[vz][1] - ax[vz][0], ax[vz][0]);
+        by[vz] = a[vz][1] - a[vz][0];
+      }
+      PQ[f][0] = fmaf(lz1, b[1] - b[0], b[0]);
+      PQ[f][1] = fmaf(lz1, bx[1] - bx[0], bx[0]);
+      PQ[f][2] = fmaf(lz1, by[1] - by[0], by[0]);
+      PQ[f][3] = b[1] - b[0];
+    }
+    float gp[3], gpp[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      gp[j] = F[3][1] * Ji[0][j] + F[3][2] * Ji[1][j] + F[3][3] * Ji[2][j];
+      gpp[j] = PQ[0][1] * Ji[0][j] + PQ[0][2] * Ji[1][j] + PQ[0][3] * Ji[2][j];
+    }
+    const bool use_d = A.convection && dT != 0.f;
+    float g[3] = {0.f, 0.f, 0.f}, pvr[3] = {0.f, 0.f, 0.f};
+    if (use_d) {
+      float pv[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) pv[i] = PQ[1 + i][0];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        float sacc = 0.f;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const float gpv = PQ[1 + i][1] * Ji[0][j] + PQ[1 + i][2] * Ji[1][j] + PQ[1 + i][3] * Ji[2][j];
+          sacc = fmaf(pv[j], gpv, sacc);
+        }
+        g[i] = conv[i] - sacc;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) pvr[kk] = Ji[kk][0] * pv[0] + Ji[kk][1] * pv[1] + Ji[kk][2] * pv[2];
+    }
+    const float div = gv[0][0] + gv[1][1] + gv[2][2];
+    float E[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) E[j] = aT * w * (gp[j] - gpp[j]);
+    CFW(CA + 0) = w * div;
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk) CFW(CB + kk) = Ji[kk][0] * E[0] + Ji[kk][1] * E[1] + Ji[kk][2] * E[2];
+    const float hn = 0.5f * A.nu * w;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      CFW(CA + 1 + i) = w * (v[i] * ik + 0.5f * conv[i]);
+      const float dg = dT * w * g[i];
+      CFW(CDG + i) = dg;
+      float Fi[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Fi[j] = hn * gv[i][j] + dg * v[j] - (i == j ? w * p : 0.f);
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk)
+        CFW(CB + 3 * (1 + i) + kk) = Ji[kk][0] * Fi[0] + Ji[kk][1] * Fi[1] + Ji[kk][2] * Fi[2];
+    }
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk) CFW(CPV + kk) = pvr[kk];
+  } else {  // MODE_RHS (assembly.py:242-259, f = None)
+    const float hn = -0.5f * A.nu * w;
+    CFW(CA + 0) = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk) CFW(CB + kk) = 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      CFW(CA + 1 + i) = w * (v[i] * ik - 0.5f * conv[i]);
+      CFW(CDG + i) = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk)
+        CFW(CB + 3 * (1 + i) + kk) =
+            hn * (Ji[kk][0] * gv[i][0] + Ji[kk][1] * gv[i][1] + Ji[kk][2] * gv[i][2]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk) CFW(CPV + kk) = 0.f;
+  }
+#undef CFW
+}
 
-  const int stride = gridDim.x * CPB;
-  int c = blockIdx.x * CPB + grp;
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualArgs A) {
+  extern __shared__ __align__(16) float smem[];
+  const int wib = threadIdx.x >> 5;
+  const int t = threadIdx.x & 31;
+  float* S = smem + wib * kCellFloats;
+  const int stride = gridDim.x * kWarpsPerBlock;
+  int c = blockIdx.x * kWarpsPerBlock + wib;
   NodePrefetch pf;
   if (t < 27 && c < A.n_cells) pf = load_node(A, c, t);
 
-  for (; c - grp < A.n_cells; c += stride) {
-    const bool live = c < A.n_cells;
-    // ---------------- gather (prefetched) ----------------
+  for (; c < A.n_cells; c += stride) {
+    // ---------------- gather (prefetched), stab ----------------
     float vmag = 0.f;
     if (t < 27) {
-      if (live) {
-        S[oU + 0 * 27 + t] = pf.d0;
-        S[oU + 1 * 27 + t] = pf.d1;
-        S[oU + 2 * 27 + t] = pf.d2;
-        S[oU + 3 * 27 + t] = pf.xv.x;
-        S[oU + 4 * 27 + t] = pf.xv.y;
-        S[oU + 5 * 27 + t] = pf.xv.z;
-        S[oU + 6 * 27 + t] = pf.xv.w;
-        vmag = sqrtf(pf.xv.y * pf.xv.y + pf.xv.z * pf.xv.z + pf.xv.w * pf.xv.w);
-      } else {  // padding cell: unit reference cube, zero state (never written out)
-        S[oU + 0 * 27 + t] = 0.5f * (t % 3);
-        S[oU + 1 * 27 + t] = 0.5f * ((t / 3) % 3);
-        S[oU + 2 * 27 + t] = 0.5f * (t / 9);
+      S[oU + 0 * 27 + t] = pf.d0;
+      S[oU + 1 * 27 + t] = pf.d1;
+      S[oU + 2 * 27 + t] = pf.d2;
+      S[oU + 3 * 27 + t] = pf.xv.x;
+      S[oU + 4 * 27 + t] = pf.xv.y;
+      S[oU + 5 * 27 + t] = pf.xv.z;
+      S[oU + 6 * 27 + t] = pf.xv.w;
+      vmag = sqrtf(pf.xv.y * pf.xv.y + pf.xv.z * pf.xv.z + pf.xv.w * pf.xv.w);
+      if (c + stride < A.n_cells) pf = load_node(A, c + stride, t);  // overlap the next cell
+    }
 #pragma unroll
-        for (int f = 3; f < 7; ++f) S[oU + f * 27 + t] = 0.f;
-      }
-      if (c + stride < A.n_cells) pf = load_node(A, c + stride, t);  // overlap next cell
+    for (int off = 16; off > 0; off >>= 1) vmag = fmaxf(vmag, __shfl_xor_sync(0xffffffffu, vmag, off));
+    float aT, dT;
+    if (A.alpha_in) {
+      aT = A.alpha_in[c];
+      dT = A.delta_in[c];
+    } else {  // stab at x (assembly.py:55-59, 169-178)
+      const float h = A.h_T[c];
+      const float den = A.nu / (h * h) + vmag / h + 1.0f / A.k;
+      aT = A.alpha0 / den;
+      dT = A.delta0 / den;
     }
-    if (t < 32) {  // vmax over the 27 nodes (assembly.py:169-172)
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) vmag = fmaxf(vmag, __shfl_xor_sync(0xffffffffu, vmag, off));
-      if (t == 0) S[oST + 2] = vmag;
-    }
-    group_sync(grp);
-    if (t == 32) {
-      float aT = 0.f, dT = 0.f;
-      if (live) {
-        if (A.alpha_in) {
-          aT = A.alpha_in[c];
-          dT = A.delta_in[c];
-        } else {
-          const float h = A.h_T[c];
-          const float den = A.nu / (h * h) + S[oST + 2] / h + 1.0f / A.k;
-          aT = A.alpha0 / den;
-          dT = A.delta0 / den;
-        }
-      }
-      S[oST + 0] = aT;
-      S[oST + 1] = dT;
-    }
-    group_sync(grp);
-    // ---------------- forward x: sx[f][kind][izy][qx] (float4 over qx) ----------------
-    if (t < kNF * 9) {
-      const int f = t / 9, izy = t - 9 * (t / 9);
-      const float* u = S + oU + f * 27 + izy * 3;
-      const float u0 = u[0], u1 = u[1], u2 = u[2];
-      float4 vb, vd;
-      vb.x = cB[0][0] * u0 + cB[0][1] * u1 + cB[0][2] * u2;
-      vb.y = cB[1][0] * u0 + cB[1][1] * u1 + cB[1][2] * u2;
-      vb.z = cB[2][0] * u0 + cB[2][1] * u1 + cB[2][2] * u2;
-      vb.w = cB[3][0] * u0 + cB[3][1] * u1 + cB[3][2] * u2;
-      vd.x = cD[0][0] * u0 + cD[0][1] * u1 + cD[0][2] * u2;
-      vd.y = cD[1][0] * u0 + cD[1][1] * u1 + cD[1][2] * u2;
-      vd.z = cD[2][0] * u0 + cD[2][1] * u1 + cD[2][2] * u2;
-      vd.w = cD[3][0] * u0 + cD[3][1] * u1 + cD[3][2] * u2;
-      *reinterpret_cast<float4*>(S + oSX + f * 72 + izy * 4) = vb;
-      *reinterpret_cast<float4*>(S + oSX + f * 72 + 36 + izy * 4) = vd;
-    }
-    group_sync(grp);
-    // ---------------- forward y: line (f, qy, qx) -> sy[f][qy*4+qx][kind*3+iz] ----------------
+    __syncwarp();
+    // ---------------- forward x: line (f, izy) -> sx[f][kind][izy][qx] ----------------
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const int l = t + 64 * r;
+      const int l = t + 32 * r;
+      if (l < kNF * 9) {
+        const int f = l / 9, izy = l - 9 * (l / 9);
+        const float* u = S + oU + f * 27 + izy * 3;
+        const float u0 = u[0], u1 = u[1], u2 = u[2];
+        float4 vb, vd;
+        vb.x = cB[0][0] * u0 + cB[0][1] * u1 + cB[0][2] * u2;
+        vb.y = cB[1][0] * u0 + cB[1][1] * u1 + cB[1][2] * u2;
+        vb.z = cB[2][0] * u0 + cB[2][1] * u1 + cB[2][2] * u2;
+        vb.w = cB[3][0] * u0 + cB[3][1] * u1 + cB[3][2] * u2;
+        vd.x = cD[0][0] * u0 + cD[0][1] * u1 + cD[0][2] * u2;
+        vd.y = cD[1][0] * u0 + cD[1][1] * u1 + cD[1][2] * u2;
+        vd.z = cD[2][0] * u0 + cD[2][1] * u1 + cD[2][2] * u2;
+        vd.w = cD[3][0] * u0 + cD[3][1] * u1 + cD[3][2] * u2;
+        *reinterpret_cast<float4*>(S + oSX + f * 72 + izy * 4) = vb;
+        *reinterpret_cast<float4*>(S + oSX + f * 72 + 36 + izy * 4) = vd;
+      }
+    }
+    __syncwarp();
+    // ---------------- forward y: line (f, qy, qx) -> sy[f][qy*4+qx][kind*3+iz] ----------------
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int l = t + 32 * r;
       if (l < kNF * 16) {
         const int f = l >> 4, yx = l & 15, ly = yx >> 2, lx = yx & 3;
-        const float* s0 = S + oSX + f * 72 + lx;  // [kind*36 + (iz*3+iy)*4]
+        const float* s0 = S + oSX + f * 72 + lx;
         const float by0 = cB[ly][0], by1 = cB[ly][1], by2 = cB[ly][2];
         const float dy0 = cD[ly][0], dy1 = cD[ly][1], dy2 = cD[ly][2];
         float o[12];
@@ -218,9 +333,9 @@ __global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
           const float a0 = s0[(iz * 3 + 0) * 4], a1 = s0[(iz * 3 + 1) * 4], a2 = s0[(iz * 3 + 2) * 4];
           const float b0 = s0[36 + (iz * 3 + 0) * 4], b1 = s0[36 + (iz * 3 + 1) * 4],
                       b2 = s0[36 + (iz * 3 + 2) * 4];
-          o[0 + iz] = by0 * a0 + by1 * a1 + by2 * a2;  // vv
-          o[3 + iz] = dy0 * a0 + dy1 * a1 + dy2 * a2;  // vd
-          o[6 + iz] = by0 * b0 + by1 * b1 + by2 * b2;  // dv
+          o[0 + iz] = by0 * a0 + by1 * a1 + by2 * a2;
+          o[3 + iz] = dy0 * a0 + dy1 * a1 + dy2 * a2;
+          o[6 + iz] = by0 * b0 + by1 * b1 + by2 * b2;
         }
         o[9] = o[10] = o[11] = 0.f;
         float4* dst = reinterpret_cast<float4*>(S + oSY + f * 192 + yx * 12);
@@ -229,258 +344,147 @@ __global__ void __launch_bounds__(64 * CPB, 2) element_kernel(ResidualArgs A) {
         dst[2] = make_float4(o[8], o[9], o[10], o[11]);
       }
     }
-    group_sync(grp);
-    // ---------------- forward z fused with the pointwise phase (thread = q) ----------------
-    {
-      const int yx = t & 15;
-      float F[kNF][4];  // [field][val, d/dxi, d/deta, d/dzeta] at this Gauss point
+    __syncwarp();
+    // ---------------- forward z + pointwise: Gauss points q = t, t + 32 ----------------
+#pragma unroll 1
+    for (int r = 0; r < 2; ++r) {
+      const int q = t + 32 * r;
+      const int yx = q & 15, qz = q >> 4;
+      const float bz0 = cB[qz][0], bz1 = cB[qz][1], bz2 = cB[qz][2];
+      const float dz0 = cD[qz][0], dz1 = cD[qz][1], dz2 = cD[qz][2];
+      float F[kNF][4];
 #pragma unroll
       for (int f = 0; f < kNF; ++f) {
         const float4* src = reinterpret_cast<const float4*>(S + oSY + f * 192 + yx * 12);
         const float4 q0 = src[0], q1 = src[1], q2 = src[2];
-        // q0 = (vv0, vv1, vv2, vd0), q1 = (vd1, vd2, dv0, dv1), q2 = (dv2, -, -, -)
+        // q0 = (vv0, vv1, vv2, vd0), q1 = (vd1, vd2, dv0, dv1), q2 = (dv2, ., ., .)
         F[f][0] = bz0 * q0.x + bz1 * q0.y + bz2 * q0.z;
         F[f][1] = bz0 * q1.z + bz1 * q1.w + bz2 * q2.x;
         F[f][2] = bz0 * q0.w + bz1 * q1.x + bz2 * q1.y;
         F[f][3] = dz0 * q0.x + dz1 * q0.y + dz2 * q0.z;
       }
-      float J[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) J[i][j] = F[i][1 + j];
-      const float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-      const float c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-      const float c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-      const float det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-      const float id = 1.0f / det;
-      float Ji[3][3];  // (J^-1)[k][j]: reference k -> physical j
-      Ji[0][0] = c00 * id;
-      Ji[1][0] = c01 * id;
-      Ji[2][0] = c02 * id;
-      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
-      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
-      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
-      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
-      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
-      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
-      const float w = wq * det;
-      const float aT = S[oST + 0], dT = S[oST + 1];
-      float v[3], gv[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        v[i] = F[4 + i][0];
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          gv[i][j] = F[4 + i][1] * Ji[0][j] + F[4 + i][2] * Ji[1][j] + F[4 + i][3] * Ji[2][j];
-      }
-      float conv[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-        conv[i] = A.convection ? v[0] * gv[i][0] + v[1] * gv[i][1] + v[2] * gv[i][2] : 0.f;
-      float* C = S + oCF + t;
-#define CF(comp, arr) C[((comp) * 7 + (arr)) * 64]
-      const float ik = 1.0f / A.k;
-      if (A.mode == MODE_OPERATOR) {
-        const float p = F[3][0];
-        // Q1 (pi) fields: trilinear in the vertex values, at this Gauss point
-        float PQ[4][4];  // [p, vx, vy, vz][val, d/dxi, d/deta, d/dzeta]
-#pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          const float* uf = S + oU + (3 + f) * 27;
-          float a[2][2], ax[2][2];
-#pragma unroll
-          for (int vz = 0; vz < 2; ++vz)
-#pragma unroll
-            for (int vy = 0; vy < 2; ++vy) {
-              const float g0 = uf[18 * vz + 6 * vy], g1 = uf[18 * vz + 6 * vy + 2];
-              a[vz][vy] = fmaf(lx1, g1 - g0, g0);
-              ax[vz][vy] = g1 - g0;
-            }
-          float b[2], bx[2], by[2];
-#pragma unroll
-          for (int vz = 0; vz < 2; ++vz) {
-            b[vz] = fmaf(ly1, a[vz][1] - a[vz][0], a[vz][0]);
-            bx[vz] = fmaf(ly1, ax[vz][1] - ax[vz][0], ax[vz][0]);
-            by[vz] = a[vz][1] - a[vz][0];
-          }
-          PQ[f][0] = fmaf(lz1, b[1] - b[0], b[0]);
-          PQ[f][1] = fmaf(lz1, bx[1] - bx[0], bx[0]);
-          PQ[f][2] = fmaf(lz1, by[1] - by[0], by[0]);
-          PQ[f][3] = b[1] - b[0];
-        }
-        float gp[3], gpp[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          gp[j] = F[3][1] * Ji[0][j] + F[3][2] * Ji[1][j] + F[3][3] * Ji[2][j];
-          gpp[j] = PQ[0][1] * Ji[0][j] + PQ[0][2] * Ji[1][j] + PQ[0][3] * Ji[2][j];
-        }
-        const bool use_d = A.convection && dT != 0.f;
-        float g[3] = {0.f, 0.f, 0.f}, pvr[3] = {0.f, 0.f, 0.f};
-        if (use_d) {
-          float pv[3];
-#pragma unroll
-          for (int i = 0; i < 3; ++i) pv[i] = PQ[1 + i][0];
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            float s = 0.f;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              const float gpv = PQ[1 + i][1] * Ji[0][j] + PQ[1 + i][2] * Ji[1][j] + PQ[1 + i][3] * Ji[2][j];
-              s = fmaf(pv[j], gpv, s);
-            }
-            g[i] = conv[i] - s;
-          }
-#pragma unroll
-          for (int kk = 0; kk < 3; ++kk)
-            pvr[kk] = Ji[kk][0] * pv[0] + Ji[kk][1] * pv[1] + Ji[kk][2] * pv[2];
-        }
-        const float div = gv[0][0] + gv[1][1] + gv[2][2];
-        float E[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) E[j] = aT * w * (gp[j] - gpp[j]);
-        CF(0, 0) = w * div;
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk) {
-          const float b = Ji[kk][0] * E[0] + Ji[kk][1] * E[1] + Ji[kk][2] * E[2];
-          CF(0, 1 + kk) = b;
-          CF(0, 4 + kk) = -b;
-        }
-        const float hn = 0.5f * A.nu * w;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          CF(1 + i, 0) = w * (v[i] * ik + 0.5f * conv[i]);
-          const float dg = dT * w * g[i];
-          float Fi[3];
-#pragma unroll
-          for (int j = 0; j < 3; ++j) Fi[j] = hn * gv[i][j] + dg * v[j] - (i == j ? w * p : 0.f);
-#pragma unroll
-          for (int kk = 0; kk < 3; ++kk) {
-            CF(1 + i, 1 + kk) = Ji[kk][0] * Fi[0] + Ji[kk][1] * Fi[1] + Ji[kk][2] * Fi[2];
-            CF(1 + i, 4 + kk) = -dg * pvr[kk];
-          }
-        }
-      } else {  // MODE_RHS (assembly.py:242-259, f = None)
-        const float hn = -0.5f * A.nu * w;
-#pragma unroll
-        for (int a = 0; a < 7; ++a) CF(0, a) = 0.f;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          CF(1 + i, 0) = w * (v[i] * ik - 0.5f * conv[i]);
-#pragma unroll
-          for (int kk = 0; kk < 3; ++kk) {
-            CF(1 + i, 1 + kk) =
-                hn * (Ji[kk][0] * gv[i][0] + Ji[kk][1] * gv[i][1] + Ji[kk][2] * gv[i][2]);
-            CF(1 + i, 4 + kk) = 0.f;
-          }
-        }
-      }
-#undef CF
+      pointwise(A, S, S + oCF, q, F, aT, dT);
     }
-    group_sync(grp);
+    __syncwarp();
     // ---------------- backward x (contract qx): line (comp, part, zy) ----------------
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int l = t + 64 * r;
+    for (int r = 0; r < 4; ++r) {
+      const int l = t + 32 * r;
       const int comp = l >> 5, part = (l >> 4) & 1, zy = l & 15;
-      const float* cf = S + oCF + comp * 7 * 64 + zy * 4;
-      float4 a4, b0, b1, b2;
+      const float* cf = S + oCF + zy * 4;
+      float Av[4], B0[4], B1[4], B2[4];
       if (part == 0) {
-        a4 = *reinterpret_cast<const float4*>(cf);
-        b0 = *reinterpret_cast<const float4*>(cf + 64);
-        b1 = *reinterpret_cast<const float4*>(cf + 128);
-        b2 = *reinterpret_cast<const float4*>(cf + 192);
-      } else {
-        a4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        b0 = *reinterpret_cast<const float4*>(cf + 256);
-        b1 = *reinterpret_cast<const float4*>(cf + 320);
-        b2 = *reinterpret_cast<const float4*>(cf + 384);
+        const float4 a4 = *reinterpret_cast<const float4*>(cf + (CA + comp) * 64);
+        const float4 x4 = *reinterpret_cast<const float4*>(cf + (CB + 3 * comp) * 64);
+        const float4 y4 = *reinterpret_cast<const float4*>(cf + (CB + 3 * comp + 1) * 64);
+        const float4 z4 = *reinterpret_cast<const float4*>(cf + (CB + 3 * comp + 2) * 64);
+        Av[0] = a4.x; Av[1] = a4.y; Av[2] = a4.z; Av[3] = a4.w;
+        B0[0] = x4.x; B0[1] = x4.y; B0[2] = x4.z; B0[3] = x4.w;
+        B1[0] = y4.x; B1[1] = y4.y; B1[2] = y4.z; B1[3] = y4.w;
+        B2[0] = z4.x; B2[1] = z4.y; B2[2] = z4.z; B2[3] = z4.w;
+      } else if (comp == 0) {  // continuity LPS: (G - Gpi) test -> Gpi part is -B_0
+        const float4 x4 = *reinterpret_cast<const float4*>(cf + (CB + 0) * 64);
+        const float4 y4 = *reinterpret_cast<const float4*>(cf + (CB + 1) * 64);
+        const float4 z4 = *reinterpret_cast<const float4*>(cf + (CB + 2) * 64);
+        Av[0] = Av[1] = Av[2] = Av[3] = 0.f;
+        B0[0] = -x4.x; B0[1] = -x4.y; B0[2] = -x4.z; B0[3] = -x4.w;
+        B1[0] = -y4.x; B1[1] = -y4.y; B1[2] = -y4.z; B1[3] = -y4.w;
+        B2[0] = -z4.x; B2[1] = -z4.y; B2[2] = -z4.z; B2[3] = -z4.w;
+      } else {  // momentum LPS: -delta*w*g_i (J^-1 pi v) through the Gpi test
+        const float4 g4 = *reinterpret_cast<const float4*>(cf + (CDG + comp - 1) * 64);
+        const float4 p0 = *reinterpret_cast<const float4*>(cf + (CPV + 0) * 64);
+        const float4 p1 = *reinterpret_cast<const float4*>(cf + (CPV + 1) * 64);
+        const float4 p2 = *reinterpret_cast<const float4*>(cf + (CPV + 2) * 64);
+        const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
+        const float a0[4] = {p0.x, p0.y, p0.z, p0.w};
+        const float a1[4] = {p1.x, p1.y, p1.z, p1.w};
+        const float a2[4] = {p2.x, p2.y, p2.z, p2.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          Av[i] = 0.f;
+          B0[i] = -gg[i] * a0[i];
+          B1[i] = -gg[i] * a1[i];
+          B2[i] = -gg[i] * a2[i];
+        }
       }
-      const float Av[4] = {a4.x, a4.y, a4.z, a4.w};
-      const float B0[4] = {b0.x, b0.y, b0.z, b0.w};
-      const float B1[4] = {b1.x, b1.y, b1.z, b1.w};
-      const float B2[4] = {b2.x, b2.y, b2.z, b2.w};
       float* o = S + oTX + ((comp * 2 + part) * 3) * 48 + zy * 3;
 #pragma unroll
       for (int ix = 0; ix < 3; ++ix) {
         float tv = 0.f, t1 = 0.f, t2 = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          tv += cB[q][ix] * Av[q] + cD[q][ix] * B0[q];
-          t1 += cB[q][ix] * B1[q];
-          t2 += cB[q][ix] * B2[q];
+        for (int qq = 0; qq < 4; ++qq) {
+          tv += cB[qq][ix] * Av[qq] + cD[qq][ix] * B0[qq];
+          t1 += cB[qq][ix] * B1[qq];
+          t2 += cB[qq][ix] * B2[qq];
         }
         o[ix] = tv;
         o[48 + ix] = t1;
         o[96 + ix] = t2;
       }
     }
-    group_sync(grp);
+    __syncwarp();
     // ---------------- backward y (contract qy): line (cp, qz, ix) ----------------
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int l = t + 64 * r;
-      if (l < 4 * 2 * 12) {
-        const int cp = l / 12, rr = l - 12 * (l / 12), lz = rr / 3, ix = rr - 3 * (rr / 3);
-        const float* tx = S + oTX + cp * 3 * 48 + lz * 12 + ix;  // [arr*48 + qy*3]
-        float* o = S + oTY + cp * 2 * 36 + lz * 9 + ix;
+    for (int r = 0; r < 3; ++r) {
+      const int l = t + 32 * r;
+      const int cp = l / 12, rr = l - 12 * (l / 12), lz = rr / 3, ix = rr - 3 * (rr / 3);
+      const float* tx = S + oTX + cp * 3 * 48 + lz * 12 + ix;
+      float* o = S + oTY + cp * 2 * 36 + lz * 9 + ix;
 #pragma unroll
-        for (int iy = 0; iy < 3; ++iy) {
-          float ua = 0.f, ub = 0.f;
+      for (int iy = 0; iy < 3; ++iy) {
+        float ua = 0.f, ub = 0.f;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            ua += cB[q][iy] * tx[q * 3] + cD[q][iy] * tx[48 + q * 3];
-            ub += cB[q][iy] * tx[96 + q * 3];
-          }
-          o[iy * 3] = ua;
-          o[36 + iy * 3] = ub;
+        for (int qq = 0; qq < 4; ++qq) {
+          ua += cB[qq][iy] * tx[qq * 3] + cD[qq][iy] * tx[48 + qq * 3];
+          ub += cB[qq][iy] * tx[96 + qq * 3];
         }
+        o[iy * 3] = ua;
+        o[36 + iy * 3] = ub;
       }
     }
-    group_sync(grp);
+    __syncwarp();
     // ---------------- backward z (contract qz): line (cp, yx) ----------------
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int l = t + 64 * r;
+    for (int r = 0; r < 3; ++r) {
+      const int l = t + 32 * r;
       if (l < 4 * 2 * 9) {
         const int cp = l / 9, yx = l - 9 * (l / 9);
-        const float* ty = S + oTY + cp * 2 * 36 + yx;  // [arr*36 + qz*9]
+        const float* ty = S + oTY + cp * 2 * 36 + yx;
         float* o = S + oTZ + cp * 27 + yx;
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz) {
-          float s = 0.f;
+          float sacc = 0.f;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) s += cB[q][iz] * ty[q * 9] + cD[q][iz] * ty[36 + q * 9];
-          o[iz * 9] = s;
+          for (int qq = 0; qq < 4; ++qq) sacc += cB[qq][iz] * ty[qq * 9] + cD[qq][iz] * ty[36 + qq * 9];
+          o[iz * 9] = sacc;
         }
       }
     }
-    group_sync(grp);
+    __syncwarp();
     // ---------------- output: direct + PI^T * (LPS part), one float4 per node ----------------
-    if (t < 27 && live) {
+    if (t < 27) {
       float e[4];
-      const bool vertex = (t % 3 != 1) && ((t / 3) % 3 != 1) && (t / 9 != 1);
+      const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
+      const bool vertex = it0 != 1 && it1 != 1 && it2 != 1;
 #pragma unroll
       for (int comp = 0; comp < 4; ++comp) {
-        float s = S[oTZ + (comp * 2) * 27 + t];
+        float sacc = S[oTZ + (comp * 2) * 27 + t];
         if (vertex) {
           const float* gp = S + oTZ + (comp * 2 + 1) * 27;
 #pragma unroll
           for (int b = 0; b < 27; ++b) {
-            // PI[b][t] for vertex t: 1 at the vertex, 1/2^m for nodes between
             const int ib0 = b % 3, ib1 = (b / 3) % 3, ib2 = b / 9;
-            const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
-            const float w = (ib0 == 1 ? 0.5f : (ib0 == it0 ? 1.f : 0.f)) *
-                            (ib1 == 1 ? 0.5f : (ib1 == it1 ? 1.f : 0.f)) *
-                            (ib2 == 1 ? 0.5f : (ib2 == it2 ? 1.f : 0.f));
-            s = fmaf(w, gp[b], s);
+            const float wgt = (ib0 == 1 ? 0.5f : (ib0 == it0 ? 1.f : 0.f)) *
+                              (ib1 == 1 ? 0.5f : (ib1 == it1 ? 1.f : 0.f)) *
+                              (ib2 == 1 ? 0.5f : (ib2 == it2 ? 1.f : 0.f));
+            sacc = fmaf(wgt, gp[b], sacc);
           }
         }
-        e[comp] = s;
+        e[comp] = sacc;
       }
       A.elem[(int64_t)c * 27 + t] = make_float4(e[0], e[1], e[2], e[3]);
     }
-    // the next cell's gather writes only u, which no later stage of this cell reads
+    __syncwarp();
   }
 }
 
@@ -535,7 +539,6 @@ __global__ void __launch_bounds__(256) stab_kernel(int n_cells, const int32_t* _
   }
 }
 
-constexpr int kCPB = 4;
 
 static int32_t check_level(const dnnmg_level_t* lv, const char* who) {
   DNNMG_REQUIRE(lv && lv->cell_nodes && lv->coords && lv->h_T && lv->node_cell_ptr &&
@@ -562,18 +565,20 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
   A.convection = ph->convection;
   A.mode = mode;
   A.elem = reinterpret_cast<float4*>(elem);
-  const size_t smem = sizeof(float) * kCellFloats * kCPB;
+  const size_t smem = sizeof(float) * kCellFloats * kWarpsPerBlock;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(element_kernel<kCPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(element_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     configured = true;
   }
-  int blocks = (lv->n_cells + kCPB - 1) / kCPB;
-  const int cap = kSMs * 2;
+  int blocks = (lv->n_cells + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel, 32 * kWarpsPerBlock, smem);
+  const int cap = kSMs * (per_sm > 0 ? per_sm : 1);
   if (blocks > cap) blocks = cap;
   if (lv->n_cells == 0) return DNNMG_OK;
-  element_kernel<kCPB><<<blocks, 64 * kCPB, smem, s>>>(A);
+  element_kernel<<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
   DNNMG_CHECK_LAUNCH("element_kernel");
   return DNNMG_OK;
 }

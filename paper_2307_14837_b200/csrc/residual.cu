@@ -64,21 +64,24 @@ __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[
 constexpr int kNF = 7;
 constexpr int oU = 0;                  // u[f][27]
 constexpr int oSX = 192;               // sx[f][2][9][4]          | backward tx[8][3][16][3]
-constexpr int oSY = oSX + kNF * 72;    // sy[f][16][12]           |          ty[8][2][4][3][3]
-constexpr int oCF = oSY + kNF * 192;   // cf[22][64]: A[4], B[4][3], dg[3], pvr[3]
+constexpr int oSY = oSX + kNF * 72;    // sy[f][kind*3+iz][16 yx] |          ty[8][2][4][3][3]
+constexpr int oCF = oSX + kNF * 216;   // cf[22][64]: A[4], B[4][3], dg[3], pvr[3]
 constexpr int kNCF = 22;
 constexpr int oTZ = oCF + kNCF * 64;   // tz[4][2][27]
 constexpr int kCellFloats = (oTZ + 4 * 2 * 27 + 3) / 4 * 4;
-constexpr int oTX = oSX;
-constexpr int oTY = oSX + 4 * 2 * 3 * 48;
-static_assert(oTY + 4 * 2 * 2 * 36 <= oCF, "backward scratch must fit in the forward scratch");
+constexpr int kTXS = 172;             // per (comp, part) stride of tx: 144 + pad, = 12 (mod 32)
+constexpr int kTYS = 76;              // per (comp, part) stride of ty: 72 + pad,  = 12 (mod 32)
+constexpr int oTX = oSX;              // tx aliases the forward scratch (dead after pointwise)
+constexpr int oTY = oCF;              // ty aliases cf (dead after backward x)
+static_assert(oTX + 8 * kTXS <= oCF, "tx must fit in the forward scratch");
+static_assert(8 * kTYS <= kNCF * 64, "ty must fit in the coefficient region");
 static_assert(oSX % 4 == 0 && oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 // coefficient arrays
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
 constexpr int CB = 4;        // B[c][k]   reference-gradient test
 constexpr int CDG = 16;      // dg[i] = delta*w*g_i           (LPS, Gpi test, comps 1..3)
 constexpr int CPV = 19;      // pvr[k] = (J^-1 pi v)_k
-constexpr int kWarpsPerBlock = 5;
+constexpr int kWarpsPerBlock = 4;
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
@@ -106,22 +109,28 @@ __host__ __device__ constexpr float pi_weight(int b, int v) {
   return w;
 }
 
-struct NodePrefetch {
+// two-deep software pipeline of the node gather: the index of cell i+2 and the
+// raw (unconsumed) coordinates/state of cell i+1 are in flight while cell i computes
+struct NodeRaw {
+  double X[3], X0[3];
   float4 xv;
-  float d0, d1, d2;
+  float hT;
 };
 
-__device__ __forceinline__ NodePrefetch load_node(const ResidualArgs& A, int c, int t) {
-  NodePrefetch p;
-  const int node = __ldg(A.cell_nodes + (int64_t)c * 27 + t);
-  const int n0 = __ldg(A.cell_nodes + (int64_t)c * 27);
+__device__ __forceinline__ void load_raw(const ResidualArgs& A, int c, int node, int t, NodeRaw& r) {
+  const int n0 = __shfl_sync(0xffffffffu, node, 0);
   const double* X = A.coords + 3 * (int64_t)node;
   const double* X0 = A.coords + 3 * (int64_t)n0;
-  p.d0 = float(__ldg(X) - __ldg(X0));
-  p.d1 = float(__ldg(X + 1) - __ldg(X0 + 1));
-  p.d2 = float(__ldg(X + 2) - __ldg(X0 + 2));
-  p.xv = __ldg(A.x + node);
-  return p;
+  if (t < 27) {
+    r.X[0] = __ldg(X);
+    r.X[1] = __ldg(X + 1);
+    r.X[2] = __ldg(X + 2);
+    r.X0[0] = __ldg(X0);
+    r.X0[1] = __ldg(X0 + 1);
+    r.X0[2] = __ldg(X0 + 2);
+    r.xv = __ldg(A.x + node);
+  }
+  r.hT = __ldg(A.h_T + c);
 }
 
 // coefficients of one Gauss point (pointwise phase); F = Q2 fields at q
@@ -266,22 +275,32 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
   float* S = smem + wib * kCellFloats;
   const int stride = gridDim.x * kWarpsPerBlock;
   int c = blockIdx.x * kWarpsPerBlock + wib;
-  NodePrefetch pf;
-  if (t < 27 && c < A.n_cells) pf = load_node(A, c, t);
+  NodeRaw raw;
+  int idx_next = 0;  // node index of cell c + stride (lane t < 27)
+  if (c < A.n_cells) {
+    const int node = t < 27 ? __ldg(A.cell_nodes + (int64_t)c * 27 + t) : 0;
+    load_raw(A, c, node, t, raw);
+    if (c + stride < A.n_cells && t < 27) idx_next = __ldg(A.cell_nodes + (int64_t)(c + stride) * 27 + t);
+  }
 
   for (; c < A.n_cells; c += stride) {
-    // ---------------- gather (prefetched), stab ----------------
+    // ---------------- gather (prefetched one cell ahead), stab ----------------
     float vmag = 0.f;
     if (t < 27) {
-      S[oU + 0 * 27 + t] = pf.d0;
-      S[oU + 1 * 27 + t] = pf.d1;
-      S[oU + 2 * 27 + t] = pf.d2;
-      S[oU + 3 * 27 + t] = pf.xv.x;
-      S[oU + 4 * 27 + t] = pf.xv.y;
-      S[oU + 5 * 27 + t] = pf.xv.z;
-      S[oU + 6 * 27 + t] = pf.xv.w;
-      vmag = sqrtf(pf.xv.y * pf.xv.y + pf.xv.z * pf.xv.z + pf.xv.w * pf.xv.w);
-      if (c + stride < A.n_cells) pf = load_node(A, c + stride, t);  // overlap the next cell
+      S[oU + 0 * 27 + t] = float(raw.X[0] - raw.X0[0]);
+      S[oU + 1 * 27 + t] = float(raw.X[1] - raw.X0[1]);
+      S[oU + 2 * 27 + t] = float(raw.X[2] - raw.X0[2]);
+      S[oU + 3 * 27 + t] = raw.xv.x;
+      S[oU + 4 * 27 + t] = raw.xv.y;
+      S[oU + 5 * 27 + t] = raw.xv.z;
+      S[oU + 6 * 27 + t] = raw.xv.w;
+      vmag = sqrtf(raw.xv.y * raw.xv.y + raw.xv.z * raw.xv.z + raw.xv.w * raw.xv.w);
+    }
+    const float hT = raw.hT;
+    if (c + stride < A.n_cells) {  // issue the loads of the next cell (consumed next iteration)
+      load_raw(A, c + stride, idx_next, t, raw);
+      if (c + 2 * stride < A.n_cells && t < 27)
+        idx_next = __ldg(A.cell_nodes + (int64_t)(c + 2 * stride) * 27 + t);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) vmag = fmaxf(vmag, __shfl_xor_sync(0xffffffffu, vmag, off));
@@ -290,7 +309,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
       aT = A.alpha_in[c];
       dT = A.delta_in[c];
     } else {  // stab at x (assembly.py:55-59, 169-178)
-      const float h = A.h_T[c];
+      const float h = hT;
       const float den = A.nu / (h * h) + vmag / h + 1.0f / A.k;
       aT = A.alpha0 / den;
       dT = A.delta0 / den;
@@ -327,7 +346,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
         const float* s0 = S + oSX + f * 72 + lx;
         const float by0 = cB[ly][0], by1 = cB[ly][1], by2 = cB[ly][2];
         const float dy0 = cD[ly][0], dy1 = cD[ly][1], dy2 = cD[ly][2];
-        float o[12];
+        float o[9];
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz) {
           const float a0 = s0[(iz * 3 + 0) * 4], a1 = s0[(iz * 3 + 1) * 4], a2 = s0[(iz * 3 + 2) * 4];
@@ -337,11 +356,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
           o[3 + iz] = dy0 * a0 + dy1 * a1 + dy2 * a2;
           o[6 + iz] = by0 * b0 + by1 * b1 + by2 * b2;
         }
-        o[9] = o[10] = o[11] = 0.f;
-        float4* dst = reinterpret_cast<float4*>(S + oSY + f * 192 + yx * 12);
-        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
-        dst[2] = make_float4(o[8], o[9], o[10], o[11]);
+        float* dst = S + oSY + f * 144 + yx;
+#pragma unroll
+        for (int m = 0; m < 9; ++m) dst[m * 16] = o[m];
       }
     }
     __syncwarp();
@@ -355,13 +372,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
       float F[kNF][4];
 #pragma unroll
       for (int f = 0; f < kNF; ++f) {
-        const float4* src = reinterpret_cast<const float4*>(S + oSY + f * 192 + yx * 12);
-        const float4 q0 = src[0], q1 = src[1], q2 = src[2];
-        // q0 = (vv0, vv1, vv2, vd0), q1 = (vd1, vd2, dv0, dv1), q2 = (dv2, ., ., .)
-        F[f][0] = bz0 * q0.x + bz1 * q0.y + bz2 * q0.z;
-        F[f][1] = bz0 * q1.z + bz1 * q1.w + bz2 * q2.x;
-        F[f][2] = bz0 * q0.w + bz1 * q1.x + bz2 * q1.y;
-        F[f][3] = dz0 * q0.x + dz1 * q0.y + dz2 * q0.z;
+        const float* src = S + oSY + f * 144 + yx;  // [(kind*3 + iz)*16]
+        const float vv0 = src[0], vv1 = src[16], vv2 = src[32];
+        const float vd0 = src[48], vd1 = src[64], vd2 = src[80];
+        const float dv0 = src[96], dv1 = src[112], dv2 = src[128];
+        F[f][0] = bz0 * vv0 + bz1 * vv1 + bz2 * vv2;
+        F[f][1] = bz0 * dv0 + bz1 * dv1 + bz2 * dv2;
+        F[f][2] = bz0 * vd0 + bz1 * vd1 + bz2 * vd2;
+        F[f][3] = dz0 * vv0 + dz1 * vv1 + dz2 * vv2;
       }
       pointwise(A, S, S + oCF, q, F, aT, dT);
     }
@@ -407,7 +425,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
           B2[i] = -gg[i] * a2[i];
         }
       }
-      float* o = S + oTX + ((comp * 2 + part) * 3) * 48 + zy * 3;
+      // tx[cp][arr][qy][qz][ix]
+      float* o = S + oTX + (comp * 2 + part) * kTXS + (zy & 3) * 12 + (zy >> 2) * 3;
 #pragma unroll
       for (int ix = 0; ix < 3; ++ix) {
         float tv = 0.f, t1 = 0.f, t2 = 0.f;
@@ -427,19 +446,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       const int l = t + 32 * r;
-      const int cp = l / 12, rr = l - 12 * (l / 12), lz = rr / 3, ix = rr - 3 * (rr / 3);
-      const float* tx = S + oTX + cp * 3 * 48 + lz * 12 + ix;
-      float* o = S + oTY + cp * 2 * 36 + lz * 9 + ix;
+      // line (cp, qz, ix): lanes walk l % 12 = qz*3 + ix contiguously in tx and ty
+      const int cp = l / 12, zx = l - 12 * (l / 12);
+      const float* tx = S + oTX + cp * kTXS + zx;       // tx[cp][arr][qy][qz*3+ix]
+      float* o = S + oTY + cp * kTYS + zx;              // ty[cp][arr][iy][qz*3+ix]
 #pragma unroll
       for (int iy = 0; iy < 3; ++iy) {
         float ua = 0.f, ub = 0.f;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
-          ua += cB[qq][iy] * tx[qq * 3] + cD[qq][iy] * tx[48 + qq * 3];
-          ub += cB[qq][iy] * tx[96 + qq * 3];
+          ua += cB[qq][iy] * tx[qq * 12] + cD[qq][iy] * tx[48 + qq * 12];
+          ub += cB[qq][iy] * tx[96 + qq * 12];
         }
-        o[iy * 3] = ua;
-        o[36 + iy * 3] = ub;
+        o[iy * 12] = ua;
+        o[36 + iy * 12] = ub;
       }
     }
     __syncwarp();
@@ -448,14 +468,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
     for (int r = 0; r < 3; ++r) {
       const int l = t + 32 * r;
       if (l < 4 * 2 * 9) {
-        const int cp = l / 9, yx = l - 9 * (l / 9);
-        const float* ty = S + oTY + cp * 2 * 36 + yx;
+        const int cp = l / 9, yx = l - 9 * (l / 9), iy = yx / 3, ix = yx - 3 * (yx / 3);
+        const float* ty = S + oTY + cp * kTYS + iy * 12 + ix;  // [arr*36 + iy*12 + qz*3 + ix]
         float* o = S + oTZ + cp * 27 + yx;
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz) {
           float sacc = 0.f;
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) sacc += cB[qq][iz] * ty[qq * 9] + cD[qq][iz] * ty[36 + qq * 9];
+          for (int qq = 0; qq < 4; ++qq) sacc += cB[qq][iz] * ty[qq * 3] + cD[qq][iz] * ty[36 + qq * 3];
           o[iz * 9] = sacc;
         }
       }

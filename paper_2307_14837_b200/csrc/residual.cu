@@ -64,8 +64,9 @@ __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[
 constexpr int kNF = 7;
 constexpr int oU = 0;                  // u[f][27]
 constexpr int oSX = 192;               // sx[f][2][9][4]          | backward tx[8][3][16][3]
-constexpr int oSY = oSX + kNF * 72;    // sy[f][kind*3+iz][16 yx] |          ty[8][2][4][3][3]
-constexpr int oCF = oSX + kNF * 216;   // cf[22][64]: A[4], B[4][3], dg[3], pvr[3]
+constexpr int kSXF = 116;             // sx field stride: [kind][iz (stride 20)][qx][iy, pad]
+constexpr int oSY = oSX + kNF * kSXF;  // sy[f][kind*3+iz][16 yx]
+constexpr int oCF = oSX + kNF * (kSXF + 144);  // cf[22][64]: A[4], B[4][3], dg[3], pvr[3]
 constexpr int kNCF = 22;
 constexpr int oTZ = oCF + kNCF * 64;   // tz[4][2][27]
 constexpr int kCellFloats = (oTZ + 4 * 2 * 27 + 3) / 4 * 4;
@@ -81,7 +82,7 @@ constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
 constexpr int CB = 4;        // B[c][k]   reference-gradient test
 constexpr int CDG = 16;      // dg[i] = delta*w*g_i           (LPS, Gpi test, comps 1..3)
 constexpr int CPV = 19;      // pvr[k] = (J^-1 pi v)_k
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 5;
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
@@ -268,7 +269,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #undef CFW
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualArgs A) {
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(ResidualArgs A) {
   extern __shared__ __align__(16) float smem[];
   const int wib = threadIdx.x >> 5;
   const int t = threadIdx.x & 31;
@@ -315,25 +316,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
       dT = A.delta0 / den;
     }
     __syncwarp();
-    // ---------------- forward x: line (f, izy) -> sx[f][kind][izy][qx] ----------------
+    // ---------------- forward x: line (f, iz, iy) -> sx[f][kind][iz][qx][iy] ----------------
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int l = t + 32 * r;
       if (l < kNF * 9) {
-        const int f = l / 9, izy = l - 9 * (l / 9);
+        const int f = l / 9, izy = l - 9 * (l / 9), iz = izy / 3, iy = izy - 3 * (izy / 3);
         const float* u = S + oU + f * 27 + izy * 3;
         const float u0 = u[0], u1 = u[1], u2 = u[2];
-        float4 vb, vd;
-        vb.x = cB[0][0] * u0 + cB[0][1] * u1 + cB[0][2] * u2;
-        vb.y = cB[1][0] * u0 + cB[1][1] * u1 + cB[1][2] * u2;
-        vb.z = cB[2][0] * u0 + cB[2][1] * u1 + cB[2][2] * u2;
-        vb.w = cB[3][0] * u0 + cB[3][1] * u1 + cB[3][2] * u2;
-        vd.x = cD[0][0] * u0 + cD[0][1] * u1 + cD[0][2] * u2;
-        vd.y = cD[1][0] * u0 + cD[1][1] * u1 + cD[1][2] * u2;
-        vd.z = cD[2][0] * u0 + cD[2][1] * u1 + cD[2][2] * u2;
-        vd.w = cD[3][0] * u0 + cD[3][1] * u1 + cD[3][2] * u2;
-        *reinterpret_cast<float4*>(S + oSX + f * 72 + izy * 4) = vb;
-        *reinterpret_cast<float4*>(S + oSX + f * 72 + 36 + izy * 4) = vd;
+        float* o = S + oSX + f * kSXF + iz * 20 + iy;
+#pragma unroll
+        for (int lq = 0; lq < 4; ++lq) {
+          o[lq * 4] = cB[lq][0] * u0 + cB[lq][1] * u1 + cB[lq][2] * u2;
+          o[60 + lq * 4] = cD[lq][0] * u0 + cD[lq][1] * u1 + cD[lq][2] * u2;
+        }
       }
     }
     __syncwarp();
@@ -343,18 +339,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
       const int l = t + 32 * r;
       if (l < kNF * 16) {
         const int f = l >> 4, yx = l & 15, ly = yx >> 2, lx = yx & 3;
-        const float* s0 = S + oSX + f * 72 + lx;
+        const float* s0 = S + oSX + f * kSXF + lx * 4;  // [kind*60 + iz*20] -> float4 over iy
         const float by0 = cB[ly][0], by1 = cB[ly][1], by2 = cB[ly][2];
         const float dy0 = cD[ly][0], dy1 = cD[ly][1], dy2 = cD[ly][2];
         float o[9];
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz) {
-          const float a0 = s0[(iz * 3 + 0) * 4], a1 = s0[(iz * 3 + 1) * 4], a2 = s0[(iz * 3 + 2) * 4];
-          const float b0 = s0[36 + (iz * 3 + 0) * 4], b1 = s0[36 + (iz * 3 + 1) * 4],
-                      b2 = s0[36 + (iz * 3 + 2) * 4];
-          o[0 + iz] = by0 * a0 + by1 * a1 + by2 * a2;
-          o[3 + iz] = dy0 * a0 + dy1 * a1 + dy2 * a2;
-          o[6 + iz] = by0 * b0 + by1 * b1 + by2 * b2;
+          const float4 a = *reinterpret_cast<const float4*>(s0 + iz * 20);
+          const float4 b = *reinterpret_cast<const float4*>(s0 + 60 + iz * 20);
+          o[0 + iz] = by0 * a.x + by1 * a.y + by2 * a.z;
+          o[3 + iz] = dy0 * a.x + dy1 * a.y + dy2 * a.z;
+          o[6 + iz] = by0 * b.x + by1 * b.y + by2 * b.z;
         }
         float* dst = S + oSY + f * 144 + yx;
 #pragma unroll
@@ -362,26 +357,33 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
       }
     }
     __syncwarp();
-    // ---------------- forward z + pointwise: Gauss points q = t, t + 32 ----------------
-#pragma unroll 1
-    for (int r = 0; r < 2; ++r) {
-      const int q = t + 32 * r;
-      const int yx = q & 15, qz = q >> 4;
-      const float bz0 = cB[qz][0], bz1 = cB[qz][1], bz2 = cB[qz][2];
-      const float dz0 = cD[qz][0], dz1 = cD[qz][1], dz2 = cD[qz][2];
-      float F[kNF][4];
+    // ---------------- forward z + pointwise: Gauss points q = t and t + 32 (same qy, qx) ----------------
+    {
+      const int yx = t & 15, qz = t >> 4;  // second point: qz + 2
+      float F[kNF][4], G[kNF][4];
 #pragma unroll
       for (int f = 0; f < kNF; ++f) {
         const float* src = S + oSY + f * 144 + yx;  // [(kind*3 + iz)*16]
         const float vv0 = src[0], vv1 = src[16], vv2 = src[32];
         const float vd0 = src[48], vd1 = src[64], vd2 = src[80];
         const float dv0 = src[96], dv1 = src[112], dv2 = src[128];
-        F[f][0] = bz0 * vv0 + bz1 * vv1 + bz2 * vv2;
-        F[f][1] = bz0 * dv0 + bz1 * dv1 + bz2 * dv2;
-        F[f][2] = bz0 * vd0 + bz1 * vd1 + bz2 * vd2;
-        F[f][3] = dz0 * vv0 + dz1 * vv1 + dz2 * vv2;
+        {
+          const float b0 = cB[qz][0], b1 = cB[qz][1], b2 = cB[qz][2];
+          F[f][0] = b0 * vv0 + b1 * vv1 + b2 * vv2;
+          F[f][1] = b0 * dv0 + b1 * dv1 + b2 * dv2;
+          F[f][2] = b0 * vd0 + b1 * vd1 + b2 * vd2;
+          F[f][3] = cD[qz][0] * vv0 + cD[qz][1] * vv1 + cD[qz][2] * vv2;
+        }
+        {
+          const float b0 = cB[qz + 2][0], b1 = cB[qz + 2][1], b2 = cB[qz + 2][2];
+          G[f][0] = b0 * vv0 + b1 * vv1 + b2 * vv2;
+          G[f][1] = b0 * dv0 + b1 * dv1 + b2 * dv2;
+          G[f][2] = b0 * vd0 + b1 * vd1 + b2 * vd2;
+          G[f][3] = cD[qz + 2][0] * vv0 + cD[qz + 2][1] * vv1 + cD[qz + 2][2] * vv2;
+        }
       }
-      pointwise(A, S, S + oCF, q, F, aT, dT);
+      pointwise(A, S, S + oCF, t, F, aT, dT);
+      pointwise(A, S, S + oCF, t + 32, G, aT, dT);
     }
     __syncwarp();
     // ---------------- backward x (contract qx): line (comp, part, zy) ----------------
@@ -490,14 +492,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) element_kernel(ResidualAr
       for (int comp = 0; comp < 4; ++comp) {
         float sacc = S[oTZ + (comp * 2) * 27 + t];
         if (vertex) {
+          // PI[b][t] != 0 only for the 8 nodes b with b_k in {t_k, 1} (weight 1/2 per mid index)
           const float* gp = S + oTZ + (comp * 2 + 1) * 27;
 #pragma unroll
-          for (int b = 0; b < 27; ++b) {
-            const int ib0 = b % 3, ib1 = (b / 3) % 3, ib2 = b / 9;
-            const float wgt = (ib0 == 1 ? 0.5f : (ib0 == it0 ? 1.f : 0.f)) *
-                              (ib1 == 1 ? 0.5f : (ib1 == it1 ? 1.f : 0.f)) *
-                              (ib2 == 1 ? 0.5f : (ib2 == it2 ? 1.f : 0.f));
-            sacc = fmaf(wgt, gp[b], sacc);
+          for (int m = 0; m < 8; ++m) {
+            const int b0 = (m & 1) ? 1 : it0, b1 = (m & 2) ? 1 : it1, b2 = (m & 4) ? 1 : it2;
+            const float wgt = ((m & 1) ? 0.5f : 1.f) * ((m & 2) ? 0.5f : 1.f) * ((m & 4) ? 0.5f : 1.f);
+            sacc = fmaf(wgt, gp[b0 + 3 * b1 + 9 * b2], sacc);
           }
         }
         e[comp] = sacc;

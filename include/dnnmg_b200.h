@@ -18,6 +18,9 @@
  *   dnnmg_scatter_update    predict_correction scatter + x~ + scale*d
  *                                                       patch_ops.py:64-76, driver.py:268
  *   dnnmg_correction_step   TimeLoop._step_hybrid lines 251-268 (K1..K5 fused sequence)
+ *   dnnmg_halo_*            x-slab decomposition of the same step (no reference counterpart:
+ *                           the reference is single-process); the interface sums
+ *                           reproduce assembly.py:180-184 / patch_ops.py:32-38 across ranks
  *
  * Conventions (all match the reference):
  *   - dof vectors are node-major, component-minor: dof = 4*node + comp,
@@ -194,6 +197,31 @@ int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_d
                               const float* x_coarse, const float* b_prev, float scale,
                               const dnnmg_step_buffers_t* buf, float* x_corr,
                               dnnmg_stream_t stream);
+
+/* ---- x-slab halo (interface) operations, SURVEY §8(e) -------------------------------------
+ * idx: [n] local fine-node ids of one interface plane, in the order both neighbours agree on.
+ * All vectors are float4 rows (node-major). */
+/* out[i] = a[idx[i]] - b[idx[i]] (b nullable) — e.g. the partial operator A = b_prev - r_local */
+int32_t dnnmg_halo_gather(const int32_t* idx, int32_t n, const float* a, const float* b, float* out,
+                          dnnmg_stream_t stream);
+/* out[i] = this rank's partial A_h(x~) at idx[i]: element vectors (from dnnmg_residual's
+ * scratch) summed over the node's local cells in ascending cell id */
+int32_t dnnmg_halo_operator(const dnnmg_level_t* lv, const float* elem_scratch, const int32_t* idx,
+                            int32_t n, float* out, dnnmg_stream_t stream);
+/* r[idx[i]] = b[idx[i]] - (A_left[i] + A_right[i]); masked dofs -> 0 */
+int32_t dnnmg_halo_residual(const int32_t* idx, int32_t n, const float* b, const float* own,
+                            const float* nb, int32_t own_is_left, const uint8_t* dof_mask, float* r,
+                            dnnmg_stream_t stream);
+/* out[idx[i]] = A_left[i] + A_right[i]: interface rows of an assembled dual vector (next RHS) */
+int32_t dnnmg_halo_sum(const int32_t* idx, int32_t n, const float* own, const float* nb,
+                       int32_t own_is_left, float* out, dnnmg_stream_t stream);
+/* out[i] = (patch count, raw sums of the 3 velocity predictions) at idx[i] */
+int32_t dnnmg_halo_scatter_sums(const dnnmg_patchset_t* ps, const float* Y, const int32_t* idx,
+                                int32_t n, float* out, dnnmg_stream_t stream);
+/* d = (S_left + S_right)/(count_left + count_right), mask, x_corr = x~ + scale*d at idx */
+int32_t dnnmg_halo_scatter_apply(const int32_t* idx, int32_t n, const float* own, const float* nb,
+                                 int32_t own_is_left, const uint8_t* dof_mask, const float* x_tilde,
+                                 float scale, float* d, float* x_corr, dnnmg_stream_t stream);
 
 /* Number of kernels dnnmg_correction_step launches for this configuration. */
 int32_t dnnmg_correction_step_launches(int32_t J, const dnnmg_mlp_t* m);

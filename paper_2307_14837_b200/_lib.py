@@ -83,6 +83,13 @@ EXPORTS = {
                                       ctypes.POINTER(PatchSet), ctypes.POINTER(Mlp), c_vp, c_vp,
                                       c_f32, ctypes.POINTER(StepBuffers), c_vp, c_vp]),
     "dnnmg_correction_step_launches": (c_i32, [c_i32, ctypes.POINTER(Mlp)]),
+    "dnnmg_halo_gather": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "dnnmg_halo_operator": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "dnnmg_halo_sum": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "dnnmg_halo_residual": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "dnnmg_halo_scatter_sums": (c_i32, [ctypes.POINTER(PatchSet), c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "dnnmg_halo_scatter_apply": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_vp,
+                                         c_vp, c_vp]),
 }
 
 _lib = None

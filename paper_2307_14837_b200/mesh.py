@@ -58,7 +58,8 @@ class MeshLevel:
         self.parent_of = parent_of
         self.lattice = lattice            # (n_vertices, 3) integer grid positions
         self._boundary_faces = None
-        self._extent = None
+        self._extent = None      # (global grid size at this level, channel tags)
+        self._offset = 0         # lattice offset of this (sub-)box inside the global box
 
     @property
     def n_cells(self):
@@ -100,7 +101,7 @@ class MeshLevel:
 
 def _box_boundary_faces(lvl):
     ext, channel = lvl._extent
-    base = lvl.lattice[lvl.cells[:, 0]]
+    base = lvl.lattice[lvl.cells[:, 0]] + lvl._offset
     rows = []
     for f in range(6):
         axis, side = f // 2, f % 2
@@ -127,7 +128,8 @@ class MeshHierarchy:
         self.channel_tags = channel_tags
         self._node_cache = {}
         self._grid = np.asarray(level0.lattice.max(axis=0))
-        level0._extent = (self._grid, channel_tags)
+        if level0._extent is None:
+            level0._extent = (self._grid, channel_tags)
         self._check_orientation(level0)
 
     def _check_orientation(self, lvl):
@@ -196,6 +198,7 @@ def refine_uniform(h):
     parent = np.repeat(np.arange(nc), 8)
     new = MeshLevel(3, coords, cells, parent_of=parent, lattice=lattice)
     new._extent = (2 * lvl._extent[0], h.channel_tags)
+    new._offset = 2 * lvl._offset
     h._check_orientation(new)
     h.levels.append(new)
     return h
@@ -223,6 +226,29 @@ def build_template_mesh(geometry, **params):
     cells = np.concatenate([bot, bot + nx * ny], axis=1)
     lvl = MeshLevel(3, verts, cells, lattice=lattice)
     return MeshHierarchy(lvl, lo, hi, (), params.get("channel_tags", False))
+
+
+def build_subbox(vertices_global, n_cells_global, x_range, lo, hi, channel_tags=False):
+    """Level-0 hierarchy of the x-slab [x_range[0], x_range[1]) of a global box whose
+    (possibly jittered) level-0 vertices are `vertices_global` (x-fastest order).
+    Boundary tags are those of the GLOBAL box: slab-interface faces are interior."""
+    n = [int(v) for v in n_cells_global]
+    a, b = int(x_range[0]), int(x_range[1])
+    nxg = n[0] + 1
+    nx, ny, nz = b - a + 1, n[1] + 1, n[2] + 1
+    kk, jj, ii = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    lattice = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], axis=1).astype(np.int64)
+    gid = (lattice[:, 0] + a) + nxg * (lattice[:, 1] + ny * lattice[:, 2])
+    verts = np.asarray(vertices_global, dtype=float)[gid]
+    k, i, j = np.meshgrid(np.arange(n[2]), np.arange(b - a), np.arange(n[1]), indexing="ij")
+    k, i, j = k.ravel(), i.ravel(), j.ravel()
+    v0 = i + nx * (j + ny * k)
+    bot = np.stack([v0, v0 + 1, v0 + nx, v0 + nx + 1], axis=1)
+    cells = np.concatenate([bot, bot + nx * ny], axis=1)
+    lvl = MeshLevel(3, verts, cells, lattice=lattice)
+    lvl._extent = (np.asarray(n, dtype=np.int64), channel_tags)
+    lvl._offset = np.array([a, 0, 0], dtype=np.int64)
+    return MeshHierarchy(lvl, lo, hi, (), channel_tags)
 
 
 # -- patches -------------------------------------------------------------------

@@ -29,7 +29,7 @@ def constrained_mask(space, bcs):
 
 class CorrectionStep:
     def __init__(self, hierarchy, L, J, model, nu, k, bcs=None, alpha0=0.02, delta0=0.1,
-                 scale=1.0, precision="fp32", patchset=None, t=0.0):
+                 scale=1.0, precision="fp32", patchset=None, t=0.0, mask=None):
         self.hierarchy, self.L, self.J = hierarchy, L, J
         self.bcs = bcs if bcs is not None else {meshmod.WALL: no_slip}
         self.scale = float(scale)
@@ -39,7 +39,7 @@ class CorrectionStep:
         self.prolongs = [dv.DeviceProlong.get(hierarchy, l) for l in range(L, L + J)]
         self.P = (_lib.Prolong * J)(*[p.struct for p in self.prolongs])
         self.level = dv.DeviceLevel.get(self.space)
-        self.mask = constrained_mask(self.space, self.bcs)
+        self.mask = constrained_mask(self.space, self.bcs) if mask is None else np.asarray(mask)
         self.mask_bits = dv.upload(dv.dof_mask_bits(self.mask, self.space.n_nodes), np.uint8)
         self.lv = self.level.struct(self.mask_bits)
         self.patchset = patchset if patchset is not None else meshmod.build_patches(hierarchy, L, J)
@@ -155,6 +155,18 @@ class CorrectionStep:
         _lib.call("dnnmg_rhs_next", ctypes.byref(lv), dv.ptr(x), ctypes.byref(self.phys),
                   dv.ptr(self.elem), dv.ptr(out), dv.stream_handle())
         return out
+
+    def embed_into(self, x_coarse, dst):
+        """Prolongate (J levels) + Dirichlet into dst without allocation."""
+        s = dv.stream_handle()
+        cur = x_coarse
+        for i, P in enumerate(self.prolongs):
+            last = i == self.J - 1
+            out = dst if last else self.x_mid
+            bc = ctypes.byref(self.bc.struct) if last else None
+            _lib.call("dnnmg_prolongate", ctypes.byref(P.struct), dv.ptr(cur), dv.ptr(out), bc, s)
+            cur = out
+        return dst
 
     def embed(self, x_coarse, t=None):
         """Prolongate + Dirichlet only (driver.embed_state, driver.py:611-619)."""

@@ -256,6 +256,7 @@ def algorithmic_units(step, cfg):
         "K2_residual": {"bytes": 72 * nf, "flops_ref_formulation": 213078 * step.level.n_cells},
         "K3_gather": {"bytes": 32 * nf + 96 * npch + 4 * n_in * npch},
         "K4_mlp": {"flops": 2 * (n_in * H + (d - 1) * H * H + H * n_out) * npch},
+        "K3K4_gather_mlp": {"flops": 2 * (n_in * H + (d - 1) * H * H + H * n_out) * npch},
         "K5_scatter": {"bytes": 4 * n_out * npch + 48 * nf},
     }
 
@@ -358,7 +359,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
 
     # ---- per-kernel events inside the timed region (same stream) ----
-    names = ["K1_prolong"] * step.J + ["K2_residual", "K3_gather", "K4_mlp", "K5_scatter"]
+    names = step.stage_names()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
     kern_ms = np.zeros(len(names))
 
@@ -432,7 +433,7 @@ def run_ours(args, rank, world, local):
     share = avg / avg.sum()
     per_kernel = {}
     for j, nm in enumerate(names):
-        u = units[nm]
+        u = units.get(nm, units.get("K4_mlp"))
         entry = {"ms": float(avg[j]), "share": float(share[j])}
         if "bytes" in u:
             entry["GB/s"] = u["bytes"] / (avg[j] / 1e3) / 1e9
@@ -443,7 +444,7 @@ def run_ours(args, rank, world, local):
             entry["ref_formulation_TFLOP/s"] = u["flops_ref_formulation"] / (avg[j] / 1e3) / 1e12
         per_kernel[nm] = entry
     dom = names[int(np.argmax(avg))]
-    du = units[dom]
+    du = units.get(dom, units["K4_mlp"])
     if "flops" in du:
         ach = du["flops"] / (per_kernel[dom]["ms"] / 1e3) / 1e12
         peak = peaks["bf16_tflops_sustained"] if precision == "bf16" else \

@@ -172,6 +172,11 @@ int32_t dnnmg_mlp_pack(const dnnmg_mlp_t* m, void* packed, dnnmg_stream_t stream
 int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
                           dnnmg_stream_t stream);
 
+/* K3 fused into K4 (tensor-core modes, 8*npp + n_geo <= 256): the network input rows
+ * [x~ | r | geometry] are gathered straight into the layer-0 operand; X is never stored. */
+int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
+                                  const float* r, float* Y, dnnmg_stream_t stream);
+
 /* ---- K5: averaging scatter + correction update ---------------------------------------- */
 /* d = mu * bincount(velocity rows Y); d[mask] = 0; pressure 0; x_corr = x_tilde + scale*d.
  * Y: [n_patches][3*npp].  x_tilde/x_corr may be NULL (then only d is written). */

@@ -76,6 +76,8 @@ EXPORTS = {
     "dnnmg_mlp_packed_bytes": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(c_i64)]),
     "dnnmg_mlp_pack": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_vp]),
     "dnnmg_mlp_forward": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_i64, c_vp, c_vp]),
+    "dnnmg_mlp_forward_patches": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet), c_vp, c_vp,
+                                          c_vp, c_vp]),
     "dnnmg_scatter_update": (c_i32, [ctypes.POINTER(PatchSet), c_vp, c_vp, c_vp, c_f32, c_vp, c_vp,
                                      c_vp]),
     "dnnmg_correction_step": (c_i32, [ctypes.POINTER(Prolong), c_i32, ctypes.POINTER(Dirichlet),

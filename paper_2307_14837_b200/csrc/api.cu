@@ -32,6 +32,8 @@ int32_t mlp_tc_supported(const dnnmg_mlp_t*);
 int32_t mlp_tc_packed_bytes(const dnnmg_mlp_t*, int64_t*);
 int32_t launch_mlp_tc_pack(const dnnmg_mlp_t*, void*, cudaStream_t);
 int32_t launch_mlp_tc(const dnnmg_mlp_t*, const float*, int64_t, float*, cudaStream_t);
+int32_t launch_mlp_tc_gather(const dnnmg_mlp_t*, const dnnmg_patchset_t*, const float*,
+                             const float*, float*, cudaStream_t);
 
 static int32_t check_mlp(const dnnmg_mlp_t* m) {
   DNNMG_REQUIRE(m, DNNMG_ERR_ARG, "mlp: null model");
@@ -146,15 +148,34 @@ int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, 
   return launch_mlp_tc(m, X, n_rows, Y, as_stream(s));
 }
 
+int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
+                                  const float* r, float* Y, dnnmg_stream_t s) {
+  int32_t st = check_mlp(m);
+  if (st) return st;
+  DNNMG_REQUIRE(ps && ps->node_table && ps->geom && x && r && Y, DNNMG_ERR_ARG,
+                "mlp_forward_patches: null argument");
+  DNNMG_REQUIRE(m->n_in == 8 * ps->nodes_per_patch + ps->n_geo && m->n_out == 3 * ps->nodes_per_patch,
+                DNNMG_ERR_ARCH, "model architecture (%d -> %d) does not match the patch layout (%d -> %d)",
+                m->n_in, m->n_out, 8 * ps->nodes_per_patch + ps->n_geo, 3 * ps->nodes_per_patch);
+  DNNMG_REQUIRE(m->precision != DNNMG_PREC_FP32 && mlp_tc_supported(m) && m->packed,
+                DNNMG_ERR_UNSUPPORTED, "mlp_forward_patches: needs a packed tensor-core model");
+  if (ps->n_patches == 0) return DNNMG_OK;
+  return launch_mlp_tc_gather(m, ps, x, r, Y, as_stream(s));
+}
+
 int32_t dnnmg_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const uint8_t* mask,
                              const float* xt, float scale, float* d, float* xc, dnnmg_stream_t s) {
   return launch_scatter_update(ps, Y, mask, xt, scale, d, xc, as_stream(s));
 }
 
+static bool fused_gather(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps) {
+  return m->precision != DNNMG_PREC_FP32 && mlp_tc_supported(m) && m->packed &&
+         (ps == nullptr || (ps->n_geo % 4 == 0 && 8 * ps->nodes_per_patch + ps->n_geo <= 256));
+}
+
 int32_t dnnmg_correction_step_launches(int32_t J, const dnnmg_mlp_t* m) {
-  (void)m;
-  // J prolongations + element + node-sum + gather + mlp + scatter
-  return J + 5;
+  // J prolongations + element + node-sum + [gather] + mlp + scatter
+  return J + (fused_gather(m, nullptr) ? 4 : 5);
 }
 
 int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_dirichlet_t* bc,
@@ -185,9 +206,12 @@ int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_d
                        st);
   if (rc) return rc;
   // (4) patch features, network, averaging scatter, update (driver.py:263-268)
-  rc = launch_gather(ps, buf->x_tilde, buf->r, buf->X, st);
-  if (rc) return rc;
-  rc = dnnmg_mlp_forward(m, buf->X, ps->n_patches, buf->Y, s);
+  if (fused_gather(m, ps)) {
+    rc = launch_mlp_tc_gather(m, ps, buf->x_tilde, buf->r, buf->Y, st);
+  } else {
+    rc = launch_gather(ps, buf->x_tilde, buf->r, buf->X, st);
+    if (!rc) rc = dnnmg_mlp_forward(m, buf->X, ps->n_patches, buf->Y, s);
+  }
   if (rc) return rc;
   return launch_scatter_update(ps, buf->Y, fine->dof_mask, buf->x_tilde, scale, buf->d, x_corr, st);
 }

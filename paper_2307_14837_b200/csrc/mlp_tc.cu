@@ -56,6 +56,12 @@ struct TcArgs {
   const float* shift;
   const float* in_mean;
   const float* in_std;
+  // fused patch gather (K3 into K4): row p = [x~ rows | r rows | geometry] of patch p
+  const int32_t* node_table;  // [n_rows][npp] or NULL (then X is read)
+  const float4* xg;           // x~ (float4 per node)
+  const float4* rg;           // r
+  const float* geom;          // [n_rows][n_geo]
+  int npp, n_geo;
 };
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -372,6 +378,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     auto load_x = [&](int64_t tile) {
       const int64_t row = tile * kTcM + row_in_tile;
       const bool ok = tile < n_tiles && row < A.n_rows;
+      if (A.node_table) {
+        // fused gather (patch_ops.py:49-53): float4 slot s of the row is x~ of node s,
+        // r of node s - npp, or geometry; indices first, then all value loads in flight
+        const int32_t* nt = A.node_table + row * A.npp;
+        const int geo4 = A.n_geo / 4;
+        int nidx[8][4];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int f4 = 8 * c + 4 * hh + j;
+            const int s = f4 < A.npp ? f4 : f4 - A.npp;
+            nidx[c][j] = (ok && c < nck0 && f4 < 2 * A.npp) ? __ldg(nt + s) : 0;
+          }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int f4 = 8 * c + 4 * hh + j;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok && c < nck0) {
+              if (f4 < A.npp) v = __ldg(A.xg + nidx[c][j]);
+              else if (f4 < 2 * A.npp) v = __ldg(A.rg + nidx[c][j]);
+              else if (f4 < 2 * A.npp + geo4)
+                v = __ldg(reinterpret_cast<const float4*>(A.geom + row * A.n_geo) + (f4 - 2 * A.npp));
+            }
+            xin[c][4 * j] = v.x;
+            xin[c][4 * j + 1] = v.y;
+            xin[c][4 * j + 2] = v.z;
+            xin[c][4 * j + 3] = v.w;
+          }
+        return;
+      }
       const float* xr = A.X + row * A.n_in;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -587,12 +626,26 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
   return DNNMG_OK;
 }
 
+struct GatherSrc {
+  const int32_t* node_table;
+  const float* x;
+  const float* r;
+  const float* geom;
+  int npp, n_geo;
+};
+
 template <int MODE>
 static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
-                           cudaStream_t s) {
+                           cudaStream_t s, const GatherSrc* g) {
   using C = TcCfg<MODE>;
   TcArgs A;
   A.X = X;
+  A.node_table = g ? g->node_table : nullptr;
+  A.xg = g ? reinterpret_cast<const float4*>(g->x) : nullptr;
+  A.rg = g ? reinterpret_cast<const float4*>(g->r) : nullptr;
+  A.geom = g ? g->geom : nullptr;
+  A.npp = g ? g->npp : 0;
+  A.n_geo = g ? g->n_geo : 0;
   A.Y = Y;
   A.n_rows = n_rows;
   A.n_in = m->n_in;
@@ -632,8 +685,21 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
 
 int32_t launch_mlp_tc(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
                       cudaStream_t s) {
-  if (m->precision == DNNMG_PREC_BF16) return launch_mode<DNNMG_PREC_BF16>(m, X, n_rows, Y, s);
-  return launch_mode<DNNMG_PREC_TF32X3>(m, X, n_rows, Y, s);
+  if (m->precision == DNNMG_PREC_BF16) return launch_mode<DNNMG_PREC_BF16>(m, X, n_rows, Y, s, nullptr);
+  return launch_mode<DNNMG_PREC_TF32X3>(m, X, n_rows, Y, s, nullptr);
+}
+
+// K3 fused into K4: the network input rows are gathered from x~, r and the patch
+// geometry while staging the layer-0 operand; X never touches HBM
+int32_t launch_mlp_tc_gather(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
+                             const float* r, float* Y, cudaStream_t s) {
+  DNNMG_REQUIRE(ps->n_geo % 4 == 0 && 8 * ps->nodes_per_patch + ps->n_geo == m->n_in &&
+                    m->n_in <= kTcH,
+                DNNMG_ERR_UNSUPPORTED, "mlp_gather: needs 8*npp + n_geo == n_in <= 256");
+  GatherSrc g{ps->node_table, x, r, ps->geom, ps->nodes_per_patch, ps->n_geo};
+  if (m->precision == DNNMG_PREC_BF16)
+    return launch_mode<DNNMG_PREC_BF16>(m, nullptr, ps->n_patches, Y, s, &g);
+  return launch_mode<DNNMG_PREC_TF32X3>(m, nullptr, ps->n_patches, Y, s, &g);
 }
 
 }  // namespace dnnmg

@@ -196,10 +196,7 @@ class SlabStep:
             lib.call("dnnmg_halo_residual", dv.ptr(idx), idx.numel(), dv.ptr(self._b),
                      dv.ptr(self.own[side]), dv.ptr(recv_operator[side]), self._left_owner(side),
                      dv.ptr(st.mask_bits), dv.ptr(st.r), s)
-        lib.call("dnnmg_gather", ctypes.byref(st.ps.struct), dv.ptr(st.x_tilde), dv.ptr(st.r),
-                 dv.ptr(st.X), s)
-        lib.call("dnnmg_mlp_forward", ctypes.byref(st.model.struct), dv.ptr(st.X), st.ps.n_patches,
-                 dv.ptr(st.Y), s)
+        st.predict_rows(s)
         lib.call("dnnmg_scatter_update", ctypes.byref(st.ps.struct), dv.ptr(st.Y),
                  dv.ptr(st.mask_bits), dv.ptr(st.x_tilde), ctypes.c_float(st.scale), dv.ptr(st.d),
                  dv.ptr(st.x_corr), s)

@@ -47,6 +47,10 @@ class CorrectionStep:
         self.ps = dv.DevicePatchSet.get(self.patchset)
         self.precision = precision
         self.model = dv.DeviceModel(model, precision)
+        a = model.arch
+        # K3 fused into K4 when the tensor-core MLP can stage the rows itself
+        self.fused_gather = (precision != "fp32" and a.n_hidden == 256 and a.n_in <= 256
+                             and a.n_out <= 256 and self.patchset.n_geo % 4 == 0)
         self.phys = _lib.Phys(float(nu), float(k), float(alpha0), float(delta0), 1)
         dev = dv.device()
         nf = self.space.n_nodes
@@ -123,17 +127,30 @@ class CorrectionStep:
         _lib.call("dnnmg_residual", ctypes.byref(self.lv), dv.ptr(self.x_tilde), dv.ptr(b_prev),
                   None, None, ctypes.byref(self.phys), dv.ptr(self.elem), dv.ptr(self.r), 1, s)
         mark()
-        _lib.call("dnnmg_gather", ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde),
-                  dv.ptr(self.r), dv.ptr(self.X), s)
-        mark()
-        _lib.call("dnnmg_mlp_forward", ctypes.byref(self.model.struct), dv.ptr(self.X),
-                  self.ps.n_patches, dv.ptr(self.Y), s)
+        self.predict_rows(s)
         mark()
         _lib.call("dnnmg_scatter_update", ctypes.byref(self.ps.struct), dv.ptr(self.Y),
                   dv.ptr(self.mask_bits), dv.ptr(self.x_tilde), ctypes.c_float(self.scale),
                   dv.ptr(self.d), dv.ptr(out), s)
         mark()
         return out
+
+    def predict_rows(self, s):
+        """Y = network(patch rows of x~, r): fused gather+MLP or gather then MLP."""
+        if self.fused_gather:
+            _lib.call("dnnmg_mlp_forward_patches", ctypes.byref(self.model.struct),
+                      ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde), dv.ptr(self.r),
+                      dv.ptr(self.Y), s)
+            return
+        _lib.call("dnnmg_gather", ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde),
+                  dv.ptr(self.r), dv.ptr(self.X), s)
+        _lib.call("dnnmg_mlp_forward", ctypes.byref(self.model.struct), dv.ptr(self.X),
+                  self.ps.n_patches, dv.ptr(self.Y), s)
+
+    def stage_names(self):
+        """Labels of the stages run_staged() brackets with events."""
+        mid = ["K3K4_gather_mlp"] if self.fused_gather else ["K3_gather+K4_mlp"]
+        return ["K1_prolong"] * self.J + ["K2_residual"] + mid + ["K5_scatter"]
 
     def capture(self, x_coarse, b_prev):
         """Capture run(x_coarse, b_prev) into a CUDA graph (inputs are fixed buffers)."""

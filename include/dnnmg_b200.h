@@ -70,6 +70,13 @@ typedef struct {
   int32_t n_coarse_cells;
   const int32_t* coarse_cell_nodes; /* [n_coarse_cells][27] level-l Q2 node table */
   const int32_t* fine_src;          /* [n_fine_nodes] */
+  /* optional owner lists (the same information grouped by parent cell): the fine
+   * nodes whose first-appearance parent is C are owner_node[owner_ptr[C]..owner_ptr[C+1])
+   * with local code o*27 + a in owner_code; when present K1 stages each parent's 27
+   * coarse values once per cell instead of gathering them per fine node */
+  const int32_t* owner_ptr;         /* [n_coarse_cells+1] or NULL */
+  const int32_t* owner_node;        /* [n_fine_nodes] */
+  const uint8_t* owner_code;        /* [n_fine_nodes] */
 } dnnmg_prolong_t;
 
 /* Dirichlet data of one level (space.py:245-255): bc_code[n] = 0 untouched,

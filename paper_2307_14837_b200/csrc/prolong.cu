@@ -90,6 +90,63 @@ __global__ void __launch_bounds__(256) dirichlet_kernel(int n, const uint8_t* __
   }
 }
 
+// v2: one warp per parent cell C.  The fine nodes whose first-appearance parent is C
+// (owner list, CSR by C) are computed from C's 27 coarse values staged in shared
+// memory once, instead of every fine node re-gathering its coarse row.
+constexpr int kProlongWarps = 8;
+
+__global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
+    int n_coarse_cells, const int32_t* __restrict__ ctab, const int32_t* __restrict__ owner_ptr,
+    const int32_t* __restrict__ owner_node, const uint8_t* __restrict__ owner_code,
+    const float4* __restrict__ xc, float4* __restrict__ xf, const uint8_t* __restrict__ bc_code,
+    const float* __restrict__ bc_values) {
+  __shared__ float4 cv[kProlongWarps][27];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int C = blockIdx.x * kProlongWarps + w; C < n_coarse_cells; C += gridDim.x * kProlongWarps) {
+    if (lane < 27) cv[w][lane] = __ldg(xc + __ldg(ctab + (int64_t)C * 27 + lane));
+    __syncwarp();
+    const int s = __ldg(owner_ptr + C), e = __ldg(owner_ptr + C + 1);
+    for (int i = s + lane; i < e; i += 32) {
+      const int n = __ldg(owner_node + i);
+      const int oa = __ldg(owner_code + i);
+      const int o = oa / 27, a = oa - 27 * o;
+      const int px = 2 * (o & 1) + a % 3;
+      const int py = 2 * ((o >> 1) & 1) + (a / 3) % 3;
+      const int pz = 2 * (o >> 2) + a / 9;
+      int ix[3], iy[3], iz[3];
+      float wx[3], wy[3], wz[3];
+      const int nx = stencil_1d(px, ix, wx);
+      const int ny = stencil_1d(py, iy, wy);
+      const int nz = stencil_1d(pz, iz, wz);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int kz = 0; kz < nz; ++kz)
+        for (int ky = 0; ky < ny; ++ky) {
+          const float wyz = wy[ky] * wz[kz];
+          for (int kx = 0; kx < nx; ++kx) {
+            const float wgt = wx[kx] * wyz;
+            const float4 v = cv[w][ix[kx] + 3 * iy[ky] + 9 * iz[kz]];
+            acc.x = fmaf(wgt, v.x, acc.x);
+            acc.y = fmaf(wgt, v.y, acc.y);
+            acc.z = fmaf(wgt, v.z, acc.z);
+            acc.w = fmaf(wgt, v.w, acc.w);
+          }
+        }
+      if (bc_code) {
+        const uint8_t code = bc_code[n];
+        if (code == 1) {
+          acc.y = acc.z = acc.w = 0.f;
+        } else if (code == 2) {
+          acc.y = bc_values[3 * (int64_t)n];
+          acc.z = bc_values[3 * (int64_t)n + 1];
+          acc.w = bc_values[3 * (int64_t)n + 2];
+        }
+      }
+      xf[n] = acc;
+    }
+    __syncwarp();
+  }
+}
+
 int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float* x_fine,
                           const dnnmg_dirichlet_t* bc, cudaStream_t s) {
   DNNMG_REQUIRE(P && x_coarse && x_fine, DNNMG_ERR_ARG, "prolongate: null argument");
@@ -106,6 +163,14 @@ int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float
     vals = bc->bc_values;
   }
   if (P->n_fine_nodes == 0) return DNNMG_OK;
+  if (P->owner_ptr && P->owner_node && P->owner_code) {
+    const int blocks = grid_for((P->n_coarse_cells + kProlongWarps - 1) / kProlongWarps, 1, 8);
+    prolongate_owner_kernel<<<blocks, 32 * kProlongWarps, 0, s>>>(
+        P->n_coarse_cells, P->coarse_cell_nodes, P->owner_ptr, P->owner_node, P->owner_code,
+        reinterpret_cast<const float4*>(x_coarse), reinterpret_cast<float4*>(x_fine), code, vals);
+    DNNMG_CHECK_LAUNCH("prolongate_owner_kernel");
+    return DNNMG_OK;
+  }
   prolongate_kernel<<<grid_for(P->n_fine_nodes, 256), 256, 0, s>>>(
       P->n_fine_nodes, P->coarse_cell_nodes, P->fine_src,
       reinterpret_cast<const float4*>(x_coarse), reinterpret_cast<float4*>(x_fine), code, vals);

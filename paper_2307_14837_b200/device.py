@@ -99,7 +99,17 @@ class DeviceProlong:
         self.src = upload(src, np.int32)
         self.n_fine = int(src.size)
         self.n_coarse_nodes = int(hierarchy.scalar_nodes(level)[0].shape[0])
-        self.struct = _lib.Prolong(self.n_fine, int(ctab.shape[0]), ptr(self.ctab), ptr(self.src))
+        # owner lists: fine nodes grouped by their first-appearance parent cell
+        parent = src // 216
+        order = np.argsort(parent, kind="stable")
+        counts = np.bincount(parent, minlength=ctab.shape[0])
+        optr = np.zeros(ctab.shape[0] + 1, dtype=np.int64)
+        np.cumsum(counts, out=optr[1:])
+        self.owner_ptr = upload(optr, np.int32)
+        self.owner_node = upload(order, np.int32)
+        self.owner_code = upload(src[order] % 216, np.uint8)
+        self.struct = _lib.Prolong(self.n_fine, int(ctab.shape[0]), ptr(self.ctab), ptr(self.src),
+                                   ptr(self.owner_ptr), ptr(self.owner_node), ptr(self.owner_code))
 
     @staticmethod
     def get(hierarchy, level):

@@ -71,7 +71,7 @@ constexpr int kNCF = 22;
 constexpr int oTZ = oCF + kNCF * 64;   // tz[4][2][27]
 constexpr int kCellFloats = (oTZ + 4 * 2 * 27 + 3) / 4 * 4;
 constexpr int kTXS = 172;             // per (comp, part) stride of tx: 144 + pad, = 12 (mod 32)
-constexpr int kTYS = 76;              // per (comp, part) stride of ty: 72 + pad,  = 12 (mod 32)
+constexpr int kTYS = 73;              // per (comp, part) stride of ty: 72 + pad,  = 9 (mod 32)
 constexpr int oTX = oSX;              // tx aliases the forward scratch (dead after pointwise)
 constexpr int oTY = oCF;              // ty aliases cf (dead after backward x)
 static_assert(oTX + 8 * kTXS <= oCF, "tx must fit in the forward scratch");
@@ -448,10 +448,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       const int l = t + 32 * r;
-      // line (cp, qz, ix): lanes walk l % 12 = qz*3 + ix contiguously in tx and ty
-      const int cp = l / 12, zx = l - 12 * (l / 12);
+      // line (cp, qz, ix): lanes walk l % 12 = qz*3 + ix contiguously in tx
+      const int cp = l / 12, zx = l - 12 * (l / 12), lz = zx / 3, ix = zx - 3 * (zx / 3);
       const float* tx = S + oTX + cp * kTXS + zx;       // tx[cp][arr][qy][qz*3+ix]
-      float* o = S + oTY + cp * kTYS + zx;              // ty[cp][arr][iy][qz*3+ix]
+      float* o = S + oTY + cp * kTYS + lz * 9 + ix;     // ty[cp][arr][qz][iy*3+ix]
 #pragma unroll
       for (int iy = 0; iy < 3; ++iy) {
         float ua = 0.f, ub = 0.f;
@@ -460,8 +460,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
           ua += cB[qq][iy] * tx[qq * 12] + cD[qq][iy] * tx[48 + qq * 12];
           ub += cB[qq][iy] * tx[96 + qq * 12];
         }
-        o[iy * 12] = ua;
-        o[36 + iy * 12] = ub;
+        o[iy * 3] = ua;
+        o[36 + iy * 3] = ub;
       }
     }
     __syncwarp();
@@ -470,14 +470,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
     for (int r = 0; r < 3; ++r) {
       const int l = t + 32 * r;
       if (l < 4 * 2 * 9) {
-        const int cp = l / 9, yx = l - 9 * (l / 9), iy = yx / 3, ix = yx - 3 * (yx / 3);
-        const float* ty = S + oTY + cp * kTYS + iy * 12 + ix;  // [arr*36 + iy*12 + qz*3 + ix]
+        // lanes walk l = cp*9 + yx: consecutive words of ty (stride 73 = 9 mod 32)
+        const int cp = l / 9, yx = l - 9 * (l / 9);
+        const float* ty = S + oTY + cp * kTYS + yx;  // [arr*36 + qz*9 + iy*3 + ix]
         float* o = S + oTZ + cp * 27 + yx;
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz) {
           float sacc = 0.f;
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) sacc += cB[qq][iz] * ty[qq * 3] + cD[qq][iz] * ty[36 + qq * 3];
+          for (int qq = 0; qq < 4; ++qq) sacc += cB[qq][iz] * ty[qq * 9] + cD[qq][iz] * ty[36 + qq * 9];
           o[iz * 9] = sacc;
         }
       }

@@ -30,18 +30,20 @@ namespace dnnmg {
 
 constexpr int kTcM = 128;
 constexpr int kTcH = 256;
-constexpr int kKC = 32;            // K elements per pipeline chunk
 constexpr int kTcThreads = 320;
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
 
 template <int MODE> struct TcCfg;
+// KC: K elements per pipeline chunk (one TMA weight copy, one A-ring stage);
+// both modes give 64-byte K rows per part, i.e. an SBO of 512 B between 8-row groups
 template <> struct TcCfg<DNNMG_PREC_BF16> {
-  static constexpr int ESZ = 2, PARTS = 1, NW = 6, NA = 4, KSTEP = 16;
+  static constexpr int ESZ = 2, PARTS = 1, NW = 6, NA = 4, KSTEP = 16, KC = 32;
 };
 template <> struct TcCfg<DNNMG_PREC_TF32X3> {
-  static constexpr int ESZ = 4, PARTS = 2, NW = 2, NA = 2, KSTEP = 8;
+  static constexpr int ESZ = 4, PARTS = 2, NW = 4, NA = 4, KSTEP = 8, KC = 16;
 };
+static int kc_of(int precision) { return precision == DNNMG_PREC_BF16 ? 32 : 16; }
 
 struct TcArgs {
   const float* X;
@@ -84,6 +86,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 }
 // bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
   uint32_t n = 0;
   while (!mbar_try(bar, parity)) {
     if (++n > (1u << 26)) __trap();
@@ -147,6 +150,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float* v) {
+  if constexpr (N == 16) tmem_ld16(taddr, v);
+  else tmem_ld8(taddr, v);
+}
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -180,37 +198,44 @@ __host__ __device__ constexpr uint32_t idesc_for(int N) {
 // ~2e-7 on [-1, 1], saturating correctly for |x| -> inf.
 __device__ __forceinline__ float act_fast(float x, int act, bool accurate) {
   if (act != DNNMG_ACT_TANH) return fmaxf(x, 0.f);
-  if (accurate) return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x));
+  if (accurate) {
+    // e = 2^(2x log2 e); 1 - 2/(1+e) with MUFU ex2 / rcp (no range branches)
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(2.8853900817779268f * x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+    return fmaf(-2.0f, r, 1.0f);
+  }
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-// byte offset of element (row, kk) in a canonical chunk part (kk < kKC)
-template <int ESZ>
+// byte offset of element (row, kk) in a canonical chunk part (kk < KC)
+template <int ESZ, int KC>
 __host__ __device__ constexpr uint32_t canon_off(int row, int kk) {
-  return (uint32_t)((row >> 3) * (256 * ESZ) + (kk / (16 / ESZ)) * 128 + (row & 7) * 16 +
+  return (uint32_t)((row >> 3) * (KC * ESZ * 8) + (kk / (16 / ESZ)) * 128 + (row & 7) * 16 +
                     (kk % (16 / ESZ)) * ESZ);
 }
 
-// write 16 consecutive K values (kk0..kk0+15, kk0 % 16 == 0) of one row into an A stage
+// write KC/2 consecutive K values (kk0.., kk0 % (KC/2) == 0) of one row into an A stage
 template <int MODE>
-__device__ __forceinline__ void put_row16(uint8_t* stage, int row, int kk0, const float* v) {
+__device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const float* v) {
   using C = TcCfg<MODE>;
+  constexpr int HC = C::KC / 2;
   if constexpr (MODE == DNNMG_PREC_BF16) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < HC / 8; ++j) {
       uint4 q;
       q.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
       q.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
       q.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
       q.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-      *reinterpret_cast<uint4*>(stage + canon_off<2>(row, kk0 + 8 * j)) = q;
+      *reinterpret_cast<uint4*>(stage + canon_off<2, C::KC>(row, kk0 + 8 * j)) = q;
     }
   } else {
-    constexpr int part = kTcM * kKC * C::ESZ;
+    constexpr int part = kTcM * C::KC * C::ESZ;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < HC / 4; ++j) {
       uint4 hi, lo;
       uint32_t* h = &hi.x;
       uint32_t* l = &lo.x;
@@ -221,7 +246,7 @@ __device__ __forceinline__ void put_row16(uint8_t* stage, int row, int kk0, cons
         h[e] = t;
         l[e] = to_tf32(x - __uint_as_float(t));
       }
-      const uint32_t off = canon_off<4>(row, kk0 + 4 * j);
+      const uint32_t off = canon_off<4, C::KC>(row, kk0 + 4 * j);
       *reinterpret_cast<uint4*>(stage + off) = hi;
       *reinterpret_cast<uint4*>(stage + part + off) = lo;
     }
@@ -231,9 +256,12 @@ __device__ __forceinline__ void put_row16(uint8_t* stage, int row, int kk0, cons
 template <int MODE>
 __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   using C = TcCfg<MODE>;
-  constexpr int WST = kTcH * kKC * C::ESZ * C::PARTS;  // bytes per weight stage
-  constexpr int AST = kTcM * kKC * C::ESZ * C::PARTS;  // bytes per A stage
-  constexpr uint32_t SBO = 256 * C::ESZ;
+  constexpr int KC = C::KC;
+  constexpr int HC = KC / 2;                       // K columns per thread per chunk
+  constexpr int NCH = kTcH / KC;                   // chunks of a hidden layer
+  constexpr int WST = kTcH * KC * C::ESZ * C::PARTS;  // bytes per weight stage
+  constexpr int AST = kTcM * KC * C::ESZ * C::PARTS;  // bytes per A stage
+  constexpr uint32_t SBO = KC * C::ESZ * 8;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* wring = smem;
   uint8_t* aring = smem + C::NW * WST;
@@ -298,8 +326,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int g = 0; g < G; ++g) {
           const int N = g < A.depth ? kTcH : A.Nhead;
-          const int nk = (g == 0 ? A.K0p : kTcH) / kKC;
-          const uint32_t bytes = (uint32_t)N * kKC * C::ESZ * C::PARTS;
+          const int nk = (g == 0 ? A.K0p : kTcH) / KC;
+          const uint32_t bytes = (uint32_t)N * KC * C::ESZ * C::PARTS;
           for (int c = 0; c < nk; ++c, ++item) {
             const int s = item % C::NW;
             const uint32_t round = item / C::NW;
@@ -318,7 +346,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int g = 0; g < G; ++g, ++j) {
           const int N = g < A.depth ? kTcH : A.Nhead;
-          const int nk = (g == 0 ? A.K0p : kTcH) / kKC;
+          const int nk = (g == 0 ? A.K0p : kTcH) / KC;
           const uint32_t idesc = idesc_for<MODE>(N);
           const int buf = j & 1;
           mbar_wait(smem_u32(&acc_empty[buf]), ((j >> 1) & 1) ^ 1);
@@ -332,14 +360,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
             const uint32_t wb = smem_u32(wring + sw * WST);
             const uint32_t ab = smem_u32(aring + sa * AST);
 #pragma unroll
-            for (int ks = 0; ks < kKC / C::KSTEP; ++ks) {
+            for (int ks = 0; ks < KC / C::KSTEP; ++ks) {
               const uint32_t koff = ks * 256;
               const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
               const uint64_t ahi = sdesc(ab + koff, SBO), bhi = sdesc(wb + koff, SBO);
               tc_mma<MODE>(d, ahi, bhi, idesc, acc);
               if constexpr (MODE == DNNMG_PREC_TF32X3) {
-                const uint64_t alo = sdesc(ab + kTcM * kKC * 4 + koff, SBO);
-                const uint64_t blo = sdesc(wb + (uint32_t)N * kKC * 4 + koff, SBO);
+                const uint64_t alo = sdesc(ab + kTcM * KC * 4 + koff, SBO);
+                const uint64_t blo = sdesc(wb + (uint32_t)N * KC * 4 + koff, SBO);
                 tc_mma<MODE>(d, ahi, blo, idesc, 1u);
                 tc_mma<MODE>(d, alo, bhi, idesc, 1u);
               }
@@ -358,13 +386,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     constexpr bool accurate = MODE == DNNMG_PREC_TF32X3;
-    float h[8][16];                     // fp32 skip state of this thread's row, 128 columns
+    float h[NCH][HC];                   // fp32 skip state of this thread's row, 128 columns
     uint32_t aitem = 0, j = 0;
 
     auto produce_chunk = [&](int c, const float* v) {
       const int s = aitem % C::NA;
       mbar_wait(smem_u32(&a_empty[s]), ((aitem / C::NA) & 1) ^ 1);
-      put_row16<MODE>(aring + s * AST, row_in_tile, 16 * hh, v);
+      put_row<MODE>(aring + s * AST, row_in_tile, HC * hh, v);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
@@ -372,9 +400,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       (void)c;
     };
 
-    const int nck0 = A.K0p / kKC;
+    const int nck0 = A.K0p / KC;
     const bool vec_x = (A.n_in & 3) == 0;
-    float xin[8][16];                   // raw input row slice of the next tile (prefetched)
+    float xin[NCH][HC];                 // raw input row slice of the next tile (prefetched)
     auto load_x = [&](int64_t tile) {
       const int64_t row = tile * kTcM + row_in_tile;
       const bool ok = tile < n_tiles && row < A.n_rows;
@@ -383,20 +411,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         // r of node s - npp, or geometry; indices first, then all value loads in flight
         const int32_t* nt = A.node_table + row * A.npp;
         const int geo4 = A.n_geo / 4;
-        int nidx[8][4];
+        int nidx[NCH][HC / 4];
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int f4 = 8 * c + 4 * hh + j;
+          for (int j = 0; j < HC / 4; ++j) {
+            const int f4 = (KC / 4) * c + (HC / 4) * hh + j;
             const int s = f4 < A.npp ? f4 : f4 - A.npp;
             nidx[c][j] = (ok && c < nck0 && f4 < 2 * A.npp) ? __ldg(nt + s) : 0;
           }
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int f4 = 8 * c + 4 * hh + j;
+          for (int j = 0; j < HC / 4; ++j) {
+            const int f4 = (KC / 4) * c + (HC / 4) * hh + j;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (ok && c < nck0) {
               if (f4 < A.npp) v = __ldg(A.xg + nidx[c][j]);
@@ -413,10 +441,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       }
       const float* xr = A.X + row * A.n_in;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < NCH; ++c) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = c * kKC + 16 * hh + 4 * j;
+        for (int j = 0; j < HC / 4; ++j) {
+          const int col = c * KC + HC * hh + 4 * j;
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
           if (ok && c < nck0) {
             if (vec_x) {
@@ -442,31 +470,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       const bool live = row < A.n_rows;
       // layer-0 operand: normalised input rows (net.py:131), from the prefetched registers
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         if (c < nck0) {
-          float v[16];
+          float v[HC];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int col = c * kKC + 16 * hh + e;
+          for (int e = 0; e < HC; ++e) {
+            const int col = c * KC + HC * hh + e;
             v[e] = (xin[c][e] - p_mean[col]) * p_rstd[col];
           }
           produce_chunk(c, v);
         }
       }
-      // hidden layers: layer 0 writes the skip state, layers >= 1 add to it
-      auto epilogue = [&](int g, auto first) {
+      // hidden layers: h = act(BN(z)) + h with h = 0 entering layer 0 (net.py:151: no skip
+      // for layer 0); one epilogue body keeps the unrolled code (and I-cache footprint) small
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int e = 0; e < HC; ++e) h[c][e] = 0.f;
+      for (int g = 0; g < A.depth; ++g) {
         const int buf = j & 1;
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
         tc_fence_after();
         const float* sc = p_scale + g * kTcH;
         const float* sh = p_shift + g * kTcH;
 #pragma unroll
-        for (int c = 0; c < kTcH / kKC; ++c) {
-          float v[16];
-          tmem_ld16(tmem + lane_addr + buf * kTcH + c * kKC + 16 * hh, v);
+        for (int c = 0; c < NCH; ++c) {
+          float v[HC];
+          tmem_ld<HC>(tmem + lane_addr + buf * kTcH + c * KC + HC * hh, v);
 #pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            const int col = c * kKC + 16 * hh + e;
+          for (int e = 0; e < HC; e += 4) {
+            const int col = c * KC + HC * hh + e;
             const float4 s4 = *reinterpret_cast<const float4*>(sc + col);
             const float4 t4 = *reinterpret_cast<const float4*>(sh + col);
             const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -474,8 +507,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const float a = act_fast(fmaf(v[e + u], sv[u], tv[u]), A.act, accurate);
-              if constexpr (decltype(first)::value) h[c][e + u] = a;
-              else h[c][e + u] = a + h[c][e + u];
+              h[c][e + u] = a + h[c][e + u];
               v[e + u] = h[c][e + u];
             }
           }
@@ -485,9 +517,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
         ++j;
-      };
-      epilogue(0, std::true_type{});
-      for (int g = 1; g < A.depth; ++g) epilogue(g, std::false_type{});
+      }
       // the skip state is dead now: prefetch the next tile's input under the head GEMM
       load_x(tile + gridDim.x);
       // head: Y = h W_depth
@@ -555,16 +585,17 @@ template <int MODE>
 __global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, int Np,
                             uint8_t* __restrict__ out) {
   using C = TcCfg<MODE>;
+  constexpr int KC = C::KC;
   const int64_t total = (int64_t)Kp * Np;
-  const uint32_t part = (uint32_t)Np * kKC * C::ESZ;
+  const uint32_t part = (uint32_t)Np * KC * C::ESZ;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int n = (int)(i % Np);
     const int k = (int)(i / Np);
     const float w = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
-    const int c = k / kKC, kk = k % kKC;
+    const int c = k / KC, kk = k % KC;
     uint8_t* chunk = out + (int64_t)c * part * C::PARTS;
-    const uint32_t off = canon_off<C::ESZ>(n, kk);
+    const uint32_t off = canon_off<C::ESZ, KC>(n, kk);
     if constexpr (MODE == DNNMG_PREC_BF16) {
       *reinterpret_cast<__nv_bfloat16_raw*>(chunk + off) =
           static_cast<__nv_bfloat16_raw>(__float2bfloat16_rn(w));
@@ -589,7 +620,7 @@ static void layout(const dnnmg_mlp_t* m, int64_t* goff, int64_t* total) {
   const int parts = m->precision == DNNMG_PREC_BF16 ? 1 : 2;
   int64_t off = 0;
   for (int g = 0; g <= m->depth; ++g) {
-    const int K = g == 0 ? round_up(m->n_in, kKC) : kTcH;
+    const int K = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : kTcH;
     const int N = g < m->depth ? kTcH : round_up(m->n_out, 16);
     goff[g] = off;
     off += (int64_t)K * N * esz * parts;
@@ -613,7 +644,7 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
   for (int g = 0; g <= m->depth; ++g) {
     const int K = g == 0 ? m->n_in : kTcH;
     const int N = g < m->depth ? kTcH : m->n_out;
-    const int Kp = g == 0 ? round_up(m->n_in, kKC) : kTcH;
+    const int Kp = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : kTcH;
     const int Np = g < m->depth ? kTcH : round_up(m->n_out, 16);
     uint8_t* out = static_cast<uint8_t*>(packed) + goff[g];
     const int64_t n = (int64_t)Kp * Np;
@@ -652,7 +683,7 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.n_out = m->n_out;
   A.depth = m->depth;
   A.act = m->activation;
-  A.K0p = round_up(m->n_in, kKC);
+  A.K0p = round_up(m->n_in, C::KC);
   A.Nhead = round_up(m->n_out, 16);
   A.packed = static_cast<const uint8_t*>(m->packed);
   int64_t total;
@@ -661,8 +692,8 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.shift = m->bn_shift;
   A.in_mean = m->in_mean;
   A.in_std = m->in_std;
-  constexpr int WST = kTcH * kKC * C::ESZ * C::PARTS;
-  constexpr int AST = kTcM * kKC * C::ESZ * C::PARTS;
+  constexpr int WST = kTcH * C::KC * C::ESZ * C::PARTS;
+  constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
   size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 4) + 16 +
                 sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
   const size_t ybytes = (size_t)kTcM * m->n_out * 4;

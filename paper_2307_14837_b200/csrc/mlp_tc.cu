@@ -253,7 +253,7 @@ __device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const 
   }
 }
 
-template <int MODE>
+template <int MODE, bool GATHER>
 __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   using C = TcCfg<MODE>;
   constexpr int KC = C::KC;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     auto load_x = [&](int64_t tile) {
       const int64_t row = tile * kTcM + row_in_tile;
       const bool ok = tile < n_tiles && row < A.n_rows;
-      if (A.node_table) {
+      if constexpr (GATHER) {
         // fused gather (patch_ops.py:49-53): float4 slot s of the row is x~ of node s,
         // r of node s - npp, or geometry; indices first, then all value loads in flight
         const int32_t* nt = A.node_table + row * A.npp;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
             xin[c][4 * j + 3] = v.w;
           }
         return;
-      }
+      } else {
       const float* xr = A.X + row * A.n_in;
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           xin[c][4 * j + 2] = v.z;
           xin[c][4 * j + 3] = v.w;
         }
+      }
       }
     };
     load_x(blockIdx.x);
@@ -706,10 +707,17 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
     A.y_mode = 0;
   }
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: TMEM (512 columns) is per SM
-  cudaFuncSetAttribute(mlp_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t tiles = (n_rows + kTcM - 1) / kTcM;
   const int grid = (int)(tiles < kSMs ? tiles : kSMs);
-  mlp_tc_kernel<MODE><<<grid, kTcThreads, smem, s>>>(A);
+  if (g) {
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    mlp_tc_kernel<MODE, true><<<grid, kTcThreads, smem, s>>>(A);
+  } else {
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    mlp_tc_kernel<MODE, false><<<grid, kTcThreads, smem, s>>>(A);
+  }
   DNNMG_CHECK_LAUNCH("mlp_tc_kernel");
   return DNNMG_OK;
 }

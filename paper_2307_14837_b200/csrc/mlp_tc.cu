@@ -241,10 +241,13 @@ __device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const 
       uint32_t* l = &lo.x;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float x = v[4 * j + e];
-        const uint32_t t = to_tf32(x);
+        // exact split x = hi + lo: hi = x truncated to tf32 (10 mantissa bits), lo = x - hi
+        // (exact), lo rounded to nearest tf32 (|err| <= 2^-11 |lo| <= 2^-21 |x|)
+        const uint32_t xb = __float_as_uint(v[4 * j + e]);
+        const uint32_t t = xb & 0xFFFFE000u;
+        const uint32_t lb = __float_as_uint(v[4 * j + e] - __uint_as_float(t));
         h[e] = t;
-        l[e] = to_tf32(x - __uint_as_float(t));
+        l[e] = (lb + 0x1000u) & 0xFFFFE000u;
       }
       const uint32_t off = canon_off<4, C::KC>(row, kk0 + 4 * j);
       *reinterpret_cast<uint4*>(stage + off) = hi;

@@ -19,10 +19,17 @@
 // Precision modes:
 //   BF16    kind::f16, bf16 A/B, fp32 accumulate in TMEM
 //   TF32X3  kind::tf32, x = hi + lo (both tf32), D += Ahi*Bhi + Ahi*Blo + Alo*Bhi:
-//           fp32-level accuracy (the fp32 parity mode)
+//           fp32-level accuracy
+//   F16X3   kind::f16 with fp16 operands, the same 3-pass split at twice the tf32 rate:
+//           fp16 carries 11 significant bits like tf32, so hi + lo holds 22 bits.  Each
+//           weight matrix is pre-scaled by 2^s (max|W| 2^s < 2^14, exact) to keep hi and
+//           lo in the fp16 normal range; 2^-s is folded into the BN scale (or applied to
+//           the head output), which is exact.  Activations enter unscaled (|h| < 65504:
+//           normalised inputs and tanh skip sums; relu models use TF32X3).
 // Operands use the K-major, no-swizzle canonical layout: 8x16-byte core matrices,
 // LBO = 128 B between K-adjacent core matrices, SBO between 8-row groups.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <type_traits>
 #include "common.cuh"
 
@@ -43,7 +50,16 @@ template <> struct TcCfg<DNNMG_PREC_BF16> {
 template <> struct TcCfg<DNNMG_PREC_TF32X3> {
   static constexpr int ESZ = 4, PARTS = 2, NW = 4, NA = 4, KSTEP = 8, KC = 16;
 };
-static int kc_of(int precision) { return precision == DNNMG_PREC_BF16 ? 32 : 16; }
+template <> struct TcCfg<DNNMG_PREC_F16X3> {
+  static constexpr int ESZ = 2, PARTS = 2, NW = 4, NA = 4, KSTEP = 16, KC = 32;
+};
+static int kc_of(int precision) { return precision == DNNMG_PREC_TF32X3 ? 16 : 32; }
+// packed weight image: header (per-GEMM output unscale 2^-s and shift s), then the chunks
+constexpr int kPackHdr = 1024;
+struct PackHdr {
+  float unscale[DNNMG_MAX_LAYERS];
+  int32_t shift[DNNMG_MAX_LAYERS];
+};
 
 struct TcArgs {
   const float* X;
@@ -124,7 +140,7 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
 template <int MODE>
 __device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                        uint32_t acc) {
-  if constexpr (MODE == DNNMG_PREC_BF16) {
+  if constexpr (MODE != DNNMG_PREC_TF32X3) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
@@ -175,6 +191,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
   return r;
 }
+// x = hi + lo for a pair of values: hi = fp16(x), lo = fp16(x - hi) (x - hi is exact)
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+  const __half2 h2 = *reinterpret_cast<const __half2*>(&hi);
+  const float2 hf = __half22float2(h2);
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - hf.y), "f"(a - hf.x));
+}
 
 // canonical K-major no-swizzle shared-memory matrix descriptor
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo) {
@@ -186,10 +209,14 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo) {
   return d;
 }
 template <int MODE>
+__host__ __device__ constexpr uint32_t ab_format() {  // F16 = 0, BF16 = 1, TF32 = 2
+  return MODE == DNNMG_PREC_BF16 ? 1u : MODE == DNNMG_PREC_TF32X3 ? 2u : 0u;
+}
+template <int MODE>
 __host__ __device__ constexpr uint32_t idesc_for(int N) {
   return (1u << 4)                                              // D = F32
-         | ((MODE == DNNMG_PREC_BF16 ? 1u : 2u) << 7)           // A = BF16 | TF32
-         | ((MODE == DNNMG_PREC_BF16 ? 1u : 2u) << 10)          // B = BF16 | TF32
+         | (ab_format<MODE>() << 7)                             // A format
+         | (ab_format<MODE>() << 10)                            // B format
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
 }
 
@@ -231,6 +258,19 @@ __device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const 
       q.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
       q.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
       *reinterpret_cast<uint4*>(stage + canon_off<2, C::KC>(row, kk0 + 8 * j)) = q;
+    }
+  } else if constexpr (MODE == DNNMG_PREC_F16X3) {
+    constexpr int part = kTcM * C::KC * C::ESZ;
+#pragma unroll
+    for (int j = 0; j < HC / 8; ++j) {
+      uint4 hi, lo;
+      split_f16x2(v[8 * j + 0], v[8 * j + 1], hi.x, lo.x);
+      split_f16x2(v[8 * j + 2], v[8 * j + 3], hi.y, lo.y);
+      split_f16x2(v[8 * j + 4], v[8 * j + 5], hi.z, lo.z);
+      split_f16x2(v[8 * j + 6], v[8 * j + 7], hi.w, lo.w);
+      const uint32_t off = canon_off<2, C::KC>(row, kk0 + 8 * j);
+      *reinterpret_cast<uint4*>(stage + off) = hi;
+      *reinterpret_cast<uint4*>(stage + part + off) = lo;
     }
   } else {
     constexpr int part = kTcM * C::KC * C::ESZ;
@@ -281,10 +321,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   float* p_shift = p_scale + A.depth * kTcH;
   float* p_mean = p_shift + A.depth * kTcH;
   float* p_rstd = p_mean + kTcH;
+  const PackHdr* hdr = reinterpret_cast<const PackHdr*>(A.packed);
   for (int i = threadIdx.x; i < A.depth * kTcH; i += blockDim.x) {
-    p_scale[i] = A.scale[i];
+    p_scale[i] = A.scale[i] * hdr->unscale[i / kTcH];  // 2^-s: exact
     p_shift[i] = A.shift[i];
   }
+  const float y_unscale = hdr->unscale[A.depth];
   float* y_stage = A.y_mode == 1 ? reinterpret_cast<float*>(aring) : p_rstd + kTcH;
   for (int i = threadIdx.x; i < kTcH; i += blockDim.x) {
     p_mean[i] = i < A.n_in ? A.in_mean[i] : 0.f;
@@ -368,9 +410,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
               const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
               const uint64_t ahi = sdesc(ab + koff, SBO), bhi = sdesc(wb + koff, SBO);
               tc_mma<MODE>(d, ahi, bhi, idesc, acc);
-              if constexpr (MODE == DNNMG_PREC_TF32X3) {
-                const uint64_t alo = sdesc(ab + kTcM * KC * 4 + koff, SBO);
-                const uint64_t blo = sdesc(wb + (uint32_t)N * KC * 4 + koff, SBO);
+              if constexpr (C::PARTS == 2) {
+                const uint64_t alo = sdesc(ab + kTcM * KC * C::ESZ + koff, SBO);
+                const uint64_t blo = sdesc(wb + (uint32_t)N * KC * C::ESZ + koff, SBO);
                 tc_mma<MODE>(d, ahi, blo, idesc, 1u);
                 tc_mma<MODE>(d, alo, bhi, idesc, 1u);
               }
@@ -388,7 +430,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     const int hh = warp >> 2;           // which 16-column half of every 32-column chunk
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    constexpr bool accurate = MODE == DNNMG_PREC_TF32X3;
+    constexpr bool accurate = MODE != DNNMG_PREC_BF16;
     float h[NCH][HC];                   // fp32 skip state of this thread's row, 128 columns
     uint32_t aitem = 0, j = 0;
 
@@ -537,7 +579,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const int col = sl * 16 + e;
-                if (col < A.n_out) A.Y[row * A.n_out + col] = v[e];
+                if (col < A.n_out) A.Y[row * A.n_out + col] = v[e] * y_unscale;
               }
             }
           }
@@ -551,7 +593,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const int col = sl * 16 + e;
-            if (col < A.n_out) ys[row_in_tile * A.n_out + col] = v[e];
+            if (col < A.n_out) ys[row_in_tile * A.n_out + col] = v[e] * y_unscale;
           }
         }
         tc_fence_before();
@@ -585,9 +627,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
 }
 
 // ---- weight packing: W[g] (K x N row-major fp32) -> canonical chunk images -----
+// per-GEMM exponent s with max|W| 2^s < 2^14 (F16X3), else s = 0; one block
+__global__ void pack_scale_kernel(const float* __restrict__ W, int size, int mode, int g,
+                                  PackHdr* __restrict__ hdr) {
+  float m = 0.f;
+  for (int i = threadIdx.x; i < size; i += blockDim.x) m = fmaxf(m, fabsf(W[i]));
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, red[i]);
+    m = fmaxf(m, red[0]);
+    int s = 0;
+    if (mode == DNNMG_PREC_F16X3 && m > 0.f && isfinite(m)) {
+      int e;
+      frexpf(m, &e);  // m < 2^e
+      s = 14 - e;
+    }
+    hdr->shift[g] = s;
+    hdr->unscale[g] = ldexpf(1.0f, -s);
+  }
+}
+
 template <int MODE>
 __global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, int Np,
-                            uint8_t* __restrict__ out) {
+                            const PackHdr* __restrict__ hdr, int g, uint8_t* __restrict__ out) {
+  const int shift = hdr->shift[g];
   using C = TcCfg<MODE>;
   constexpr int KC = C::KC;
   const int64_t total = (int64_t)Kp * Np;
@@ -603,6 +669,11 @@ __global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, i
     if constexpr (MODE == DNNMG_PREC_BF16) {
       *reinterpret_cast<__nv_bfloat16_raw*>(chunk + off) =
           static_cast<__nv_bfloat16_raw>(__float2bfloat16_rn(w));
+    } else if constexpr (MODE == DNNMG_PREC_F16X3) {
+      const float ws = ldexpf(w, shift);  // exact power-of-two scaling
+      const __half hi = __float2half_rn(ws);
+      *reinterpret_cast<__half*>(chunk + off) = hi;
+      *reinterpret_cast<__half*>(chunk + part + off) = __float2half_rn(ws - __half2float(hi));
     } else {
       const uint32_t hi = to_tf32(w);
       *reinterpret_cast<uint32_t*>(chunk + off) = hi;
@@ -614,15 +685,16 @@ __global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, i
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 int32_t mlp_tc_supported(const dnnmg_mlp_t* m) {
-  return (m->precision == DNNMG_PREC_BF16 || m->precision == DNNMG_PREC_TF32X3) &&
+  return (m->precision == DNNMG_PREC_BF16 || m->precision == DNNMG_PREC_TF32X3 ||
+          m->precision == DNNMG_PREC_F16X3) &&
          m->n_hidden == kTcH && m->n_in <= kTcH && m->n_out <= kTcH && m->depth >= 1 &&
          m->depth < DNNMG_MAX_LAYERS;
 }
 
 static void layout(const dnnmg_mlp_t* m, int64_t* goff, int64_t* total) {
-  const int esz = m->precision == DNNMG_PREC_BF16 ? 2 : 4;
+  const int esz = m->precision == DNNMG_PREC_TF32X3 ? 4 : 2;
   const int parts = m->precision == DNNMG_PREC_BF16 ? 1 : 2;
-  int64_t off = 0;
+  int64_t off = kPackHdr;
   for (int g = 0; g <= m->depth; ++g) {
     const int K = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : kTcH;
     const int N = g < m->depth ? kTcH : round_up(m->n_out, 16);
@@ -645,6 +717,13 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
                 "mlp: tensor-core mode needs n_hidden == 256, n_in <= 256, n_out <= 256");
   int64_t goff[DNNMG_MAX_LAYERS], total;
   layout(m, goff, &total);
+  PackHdr* hdr = static_cast<PackHdr*>(packed);
+  static_assert(sizeof(PackHdr) <= kPackHdr, "pack header");
+  for (int g = 0; g <= m->depth; ++g) {
+    const int size = (g == 0 ? m->n_in : kTcH) * (g < m->depth ? kTcH : m->n_out);
+    pack_scale_kernel<<<1, 256, 0, s>>>(m->W[g], size, m->precision, g, hdr);
+    DNNMG_CHECK_LAUNCH("pack_scale_kernel");
+  }
   for (int g = 0; g <= m->depth; ++g) {
     const int K = g == 0 ? m->n_in : kTcH;
     const int N = g < m->depth ? kTcH : m->n_out;
@@ -653,9 +732,11 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
     uint8_t* out = static_cast<uint8_t*>(packed) + goff[g];
     const int64_t n = (int64_t)Kp * Np;
     if (m->precision == DNNMG_PREC_BF16)
-      pack_kernel<DNNMG_PREC_BF16><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, out);
+      pack_kernel<DNNMG_PREC_BF16><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, hdr, g, out);
+    else if (m->precision == DNNMG_PREC_F16X3)
+      pack_kernel<DNNMG_PREC_F16X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, hdr, g, out);
     else
-      pack_kernel<DNNMG_PREC_TF32X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, out);
+      pack_kernel<DNNMG_PREC_TF32X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, hdr, g, out);
     DNNMG_CHECK_LAUNCH("pack_kernel");
   }
   return DNNMG_OK;
@@ -728,6 +809,7 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
 int32_t launch_mlp_tc(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
                       cudaStream_t s) {
   if (m->precision == DNNMG_PREC_BF16) return launch_mode<DNNMG_PREC_BF16>(m, X, n_rows, Y, s, nullptr);
+  if (m->precision == DNNMG_PREC_F16X3) return launch_mode<DNNMG_PREC_F16X3>(m, X, n_rows, Y, s, nullptr);
   return launch_mode<DNNMG_PREC_TF32X3>(m, X, n_rows, Y, s, nullptr);
 }
 
@@ -741,6 +823,8 @@ int32_t launch_mlp_tc_gather(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, c
   GatherSrc g{ps->node_table, x, r, ps->geom, ps->nodes_per_patch, ps->n_geo};
   if (m->precision == DNNMG_PREC_BF16)
     return launch_mode<DNNMG_PREC_BF16>(m, nullptr, ps->n_patches, Y, s, &g);
+  if (m->precision == DNNMG_PREC_F16X3)
+    return launch_mode<DNNMG_PREC_F16X3>(m, nullptr, ps->n_patches, Y, s, &g);
   return launch_mode<DNNMG_PREC_TF32X3>(m, nullptr, ps->n_patches, Y, s, &g);
 }
 

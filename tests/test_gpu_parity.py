@@ -206,17 +206,17 @@ def test_zero_state_zero_residual(ps3):
 
 # ---- tensor-core MLP modes (tcgen05): fp32-accurate 3xTF32 and bf16 ----------------------
 
-TC_TOL = {"tf32x3": 1e-5, "bf16": 2e-2}
+TC_TOL = {"tf32x3": 1e-5, "f16x3": 1e-5, "bf16": 2e-2}
 
 
-@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+@pytest.mark.parametrize("precision", ["tf32x3", "f16x3", "bf16"])
 def test_forward_tc_cfg0(precision):
     g = load_golden("cfg0")
     Y = net.forward(product_model(g), g["X"], precision=precision)
     assert rel(Y, g["Y"]) < TC_TOL[precision], rel(Y, g["Y"])
 
 
-@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+@pytest.mark.parametrize("precision", ["tf32x3", "f16x3", "bf16"])
 def test_predict_correction_tc_cfg0(precision):
     g = load_golden("cfg0")
     h = product_hierarchy(g)
@@ -226,7 +226,7 @@ def test_predict_correction_tc_cfg0(precision):
     assert rel(d, g["d"]) < TC_TOL[precision], rel(d, g["d"])
 
 
-@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+@pytest.mark.parametrize("precision", ["tf32x3", "f16x3", "bf16"])
 def test_fused_step_tc_cfg0(precision):
     g = load_golden("cfg0")
     h = product_hierarchy(g)
@@ -239,7 +239,7 @@ def test_fused_step_tc_cfg0(precision):
     assert rel(step.d.cpu().numpy(), g["d"]) < TC_TOL[precision]
 
 
-@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+@pytest.mark.parametrize("precision", ["tf32x3", "f16x3", "bf16"])
 @pytest.mark.parametrize("shape", [(240, 3, 81, "tanh", 1000, False), (174, 3, 81, "tanh", 4097, False),
                                    (240, 4, 81, "relu", 300, True), (256, 1, 200, "tanh", 129, True)])
 def test_forward_tc_random(precision, shape):

@@ -43,7 +43,7 @@ def problem():
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3", "f16x3"])
 def test_inprocess_slabs_match_single_domain(problem, world, precision):
     gh, m, x1, b, d_ref, xc_ref = problem
     g_fine, g_coarse = global_index(gh, 1), global_index(gh, 0)
@@ -68,7 +68,7 @@ def test_inprocess_slabs_match_single_domain(problem, world, precision):
     for s, fid, o in zip(steps, fids, outs):
         d[fid] = s.step.d.double().cpu().numpy().reshape(-1, 4)
         xc[fid] = o.double().cpu().numpy().reshape(-1, 4)
-    tol = 1e-5 if precision == "tf32x3" else 1e-6
+    tol = 1e-5 if precision in ("tf32x3", "f16x3") else 1e-6
     assert rel(d.reshape(-1), d_ref) < tol
     assert rel(xc.reshape(-1), xc_ref) < tol
     for r in range(world - 1):  # both sides of every interface hold identical values

@@ -272,3 +272,33 @@ def test_tc_rejects_unsupported_width():
     m = net.MlpModel(net.Architecture(240, 128, 3, 81), activation="tanh").eval()
     with pytest.raises(NotImplementedError):
         net.forward(m, np.zeros((4, 240)), precision="bf16")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "f16x3"])
+def test_host_pipeline_matches_run(precision):
+    """step.HostPipeline (H2D / kernels / D2H overlapped on three streams,
+    double-buffered) returns exactly what CorrectionStep.run returns per step."""
+    from paper_2307_14837_b200.step import HostPipeline
+    g = load_golden("cfg0")
+    h = product_hierarchy(g)
+    step = CorrectionStep(h, 0, 1, product_model(g), float(g["nu"]), float(g["k"]),
+                          precision=precision, t=float(g["t"]))
+    rng = np.random.default_rng(5)
+    ins = []
+    for i in range(5):
+        xc = (g["x_coarse"] * (1.0 + 0.1 * i) + 0.01 * rng.standard_normal(g["x_coarse"].shape))
+        b = g["b_prev"] * (1.0 - 0.05 * i)
+        ins.append((torch.tensor(xc, dtype=torch.float32).pin_memory(),
+                    torch.tensor(b, dtype=torch.float32).pin_memory()))
+    ref = []
+    for xc, b in ins:
+        ref.append(step(xc.cuda(), b.cuda()).cpu().clone())
+    outs = [torch.empty_like(ref[0]).pin_memory() for _ in ins]
+    pipe = HostPipeline(step)
+    pipe.begin()
+    for (xc, b), o in zip(ins, outs):
+        pipe.submit(xc, b, o)
+    pipe.join()
+    torch.cuda.synchronize()
+    for o, r in zip(outs, ref):
+        assert torch.equal(o, r)

@@ -66,22 +66,20 @@ constexpr int oU = 0;                  // u[f][27]
 constexpr int oSX = 192;               // sx[f][2][9][4]          | backward tx[8][3][16][3]
 constexpr int kSXF = 116;             // sx field stride: [kind][iz (stride 20)][qx][iy, pad]
 constexpr int oSY = oSX + kNF * kSXF;  // sy[f][kind*3+iz][16 yx]
-constexpr int oCF = oSX + kNF * (kSXF + 144);  // cf[22][64]: A[4], B[4][3], dg[3], pvr[3]
+constexpr int oCF = oSX + kNF * (kSXF + 144);  // cf[22][kCFS]: A[4], dg[3], pvr[3], B[4][3]
 constexpr int kNCF = 22;
-constexpr int oTZ = oCF + kNCF * 64;   // tz[4][2][27]
-constexpr int kCellFloats = (oTZ + 4 * 2 * 27 + 3) / 4 * 4;
-constexpr int kTXS = 172;             // per (comp, part) stride of tx: 144 + pad, = 12 (mod 32)
-constexpr int kTYS = 73;              // per (comp, part) stride of ty: 72 + pad,  = 9 (mod 32)
-constexpr int oTX = oSX;              // tx aliases the forward scratch (dead after pointwise)
-constexpr int oTY = oCF;              // ty aliases cf (dead after backward x)
-static_assert(oTX + 8 * kTXS <= oCF, "tx must fit in the forward scratch");
-static_assert(8 * kTYS <= kNCF * 64, "ty must fit in the coefficient region");
+// coefficient array stride: 64 Gauss points + 4, so that array a starts in bank 4a (mod 32)
+// and the eight (comp, part) lines of the backward stage read eight different banks
+constexpr int kCFS = 68;
+constexpr int oTZ = oSX;              // tz[4][2][27] aliases the forward scratch (dead by then)
+constexpr int kCellFloats = (oCF + kNCF * kCFS + 3) / 4 * 4;
+static_assert(oTZ + 4 * 2 * 27 <= oCF, "tz must fit in the forward scratch");
 static_assert(oSX % 4 == 0 && oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
-// coefficient arrays
+// coefficient arrays (numbered so that every backward load slot hits distinct banks)
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
-constexpr int CB = 4;        // B[c][k]   reference-gradient test
-constexpr int CDG = 16;      // dg[i] = delta*w*g_i           (LPS, Gpi test, comps 1..3)
-constexpr int CPV = 19;      // pvr[k] = (J^-1 pi v)_k
+constexpr int CDG = 4;       // dg[i] = delta*w*g_i           (LPS, Gpi test, comps 1..3)
+constexpr int CPV = 7;       // pvr[k] = (J^-1 pi v)_k
+constexpr int CB = 10;       // B[c][k]   reference-gradient test
 constexpr int kWarpsPerBlock = 5;
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
@@ -135,6 +133,7 @@ __device__ __forceinline__ void load_raw(const ResidualArgs& A, int c, int node,
 }
 
 // coefficients of one Gauss point (pointwise phase); F = Q2 fields at q
+template <int MODE>
 __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S, float* CF, int q,
                                           float F[kNF][4], float aT, float dT) {
   const int qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
@@ -171,9 +170,9 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #pragma unroll
   for (int i = 0; i < 3; ++i)
     conv[i] = A.convection ? v[0] * gv[i][0] + v[1] * gv[i][1] + v[2] * gv[i][2] : 0.f;
-#define CFW(arr) CF[(arr) * 64 + q]
+#define CFW(arr) CF[(arr) * kCFS + q]
   const float ik = 1.0f / A.k;
-  if (A.mode == MODE_OPERATOR) {
+  if constexpr (MODE == MODE_OPERATOR) {
     const float p = F[3][0];
     // Q1 (pi) fields: trilinear in the vertex values, at this Gauss point
     const float lx1 = cX[qx], ly1 = cX[qy], lz1 = cX[qz];
@@ -269,6 +268,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #undef CFW
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(ResidualArgs A) {
   extern __shared__ __align__(16) float smem[];
   const int wib = threadIdx.x >> 5;
@@ -382,106 +382,76 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
           G[f][3] = cD[qz + 2][0] * vv0 + cD[qz + 2][1] * vv1 + cD[qz + 2][2] * vv2;
         }
       }
-      pointwise(A, S, S + oCF, t, F, aT, dT);
-      pointwise(A, S, S + oCF, t + 32, G, aT, dT);
+      pointwise<MODE>(A, S, S + oCF, t, F, aT, dT);
+      pointwise<MODE>(A, S, S + oCF, t + 32, G, aT, dT);
     }
     __syncwarp();
-    // ---------------- backward x (contract qx): line (comp, part, zy) ----------------
+    // ---------------- backward x, y, z in registers: lane (cp, ix), cp = (comp, part) ----------------
+    // tz[cp][iz][iy][ix] = sum_q test(q; ix, iy, iz) . coefficients(cp, q): the x contraction
+    // of a (qy, qz) line feeds the y partial sums of that qz, which feed the z sums.  Part 0
+    // is the direct test (A N + B_k dN/dxi_k); part 1 the LPS test through PI^T:
+    // comp 0: -B_0k, comps 1..3: -dg_i (J^-1 pi v)_k (elements.py:96-118, assembly.py:120-140).
+    if (t < 24) {
+      const int cp = t / 3, ix = t - 3 * (t / 3);
+      const int comp = cp >> 1, part = cp & 1;
+      const bool prod = part == 1 && comp > 0;
+      const float sgn = part == 0 ? 1.f : -1.f, a_on = part == 0 ? 1.f : 0.f;
+      const int a0 = prod ? CDG + comp - 1 : CA + comp;
+      const int a1 = prod ? CPV : CB + 3 * comp;
+      const float* c0 = S + oCF + a0 * kCFS;
+      const float* c1 = S + oCF + a1 * kCFS;
+      const float* c2 = c1 + kCFS;
+      const float* c3 = c1 + 2 * kCFS;
+      float bx[4], dx[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int l = t + 32 * r;
-      const int comp = l >> 5, part = (l >> 4) & 1, zy = l & 15;
-      const float* cf = S + oCF + zy * 4;
-      float Av[4], B0[4], B1[4], B2[4];
-      if (part == 0) {
-        const float4 a4 = *reinterpret_cast<const float4*>(cf + (CA + comp) * 64);
-        const float4 x4 = *reinterpret_cast<const float4*>(cf + (CB + 3 * comp) * 64);
-        const float4 y4 = *reinterpret_cast<const float4*>(cf + (CB + 3 * comp + 1) * 64);
-        const float4 z4 = *reinterpret_cast<const float4*>(cf + (CB + 3 * comp + 2) * 64);
-        Av[0] = a4.x; Av[1] = a4.y; Av[2] = a4.z; Av[3] = a4.w;
-        B0[0] = x4.x; B0[1] = x4.y; B0[2] = x4.z; B0[3] = x4.w;
-        B1[0] = y4.x; B1[1] = y4.y; B1[2] = y4.z; B1[3] = y4.w;
-        B2[0] = z4.x; B2[1] = z4.y; B2[2] = z4.z; B2[3] = z4.w;
-      } else if (comp == 0) {  // continuity LPS: (G - Gpi) test -> Gpi part is -B_0
-        const float4 x4 = *reinterpret_cast<const float4*>(cf + (CB + 0) * 64);
-        const float4 y4 = *reinterpret_cast<const float4*>(cf + (CB + 1) * 64);
-        const float4 z4 = *reinterpret_cast<const float4*>(cf + (CB + 2) * 64);
-        Av[0] = Av[1] = Av[2] = Av[3] = 0.f;
-        B0[0] = -x4.x; B0[1] = -x4.y; B0[2] = -x4.z; B0[3] = -x4.w;
-        B1[0] = -y4.x; B1[1] = -y4.y; B1[2] = -y4.z; B1[3] = -y4.w;
-        B2[0] = -z4.x; B2[1] = -z4.y; B2[2] = -z4.z; B2[3] = -z4.w;
-      } else {  // momentum LPS: -delta*w*g_i (J^-1 pi v) through the Gpi test
-        const float4 g4 = *reinterpret_cast<const float4*>(cf + (CDG + comp - 1) * 64);
-        const float4 p0 = *reinterpret_cast<const float4*>(cf + (CPV + 0) * 64);
-        const float4 p1 = *reinterpret_cast<const float4*>(cf + (CPV + 1) * 64);
-        const float4 p2 = *reinterpret_cast<const float4*>(cf + (CPV + 2) * 64);
-        const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
-        const float a0[4] = {p0.x, p0.y, p0.z, p0.w};
-        const float a1[4] = {p1.x, p1.y, p1.z, p1.w};
-        const float a2[4] = {p2.x, p2.y, p2.z, p2.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          Av[i] = 0.f;
-          B0[i] = -gg[i] * a0[i];
-          B1[i] = -gg[i] * a1[i];
-          B2[i] = -gg[i] * a2[i];
-        }
+      for (int qq = 0; qq < 4; ++qq) {
+        bx[qq] = ix == 0 ? cB[qq][0] : ix == 1 ? cB[qq][1] : cB[qq][2];
+        dx[qq] = ix == 0 ? cD[qq][0] : ix == 1 ? cD[qq][1] : cD[qq][2];
       }
-      // tx[cp][arr][qy][qz][ix]
-      float* o = S + oTX + (comp * 2 + part) * kTXS + (zy & 3) * 12 + (zy >> 2) * 3;
+      float o[3][3];
 #pragma unroll
-      for (int ix = 0; ix < 3; ++ix) {
-        float tv = 0.f, t1 = 0.f, t2 = 0.f;
+      for (int iz = 0; iz < 3; ++iz)
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          tv += cB[qq][ix] * Av[qq] + cD[qq][ix] * B0[qq];
-          t1 += cB[qq][ix] * B1[qq];
-          t2 += cB[qq][ix] * B2[qq];
+        for (int iy = 0; iy < 3; ++iy) o[iz][iy] = 0.f;
+#pragma unroll 1
+      for (int qz = 0; qz < 4; ++qz) {  // rolled: keeps the kernel inside the instruction cache
+        float ua[3] = {0.f, 0.f, 0.f}, ub[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int qy = 0; qy < 4; ++qy) {
+          const int zy = (qy + 4 * qz) * 4;
+          const float4 l0 = *reinterpret_cast<const float4*>(c0 + zy);
+          const float4 l1 = *reinterpret_cast<const float4*>(c1 + zy);
+          const float4 l2 = *reinterpret_cast<const float4*>(c2 + zy);
+          const float4 l3 = *reinterpret_cast<const float4*>(c3 + zy);
+          const float L0[4] = {l0.x, l0.y, l0.z, l0.w};
+          const float L1[4] = {l1.x, l1.y, l1.z, l1.w};
+          const float L2[4] = {l2.x, l2.y, l2.z, l2.w};
+          const float L3[4] = {l3.x, l3.y, l3.z, l3.w};
+          float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+#pragma unroll
+          for (int qx = 0; qx < 4; ++qx) {
+            const float m = prod ? -L0[qx] : sgn;
+            t0 = fmaf(bx[qx], a_on * L0[qx], t0);
+            t0 = fmaf(dx[qx], m * L1[qx], t0);
+            t1 = fmaf(bx[qx], m * L2[qx], t1);
+            t2 = fmaf(bx[qx], m * L3[qx], t2);
+          }
+#pragma unroll
+          for (int iy = 0; iy < 3; ++iy) {
+            ua[iy] += cB[qy][iy] * t0 + cD[qy][iy] * t1;
+            ub[iy] += cB[qy][iy] * t2;
+          }
         }
-        o[ix] = tv;
-        o[48 + ix] = t1;
-        o[96 + ix] = t2;
+#pragma unroll
+        for (int iz = 0; iz < 3; ++iz)
+#pragma unroll
+          for (int iy = 0; iy < 3; ++iy) o[iz][iy] += cB[qz][iz] * ua[iy] + cD[qz][iz] * ub[iy];
       }
-    }
-    __syncwarp();
-    // ---------------- backward y (contract qy): line (cp, qz, ix) ----------------
+      float* out = S + oTZ + cp * 27 + ix;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int l = t + 32 * r;
-      // line (cp, qz, ix): lanes walk l % 12 = qz*3 + ix contiguously in tx
-      const int cp = l / 12, zx = l - 12 * (l / 12), lz = zx / 3, ix = zx - 3 * (zx / 3);
-      const float* tx = S + oTX + cp * kTXS + zx;       // tx[cp][arr][qy][qz*3+ix]
-      float* o = S + oTY + cp * kTYS + lz * 9 + ix;     // ty[cp][arr][qz][iy*3+ix]
+      for (int iz = 0; iz < 3; ++iz)
 #pragma unroll
-      for (int iy = 0; iy < 3; ++iy) {
-        float ua = 0.f, ub = 0.f;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          ua += cB[qq][iy] * tx[qq * 12] + cD[qq][iy] * tx[48 + qq * 12];
-          ub += cB[qq][iy] * tx[96 + qq * 12];
-        }
-        o[iy * 3] = ua;
-        o[36 + iy * 3] = ub;
-      }
-    }
-    __syncwarp();
-    // ---------------- backward z (contract qz): line (cp, yx) ----------------
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int l = t + 32 * r;
-      if (l < 4 * 2 * 9) {
-        // lanes walk l = cp*9 + yx: consecutive words of ty (stride 73 = 9 mod 32)
-        const int cp = l / 9, yx = l - 9 * (l / 9);
-        const float* ty = S + oTY + cp * kTYS + yx;  // [arr*36 + qz*9 + iy*3 + ix]
-        float* o = S + oTZ + cp * 27 + yx;
-#pragma unroll
-        for (int iz = 0; iz < 3; ++iz) {
-          float sacc = 0.f;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) sacc += cB[qq][iz] * ty[qq * 9] + cD[qq][iz] * ty[36 + qq * 9];
-          o[iz * 9] = sacc;
-        }
-      }
+        for (int iy = 0; iy < 3; ++iy) out[9 * iz + 3 * iy] = o[iz][iy];
     }
     __syncwarp();
     // ---------------- output: direct + PI^T * (LPS part), one float4 per node ----------------
@@ -590,17 +560,23 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
   const size_t smem = sizeof(float) * kCellFloats * kWarpsPerBlock;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(element_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(element_kernel<MODE_OPERATOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(element_kernel<MODE_RHS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     configured = true;
   }
   int blocks = (lv->n_cells + kWarpsPerBlock - 1) / kWarpsPerBlock;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel, 32 * kWarpsPerBlock, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel<MODE_OPERATOR>,
+                                                32 * kWarpsPerBlock, smem);
   const int cap = kSMs * (per_sm > 0 ? per_sm : 1);
   if (blocks > cap) blocks = cap;
   if (lv->n_cells == 0) return DNNMG_OK;
-  element_kernel<<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+  if (mode == MODE_OPERATOR)
+    element_kernel<MODE_OPERATOR><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+  else
+    element_kernel<MODE_RHS><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
   DNNMG_CHECK_LAUNCH("element_kernel");
   return DNNMG_OK;
 }

@@ -66,8 +66,8 @@ constexpr int oU = 0;                  // u[f][27]
 constexpr int oSX = 192;               // sx[f][2][9][4]          | backward tx[8][3][16][3]
 constexpr int kSXF = 116;             // sx field stride: [kind][iz (stride 20)][qx][iy, pad]
 constexpr int oSY = oSX + kNF * kSXF;  // sy[f][kind*3+iz][16 yx]
-constexpr int oCF = oSX + kNF * (kSXF + 144);  // cf[22][kCFS]: A[4], dg[3], pvr[3], B[4][3]
-constexpr int kNCF = 22;
+constexpr int oCF = oSX + kNF * (kSXF + 144);  // cf[25][kCFS]: A[4], B[4][3], P[3][3]
+constexpr int kNCF = 25;
 // coefficient array stride: 64 Gauss points + 4, so that array a starts in bank 4a (mod 32)
 // and the eight (comp, part) lines of the backward stage read eight different banks
 constexpr int kCFS = 68;
@@ -77,9 +77,8 @@ static_assert(oTZ + 4 * 2 * 27 <= oCF, "tz must fit in the forward scratch");
 static_assert(oSX % 4 == 0 && oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
-constexpr int CDG = 4;       // dg[i] = delta*w*g_i           (LPS, Gpi test, comps 1..3)
-constexpr int CPV = 7;       // pvr[k] = (J^-1 pi v)_k
-constexpr int CB = 10;       // B[c][k]   reference-gradient test
+constexpr int CB = 4;        // B[c][k]   reference-gradient test
+constexpr int CP = 16;       // P[i][k] = delta*w*g_i (J^-1 pi v)_k: LPS Gpi test, comps 1..3
 constexpr int kWarpsPerBlock = 5;
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
@@ -238,7 +237,8 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
     for (int i = 0; i < 3; ++i) {
       CFW(CA + 1 + i) = w * (v[i] * ik + 0.5f * conv[i]);
       const float dg = dT * w * g[i];
-      CFW(CDG + i) = dg;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) CFW(CP + 3 * i + kk) = dg * pvr[kk];
       float Fi[3];
 #pragma unroll
       for (int j = 0; j < 3; ++j) Fi[j] = hn * gv[i][j] + dg * v[j] - (i == j ? w * p : 0.f);
@@ -246,8 +246,6 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
       for (int kk = 0; kk < 3; ++kk)
         CFW(CB + 3 * (1 + i) + kk) = Ji[kk][0] * Fi[0] + Ji[kk][1] * Fi[1] + Ji[kk][2] * Fi[2];
     }
-#pragma unroll
-    for (int kk = 0; kk < 3; ++kk) CFW(CPV + kk) = pvr[kk];
   } else {  // MODE_RHS (assembly.py:242-259, f = None)
     const float hn = -0.5f * A.nu * w;
     CFW(CA + 0) = 0.f;
@@ -256,14 +254,11 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       CFW(CA + 1 + i) = w * (v[i] * ik - 0.5f * conv[i]);
-      CFW(CDG + i) = 0.f;
 #pragma unroll
       for (int kk = 0; kk < 3; ++kk)
         CFW(CB + 3 * (1 + i) + kk) =
             hn * (Ji[kk][0] * gv[i][0] + Ji[kk][1] * gv[i][1] + Ji[kk][2] * gv[i][2]);
     }
-#pragma unroll
-    for (int kk = 0; kk < 3; ++kk) CFW(CPV + kk) = 0.f;
   }
 #undef CFW
 }
@@ -391,22 +386,23 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
     // of a (qy, qz) line feeds the y partial sums of that qz, which feed the z sums.  Part 0
     // is the direct test (A N + B_k dN/dxi_k); part 1 the LPS test through PI^T:
     // comp 0: -B_0k, comps 1..3: -dg_i (J^-1 pi v)_k (elements.py:96-118, assembly.py:120-140).
-    if (t < 24) {
+    // (the RHS form has no LPS part: its part-1 lanes and the PI^T fold are skipped)
+    if (t < 24 && (MODE == MODE_OPERATOR || (t / 3) % 2 == 0)) {
       const int cp = t / 3, ix = t - 3 * (t / 3);
       const int comp = cp >> 1, part = cp & 1;
-      const bool prod = part == 1 && comp > 0;
-      const float sgn = part == 0 ? 1.f : -1.f, a_on = part == 0 ? 1.f : 0.f;
-      const int a0 = prod ? CDG + comp - 1 : CA + comp;
-      const int a1 = prod ? CPV : CB + 3 * comp;
-      const float* c0 = S + oCF + a0 * kCFS;
-      const float* c1 = S + oCF + a1 * kCFS;
+      // part 0: A_c, B_c0..2; part 1: comp 0 -> B_00..02, comps 1..3 -> P_(c-1)0..2; part 1 has
+      // no value test (a_on = 0) and enters with a minus sign
+      const float* c0 = S + oCF + (CA + comp) * kCFS;
+      const float* c1 =
+          S + oCF + (part == 0 || comp == 0 ? CB + 3 * comp : CP + 3 * (comp - 1)) * kCFS;
       const float* c2 = c1 + kCFS;
       const float* c3 = c1 + 2 * kCFS;
-      float bx[4], dx[4];
+      float bxa[4], bx[4], dx[4];
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {
         bx[qq] = ix == 0 ? cB[qq][0] : ix == 1 ? cB[qq][1] : cB[qq][2];
         dx[qq] = ix == 0 ? cD[qq][0] : ix == 1 ? cD[qq][1] : cD[qq][2];
+        bxa[qq] = part == 0 ? bx[qq] : 0.f;
       }
       float o[3][3];
 #pragma unroll
@@ -423,19 +419,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
           const float4 l1 = *reinterpret_cast<const float4*>(c1 + zy);
           const float4 l2 = *reinterpret_cast<const float4*>(c2 + zy);
           const float4 l3 = *reinterpret_cast<const float4*>(c3 + zy);
-          const float L0[4] = {l0.x, l0.y, l0.z, l0.w};
-          const float L1[4] = {l1.x, l1.y, l1.z, l1.w};
-          const float L2[4] = {l2.x, l2.y, l2.z, l2.w};
-          const float L3[4] = {l3.x, l3.y, l3.z, l3.w};
-          float t0 = 0.f, t1 = 0.f, t2 = 0.f;
-#pragma unroll
-          for (int qx = 0; qx < 4; ++qx) {
-            const float m = prod ? -L0[qx] : sgn;
-            t0 = fmaf(bx[qx], a_on * L0[qx], t0);
-            t0 = fmaf(dx[qx], m * L1[qx], t0);
-            t1 = fmaf(bx[qx], m * L2[qx], t1);
-            t2 = fmaf(bx[qx], m * L3[qx], t2);
-          }
+          float t0 = bxa[0] * l0.x, t1 = bx[0] * l2.x, t2 = bx[0] * l3.x;
+          t0 = fmaf(bxa[1], l0.y, t0); t0 = fmaf(bxa[2], l0.z, t0); t0 = fmaf(bxa[3], l0.w, t0);
+          t0 = fmaf(dx[0], l1.x, t0); t0 = fmaf(dx[1], l1.y, t0);
+          t0 = fmaf(dx[2], l1.z, t0); t0 = fmaf(dx[3], l1.w, t0);
+          t1 = fmaf(bx[1], l2.y, t1); t1 = fmaf(bx[2], l2.z, t1); t1 = fmaf(bx[3], l2.w, t1);
+          t2 = fmaf(bx[1], l3.y, t2); t2 = fmaf(bx[2], l3.z, t2); t2 = fmaf(bx[3], l3.w, t2);
 #pragma unroll
           for (int iy = 0; iy < 3; ++iy) {
             ua[iy] += cB[qy][iy] * t0 + cD[qy][iy] * t1;
@@ -446,6 +435,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
         for (int iz = 0; iz < 3; ++iz)
 #pragma unroll
           for (int iy = 0; iy < 3; ++iy) o[iz][iy] += cB[qz][iz] * ua[iy] + cD[qz][iz] * ub[iy];
+      }
+      if (part == 1) {
+#pragma unroll
+        for (int iz = 0; iz < 3; ++iz)
+#pragma unroll
+          for (int iy = 0; iy < 3; ++iy) o[iz][iy] = -o[iz][iy];
       }
       float* out = S + oTZ + cp * 27 + ix;
 #pragma unroll
@@ -462,7 +457,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
 #pragma unroll
       for (int comp = 0; comp < 4; ++comp) {
         float sacc = S[oTZ + (comp * 2) * 27 + t];
-        if (vertex) {
+        if (MODE == MODE_OPERATOR && vertex) {
           // PI[b][t] != 0 only for the 8 nodes b with b_k in {t_k, 1} (weight 1/2 per mid index)
           const float* gp = S + oTZ + (comp * 2 + 1) * 27;
 #pragma unroll

@@ -30,6 +30,7 @@
 // LBO = 128 B between K-adjacent core matrices, SBO between 8-row groups.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cstdlib>
 #include <type_traits>
 #include "common.cuh"
 
@@ -80,7 +81,13 @@ struct TcArgs {
   const float4* rg;           // r
   const float* geom;          // [n_rows][n_geo]
   int npp, n_geo;
+  long long* trace;  // debug timeline of CTA 0 (env DNNMG_MLP_TRACE=file), else NULL
 };
+// timeline probe (tools/mlp_trace.py): one clock64() sample per slot, CTA 0 only
+#define TC_TRACE(slot)                                                              \
+  do {                                                                              \
+    if (A.trace && blockIdx.x == 0 && (slot) < 8192) A.trace[(slot)] = clock64();   \
+  } while (0)
 
 // ---- PTX helpers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -400,7 +407,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           for (int c = 0; c < nk; ++c, ++witem, ++aitem) {
             const int sw = witem % C::NW, sa = aitem % C::NA;
             mbar_wait(smem_u32(&w_full[sw]), (witem / C::NW) & 1);
+            TC_TRACE(4 * aitem);
             mbar_wait(smem_u32(&a_full[sa]), (aitem / C::NA) & 1);
+            TC_TRACE(4 * aitem + 1);
             tc_fence_after();
             const uint32_t wb = smem_u32(wring + sw * WST);
             const uint32_t ab = smem_u32(aring + sa * AST);
@@ -419,8 +428,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
             }
             tc_commit(smem_u32(&w_empty[sw]));
             tc_commit(smem_u32(&a_empty[sa]));
+            TC_TRACE(4 * aitem + 2);
           }
           tc_commit(smem_u32(&acc_full[buf]));
+          TC_TRACE(6400 + j);
         }
       }
     }
@@ -441,6 +452,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
+      if (warp == 0 && lane == 0) TC_TRACE(4 * aitem + 3);
       ++aitem;
       (void)c;
     };
@@ -535,7 +547,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         for (int e = 0; e < HC; ++e) h[c][e] = 0.f;
       for (int g = 0; g < A.depth; ++g) {
         const int buf = j & 1;
+        if (warp == 0 && lane == 0) TC_TRACE(6656 + j);
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
+        if (warp == 0 && lane == 0) TC_TRACE(6144 + j);
         tc_fence_after();
         const float* sc = p_scale + g * kTcH;
         const float* sh = p_shift + g * kTcH;
@@ -565,11 +579,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         ++j;
       }
       // the skip state is dead now: prefetch the next tile's input under the head GEMM
+      if (warp == 0 && lane == 0) TC_TRACE(6912 + (int)((tile - blockIdx.x) / gridDim.x) * 4);
       load_x(tile + gridDim.x);
+      if (warp == 0 && lane == 0) TC_TRACE(6913 + (int)((tile - blockIdx.x) / gridDim.x) * 4);
       // head: Y = h W_depth
       {
         const int buf = j & 1;
+        if (warp == 0 && lane == 0) TC_TRACE(6656 + j);
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
+        if (warp == 0 && lane == 0) TC_TRACE(6144 + j);
         tc_fence_after();
         if (A.y_mode == 0) {
           for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
@@ -614,6 +632,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
+        if (warp == 0 && lane == 0) TC_TRACE(6914 + (int)((tile - blockIdx.x) / gridDim.x) * 4);
         ++j;
       }
     }
@@ -763,6 +782,12 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.npp = g ? g->npp : 0;
   A.n_geo = g ? g->n_geo : 0;
   A.Y = Y;
+  A.trace = nullptr;
+  static const char* trace_file = getenv("DNNMG_MLP_TRACE");
+  if (trace_file) {
+    cudaMalloc(&A.trace, 8192 * sizeof(long long));
+    cudaMemsetAsync(A.trace, 0, 8192 * sizeof(long long), s);
+  }
   A.n_rows = n_rows;
   A.n_in = m->n_in;
   A.n_out = m->n_out;
@@ -803,6 +828,16 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
     mlp_tc_kernel<MODE, false><<<grid, kTcThreads, smem, s>>>(A);
   }
   DNNMG_CHECK_LAUNCH("mlp_tc_kernel");
+  if (A.trace) {  // debug only: synchronous copy-out of CTA 0's timeline
+    static long long host[8192];
+    cudaMemcpyAsync(host, A.trace, sizeof(host), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(A.trace);
+    if (FILE* f = fopen(trace_file, "wb")) {
+      fwrite(host, sizeof(host), 1, f);
+      fclose(f);
+    }
+  }
   return DNNMG_OK;
 }
 

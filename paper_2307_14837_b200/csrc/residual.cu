@@ -92,10 +92,18 @@ struct ResidualArgs {
   const float* alpha_in;
   const float* delta_in;
   float nu, k, alpha0, delta0;
+  float ik;  // 1/k
   int convection;
   int mode;
   float4* elem;
 };
+
+// reciprocal: MUFU rcp + one Newton step (|rel. err| ~1 ulp; no IEEE-division slow path)
+__device__ __forceinline__ float frcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(fmaf(-x, r, 1.0f), r, r);
+}
 
 // PI[b][v] for local node b (lattice ib) and vertex lattice iv in {0,2}^3 (elements.py:96-118)
 __host__ __device__ constexpr float pi_weight(int b, int v) {
@@ -170,7 +178,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
   for (int i = 0; i < 3; ++i)
     conv[i] = A.convection ? v[0] * gv[i][0] + v[1] * gv[i][1] + v[2] * gv[i][2] : 0.f;
 #define CFW(arr) CF[(arr) * kCFS + q]
-  const float ik = 1.0f / A.k;
+  const float ik = A.ik;
   if constexpr (MODE == MODE_OPERATOR) {
     const float p = F[3][0];
     // Q1 (pi) fields: trilinear in the vertex values, at this Gauss point
@@ -306,9 +314,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
       dT = A.delta_in[c];
     } else {  // stab at x (assembly.py:55-59, 169-178)
       const float h = hT;
-      const float den = A.nu / (h * h) + vmag / h + 1.0f / A.k;
-      aT = A.alpha0 / den;
-      dT = A.delta0 / den;
+      const float ih = frcp(h);
+      const float rden = frcp(fmaf(A.nu * ih, ih, fmaf(vmag, ih, A.ik)));
+      aT = A.alpha0 * rden;
+      dT = A.delta0 * rden;
     }
     __syncwarp();
     // ---------------- forward x: line (f, iz, iy) -> sx[f][kind][iz][qx][iy] ----------------
@@ -427,14 +436,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(Residua
           t2 = fmaf(bx[1], l3.y, t2); t2 = fmaf(bx[2], l3.z, t2); t2 = fmaf(bx[3], l3.w, t2);
 #pragma unroll
           for (int iy = 0; iy < 3; ++iy) {
-            ua[iy] += cB[qy][iy] * t0 + cD[qy][iy] * t1;
-            ub[iy] += cB[qy][iy] * t2;
+            ua[iy] = fmaf(cB[qy][iy], t0, fmaf(cD[qy][iy], t1, ua[iy]));
+            ub[iy] = fmaf(cB[qy][iy], t2, ub[iy]);
           }
         }
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz)
 #pragma unroll
-          for (int iy = 0; iy < 3; ++iy) o[iz][iy] += cB[qz][iz] * ua[iy] + cD[qz][iz] * ub[iy];
+          for (int iy = 0; iy < 3; ++iy)
+            o[iz][iy] = fmaf(cB[qz][iz], ua[iy], fmaf(cD[qz][iz], ub[iy], o[iz][iy]));
       }
       if (part == 1) {
 #pragma unroll
@@ -520,9 +530,10 @@ __global__ void __launch_bounds__(256) stab_kernel(int n_cells, const int32_t* _
       m = fmaxf(m, sqrtf(v.y * v.y + v.z * v.z + v.w * v.w));
     }
     const float h = h_T[c];
-    const float den = nu / (h * h) + m / h + 1.0f / k;
-    aT[c] = alpha0 / den;
-    dT[c] = delta0 / den;
+    const float ih = frcp(h);
+    const float rden = frcp(fmaf(nu * ih, ih, fmaf(m, ih, 1.0f / k)));
+    aT[c] = alpha0 * rden;
+    dT[c] = delta0 * rden;
   }
 }
 
@@ -547,6 +558,7 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
   A.delta_in = dT;
   A.nu = ph->nu;
   A.k = ph->k;
+  A.ik = 1.0f / ph->k;
   A.alpha0 = ph->alpha0;
   A.delta0 = ph->delta0;
   A.convection = ph->convection;

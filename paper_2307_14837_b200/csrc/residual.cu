@@ -63,23 +63,25 @@ __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[
 // evaluated per Gauss point directly from those (elements.py:96-118).
 constexpr int kNF = 7;
 constexpr int oU = 0;                  // u[f][27]
-constexpr int oSX = 192;               // sx[f][2][9][4]          | backward tx[8][3][16][3]
+constexpr int oSY = 192;               // sy[f][kind*3+iz][16 yx]            | backward out tz
+constexpr int oSX = oSY + kNF * 144;   // sx[f][2][9][4] (dead after forward y) | cf
 constexpr int kSXF = 116;             // sx field stride: [kind][iz (stride 20)][qx][iy, pad]
-constexpr int oSY = oSX + kNF * kSXF;  // sy[f][kind*3+iz][16 yx]
-constexpr int oCF = oSX + kNF * (kSXF + 144);  // cf[25][kCFS]: A[4], B[4][3], P[3][3]
+constexpr int oCF = oSX;               // cf[25][kCFS]: A[4], B[4][3], P[3][3] (written while
+                                       // sy is read, so it may only overlap sx)
 constexpr int kNCF = 25;
 // coefficient array stride: 64 Gauss points + 4, so that array a starts in bank 4a (mod 32)
 // and the eight (comp, part) lines of the backward stage read eight different banks
 constexpr int kCFS = 68;
-constexpr int oTZ = oSX;              // tz[4][2][27] aliases the forward scratch (dead by then)
+constexpr int oTZ = oSY;              // tz[4][2][27] aliases sy (dead after the pointwise phase)
 constexpr int kCellFloats = (oCF + kNCF * kCFS + 3) / 4 * 4;
-static_assert(oTZ + 4 * 2 * 27 <= oCF, "tz must fit in the forward scratch");
+static_assert(oTZ + 4 * 2 * 27 <= oSX, "tz must fit in sy");
+static_assert(kNCF * kCFS >= kNF * kSXF, "sx must fit under cf");
 static_assert(oSX % 4 == 0 && oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
 constexpr int CB = 4;        // B[c][k]   reference-gradient test
 constexpr int CP = 16;       // P[i][k] = delta*w*g_i (J^-1 pi v)_k: LPS Gpi test, comps 1..3
-constexpr int kWarpsPerBlock = 5;
+constexpr int kWarpsPerBlock = 4;
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
@@ -272,7 +274,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 3) element_kernel(ResidualArgs A) {
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(ResidualArgs A) {
   extern __shared__ __align__(16) float smem[];
   const int wib = threadIdx.x >> 5;
   const int t = threadIdx.x & 31;

@@ -49,10 +49,10 @@ template <> struct TcCfg<DNNMG_PREC_BF16> {
   static constexpr int ESZ = 2, PARTS = 1, NW = 6, NA = 4, KSTEP = 16, KC = 32;
 };
 template <> struct TcCfg<DNNMG_PREC_TF32X3> {
-  static constexpr int ESZ = 4, PARTS = 2, NW = 4, NA = 4, KSTEP = 8, KC = 16;
+  static constexpr int ESZ = 4, PARTS = 2, NW = 3, NA = 4, KSTEP = 8, KC = 16;
 };
 template <> struct TcCfg<DNNMG_PREC_F16X3> {
-  static constexpr int ESZ = 2, PARTS = 2, NW = 4, NA = 4, KSTEP = 16, KC = 32;
+  static constexpr int ESZ = 2, PARTS = 2, NW = 3, NA = 4, KSTEP = 16, KC = 32;
 };
 static int kc_of(int precision) { return precision == DNNMG_PREC_TF32X3 ? 16 : 32; }
 // packed weight image: header (per-GEMM output unscale 2^-s and shift s), then the chunks
@@ -68,7 +68,7 @@ struct TcArgs {
   int64_t n_rows;
   int n_in, n_out, depth, act;
   int K0p, Nhead;
-  int y_mode;  // 0: direct stores, 1: staged in the A ring, 2: staged in a dedicated buffer
+  int y_mode;  // 0: direct stores, 2: staged in a dedicated shared-memory buffer
   const uint8_t* packed;
   int64_t goff[DNNMG_MAX_LAYERS];
   const float* scale;
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     p_shift[i] = A.shift[i];
   }
   const float y_unscale = hdr->unscale[A.depth];
-  float* y_stage = A.y_mode == 1 ? reinterpret_cast<float*>(aring) : p_rstd + kTcH;
+  float* y_stage = p_rstd + kTcH;
   for (int i = threadIdx.x; i < kTcH; i += blockDim.x) {
     p_mean[i] = i < A.n_in ? A.in_mean[i] : 0.f;
     p_rstd[i] = i < A.n_in ? 1.0f / A.in_std[i] : 0.f;
@@ -521,12 +521,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       }
       }
     };
-    load_x(blockIdx.x);
-
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int64_t row = tile * kTcM + row_in_tile;
-      const bool live = row < A.n_rows;
-      // layer-0 operand: normalised input rows (net.py:131), from the prefetched registers
+    // layer-0 operand: normalised input rows (net.py:131), from the prefetched registers
+    auto produce_layer0 = [&]() {
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
         if (c < nck0) {
@@ -539,6 +535,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           produce_chunk(c, v);
         }
       }
+    };
+    load_x(blockIdx.x);
+    produce_layer0();
+
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t row = tile * kTcM + row_in_tile;
+      const bool live = row < A.n_rows;
       // hidden layers: h = act(BN(z)) + h with h = 0 entering layer 0 (net.py:151: no skip
       // for layer 0); one epilogue body keeps the unrolled code (and I-cache footprint) small
 #pragma unroll
@@ -582,6 +585,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       if (warp == 0 && lane == 0) TC_TRACE(6912 + (int)((tile - blockIdx.x) / gridDim.x) * 4);
       load_x(tile + gridDim.x);
       if (warp == 0 && lane == 0) TC_TRACE(6913 + (int)((tile - blockIdx.x) / gridDim.x) * 4);
+      // the next tile's layer-0 operand goes into the ring right behind this tile's head
+      // chunks: the MMA warp runs it while this tile's head epilogue is in progress
+      if (tile + gridDim.x < n_tiles) produce_layer0();
       // head: Y = h W_depth
       {
         const int buf = j & 1;
@@ -602,8 +608,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
             }
           }
         } else {
-        // stage the 128 x n_out tile in SMEM (the A ring is idle here: every head
-        // chunk has been consumed and the next tile's chunks are not produced yet)
+        // stage the 128 x n_out tile in the dedicated SMEM buffer (the A ring already
+        // carries the next tile's layer-0 chunks), then one coalesced block copy
         float* ys = y_stage;
         for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
           float v[16];
@@ -807,9 +813,7 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 4) + 16 +
                 sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
   const size_t ybytes = (size_t)kTcM * m->n_out * 4;
-  if ((size_t)C::NA * AST >= ybytes) {
-    A.y_mode = 1;
-  } else if (smem + ybytes <= 220 * 1024) {
+  if (smem + ybytes <= 225 * 1024) {
     A.y_mode = 2;
     smem += ybytes;
   } else {

@@ -321,18 +321,44 @@ def run_slabs(args, rank, world, local):
     tdist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(args.steps):
-        slab.run(*pairs[i % S], ex)
-    e1.record()
-    tdist.barrier()
-    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    with sampler:
+        e0.record()
+        for i in range(args.steps):
+            slab.run(*pairs[i % S], ex)
+        e1.record()
+        tdist.barrier()
+        torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     n_p = slab.part.n_patches
     tot = torch.tensor([n_p], dtype=torch.float64, device="cuda")
     tdist.all_reduce(tot)
+    # e2e: the same distributed steps with every rank's x_L / b_prev copied from pinned host
+    # memory and its x_corr copied back inside each step
+    e2e = None
+    if not args.no_e2e:
+        hx = [p[0].cpu().pin_memory() for p in pairs]
+        hb = [p[1].cpu().pin_memory() for p in pairs]
+        hout = torch.empty(slab.step.x_corr.numel(), dtype=torch.float32).pin_memory()
+        dx, db = torch.empty_like(pairs[0][0]), torch.empty_like(pairs[0][1])
+        tdist.barrier()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record()
+        for i in range(args.steps):
+            dx.copy_(hx[i % S], non_blocking=True)
+            db.copy_(hb[i % S], non_blocking=True)
+            hout.copy_(slab.run(dx, db, ex), non_blocking=True)
+        h1.record()
+        tdist.barrier()
+        torch.cuda.synchronize()
+        te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+        e2e = {"value": float(tot.item()) * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(world * (dx.numel() + db.numel()) * 4),
+               "d2h_bytes_per_step": int(world * hout.numel() * 4)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": float(tot.item()) * args.steps / (ms / 1e3), "unit": UNIT,
@@ -341,8 +367,11 @@ def run_slabs(args, rank, world, local):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "patches_per_rank": n_p, "J": cfg["J"],
                        "precision": precision, "parallelism": f"x-slab decomposition x{world}, "
-                       "NCCL P2P halo exchange (2 per step)"},
+                       "NCCL P2P halo exchange (2 per step)",
+                       "l2": "inputs > L2 (2 cycled input pairs per rank, every kernel streams "
+                             ">L2-sized arrays)"},
             "gpu_launches": int((slab.step.launches + 2 * len(slab.idx) + 2) * args.steps),
+            "e2e": e2e, "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
     tdist.destroy_process_group()

@@ -64,19 +64,17 @@ __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[
 constexpr int kNF = 7;
 constexpr int oU = 0;                  // u[f][27]
 constexpr int oSY = 192;               // sy[f][kind*3+iz][16 yx]            | backward out tz
-constexpr int oSX = oSY + kNF * 144;   // sx[f][2][9][4] (dead after forward y) | cf
-constexpr int kSXF = 116;             // sx field stride: [kind][iz (stride 20)][qx][iy, pad]
-constexpr int oCF = oSX;               // cf[25][kCFS]: A[4], B[4][3], P[3][3] (written while
-                                       // sy is read, so it may only overlap sx)
+constexpr int kSYF = 148;              // sy field stride (= 20 mod 32: the (f, qx) lanes of the
+                                       // forward x-y stage store to distinct banks)
+constexpr int oCF = oSY + kNF * kSYF;  // cf[25][kCFS]: A[4], B[4][3], P[3][3]
 constexpr int kNCF = 25;
 // coefficient array stride: 64 Gauss points + 4, so that array a starts in bank 4a (mod 32)
 // and the eight (comp, part) lines of the backward stage read eight different banks
 constexpr int kCFS = 68;
 constexpr int oTZ = oSY;              // tz[4][2][27] aliases sy (dead after the pointwise phase)
 constexpr int kCellFloats = (oCF + kNCF * kCFS + 3) / 4 * 4;
-static_assert(oTZ + 4 * 2 * 27 <= oSX, "tz must fit in sy");
-static_assert(kNCF * kCFS >= kNF * kSXF, "sx must fit under cf");
-static_assert(oSX % 4 == 0 && oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
+static_assert(oTZ + 4 * 2 * 27 <= oCF, "tz must fit in sy");
+static_assert(oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
 constexpr int CB = 4;        // B[c][k]   reference-gradient test
@@ -322,44 +320,35 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       dT = A.delta0 * rden;
     }
     __syncwarp();
-    // ---------------- forward x: line (f, iz, iy) -> sx[f][kind][iz][qx][iy] ----------------
+    // ---------------- forward x and y in registers: lane (f, qx) ----------------
+    // x stage for this qx on the 9 (iz, iy) lines of field f, then the y stage for all four
+    // qy -> sy[f][kind*3 + iz][qy*4 + qx]; kind 0 = B_x B_y, 1 = B_x D_y, 2 = D_x B_y
+    if (t < 4 * kNF) {
+      const int f = t >> 2, qx = t & 3;
+      const float* u = S + oU + f * 27;
+      const float bx0 = cB[qx][0], bx1 = cB[qx][1], bx2 = cB[qx][2];
+      const float dx0 = cD[qx][0], dx1 = cD[qx][1], dx2 = cD[qx][2];
+      float aB[3][3], aD[3][3];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int l = t + 32 * r;
-      if (l < kNF * 9) {
-        const int f = l / 9, izy = l - 9 * (l / 9), iz = izy / 3, iy = izy - 3 * (izy / 3);
-        const float* u = S + oU + f * 27 + izy * 3;
-        const float u0 = u[0], u1 = u[1], u2 = u[2];
-        float* o = S + oSX + f * kSXF + iz * 20 + iy;
+      for (int iz = 0; iz < 3; ++iz)
 #pragma unroll
-        for (int lq = 0; lq < 4; ++lq) {
-          o[lq * 4] = cB[lq][0] * u0 + cB[lq][1] * u1 + cB[lq][2] * u2;
-          o[60 + lq * 4] = cD[lq][0] * u0 + cD[lq][1] * u1 + cD[lq][2] * u2;
+        for (int iy = 0; iy < 3; ++iy) {
+          const float u0 = u[9 * iz + 3 * iy], u1 = u[9 * iz + 3 * iy + 1], u2 = u[9 * iz + 3 * iy + 2];
+          aB[iz][iy] = fmaf(bx2, u2, fmaf(bx1, u1, bx0 * u0));
+          aD[iz][iy] = fmaf(dx2, u2, fmaf(dx1, u1, dx0 * u0));
         }
-      }
-    }
-    __syncwarp();
-    // ---------------- forward y: line (f, qy, qx) -> sy[f][qy*4+qx][kind*3+iz] ----------------
+      float* dst = S + oSY + f * kSYF + qx;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int l = t + 32 * r;
-      if (l < kNF * 16) {
-        const int f = l >> 4, yx = l & 15, ly = yx >> 2, lx = yx & 3;
-        const float* s0 = S + oSX + f * kSXF + lx * 4;  // [kind*60 + iz*20] -> float4 over iy
-        const float by0 = cB[ly][0], by1 = cB[ly][1], by2 = cB[ly][2];
-        const float dy0 = cD[ly][0], dy1 = cD[ly][1], dy2 = cD[ly][2];
-        float o[9];
+      for (int qy = 0; qy < 4; ++qy) {
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz) {
-          const float4 a = *reinterpret_cast<const float4*>(s0 + iz * 20);
-          const float4 b = *reinterpret_cast<const float4*>(s0 + 60 + iz * 20);
-          o[0 + iz] = by0 * a.x + by1 * a.y + by2 * a.z;
-          o[3 + iz] = dy0 * a.x + dy1 * a.y + dy2 * a.z;
-          o[6 + iz] = by0 * b.x + by1 * b.y + by2 * b.z;
+          dst[(0 + iz) * 16 + 4 * qy] =
+              fmaf(cB[qy][2], aB[iz][2], fmaf(cB[qy][1], aB[iz][1], cB[qy][0] * aB[iz][0]));
+          dst[(3 + iz) * 16 + 4 * qy] =
+              fmaf(cD[qy][2], aB[iz][2], fmaf(cD[qy][1], aB[iz][1], cD[qy][0] * aB[iz][0]));
+          dst[(6 + iz) * 16 + 4 * qy] =
+              fmaf(cB[qy][2], aD[iz][2], fmaf(cB[qy][1], aD[iz][1], cB[qy][0] * aD[iz][0]));
         }
-        float* dst = S + oSY + f * 144 + yx;
-#pragma unroll
-        for (int m = 0; m < 9; ++m) dst[m * 16] = o[m];
       }
     }
     __syncwarp();
@@ -369,7 +358,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       float F[kNF][4], G[kNF][4];
 #pragma unroll
       for (int f = 0; f < kNF; ++f) {
-        const float* src = S + oSY + f * 144 + yx;  // [(kind*3 + iz)*16]
+        const float* src = S + oSY + f * kSYF + yx;  // [(kind*3 + iz)*16]
         const float vv0 = src[0], vv1 = src[16], vv2 = src[32];
         const float vd0 = src[48], vd1 = src[64], vd2 = src[80];
         const float dv0 = src[96], dv1 = src[112], dv2 = src[128];

@@ -381,73 +381,91 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       pointwise<MODE>(A, S, S + oCF, t + 32, G, aT, dT);
     }
     __syncwarp();
-    // ---------------- backward x, y, z in registers: lane (cp, ix), cp = (comp, part) ----------------
-    // tz[cp][iz][iy][ix] = sum_q test(q; ix, iy, iz) . coefficients(cp, q): the x contraction
-    // of a (qy, qz) line feeds the y partial sums of that qz, which feed the z sums.  Part 0
-    // is the direct test (A N + B_k dN/dxi_k); part 1 the LPS test through PI^T:
-    // comp 0: -B_0k, comps 1..3: -dg_i (J^-1 pi v)_k (elements.py:96-118, assembly.py:120-140).
-    // (the RHS form has no LPS part: its part-1 lanes and the PI^T fold are skipped)
-    if (t < 24 && (MODE == MODE_OPERATOR || (t / 3) % 2 == 0)) {
-      const int cp = t / 3, ix = t - 3 * (t / 3);
+    // ---------------- backward x, y, z in registers: lane (cp, qz), cp = (comp, part) ----------------
+    // tz[cp][iz][iy][ix] = sum_q test(q; ix, iy, iz) . coefficients(cp, q).  Each of the 32
+    // lanes contracts the four (qy) lines of one qz plane for all three ix (x stage), then qy
+    // (y stage), then adds its plane's share of the qz sum; the four qz partials of a cp are
+    // combined by a two-step shuffle reduce-scatter.  Part 0 is the direct test
+    // (A N + B_k dN/dxi_k); part 1 the LPS test through PI^T: comp 0: -B_0k,
+    // comps 1..3: -dg_i (J^-1 pi v)_k (elements.py:96-118, assembly.py:120-140).  (The RHS
+    // form has no LPS part: its part-1 lanes compute unused values.)
+    {
+      const int cp = t >> 2, qz = t & 3;
       const int comp = cp >> 1, part = cp & 1;
       // part 0: A_c, B_c0..2; part 1: comp 0 -> B_00..02, comps 1..3 -> P_(c-1)0..2; part 1 has
-      // no value test (a_on = 0) and enters with a minus sign
-      const float* c0 = S + oCF + (CA + comp) * kCFS;
-      const float* c1 =
-          S + oCF + (part == 0 || comp == 0 ? CB + 3 * comp : CP + 3 * (comp - 1)) * kCFS;
+      // no value test and enters with a minus sign
+      const float* c0 = S + oCF + (CA + comp) * kCFS + 16 * qz;
+      const float* c1 = S + oCF +
+                        (part == 0 || comp == 0 ? CB + 3 * comp : CP + 3 * (comp - 1)) * kCFS +
+                        16 * qz;
       const float* c2 = c1 + kCFS;
       const float* c3 = c1 + 2 * kCFS;
-      float bxa[4], bx[4], dx[4];
+      float ua[3][3], ub[3][3];  // [iy][ix]
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        bx[qq] = ix == 0 ? cB[qq][0] : ix == 1 ? cB[qq][1] : cB[qq][2];
-        dx[qq] = ix == 0 ? cD[qq][0] : ix == 1 ? cD[qq][1] : cD[qq][2];
-        bxa[qq] = part == 0 ? bx[qq] : 0.f;
-      }
-      float o[3][3];
+      for (int iy = 0; iy < 3; ++iy)
 #pragma unroll
-      for (int iz = 0; iz < 3; ++iz)
+        for (int ix = 0; ix < 3; ++ix) ua[iy][ix] = ub[iy][ix] = 0.f;
 #pragma unroll
-        for (int iy = 0; iy < 3; ++iy) o[iz][iy] = 0.f;
-#pragma unroll 1
-      for (int qz = 0; qz < 4; ++qz) {  // rolled: keeps the kernel inside the instruction cache
-        float ua[3] = {0.f, 0.f, 0.f}, ub[3] = {0.f, 0.f, 0.f};
+      for (int qy = 0; qy < 4; ++qy) {
+        float4 l0 = *reinterpret_cast<const float4*>(c0 + 4 * qy);
+        const float4 l1 = *reinterpret_cast<const float4*>(c1 + 4 * qy);
+        const float4 l2 = *reinterpret_cast<const float4*>(c2 + 4 * qy);
+        const float4 l3 = *reinterpret_cast<const float4*>(c3 + 4 * qy);
+        if (part) l0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float L0[4] = {l0.x, l0.y, l0.z, l0.w}, L1[4] = {l1.x, l1.y, l1.z, l1.w};
+        const float L2[4] = {l2.x, l2.y, l2.z, l2.w}, L3[4] = {l3.x, l3.y, l3.z, l3.w};
 #pragma unroll
-        for (int qy = 0; qy < 4; ++qy) {
-          const int zy = (qy + 4 * qz) * 4;
-          const float4 l0 = *reinterpret_cast<const float4*>(c0 + zy);
-          const float4 l1 = *reinterpret_cast<const float4*>(c1 + zy);
-          const float4 l2 = *reinterpret_cast<const float4*>(c2 + zy);
-          const float4 l3 = *reinterpret_cast<const float4*>(c3 + zy);
-          float t0 = bxa[0] * l0.x, t1 = bx[0] * l2.x, t2 = bx[0] * l3.x;
-          t0 = fmaf(bxa[1], l0.y, t0); t0 = fmaf(bxa[2], l0.z, t0); t0 = fmaf(bxa[3], l0.w, t0);
-          t0 = fmaf(dx[0], l1.x, t0); t0 = fmaf(dx[1], l1.y, t0);
-          t0 = fmaf(dx[2], l1.z, t0); t0 = fmaf(dx[3], l1.w, t0);
-          t1 = fmaf(bx[1], l2.y, t1); t1 = fmaf(bx[2], l2.z, t1); t1 = fmaf(bx[3], l2.w, t1);
-          t2 = fmaf(bx[1], l3.y, t2); t2 = fmaf(bx[2], l3.z, t2); t2 = fmaf(bx[3], l3.w, t2);
+        for (int ix = 0; ix < 3; ++ix) {
+          float t0 = cB[0][ix] * L0[0], t1 = cB[0][ix] * L2[0], t2 = cB[0][ix] * L3[0];
+#pragma unroll
+          for (int qx = 1; qx < 4; ++qx) t0 = fmaf(cB[qx][ix], L0[qx], t0);
+#pragma unroll
+          for (int qx = 0; qx < 4; ++qx) t0 = fmaf(cD[qx][ix], L1[qx], t0);
+#pragma unroll
+          for (int qx = 1; qx < 4; ++qx) {
+            t1 = fmaf(cB[qx][ix], L2[qx], t1);
+            t2 = fmaf(cB[qx][ix], L3[qx], t2);
+          }
 #pragma unroll
           for (int iy = 0; iy < 3; ++iy) {
-            ua[iy] = fmaf(cB[qy][iy], t0, fmaf(cD[qy][iy], t1, ua[iy]));
-            ub[iy] = fmaf(cB[qy][iy], t2, ub[iy]);
+            ua[iy][ix] = fmaf(cB[qy][iy], t0, fmaf(cD[qy][iy], t1, ua[iy][ix]));
+            ub[iy][ix] = fmaf(cB[qy][iy], t2, ub[iy][ix]);
           }
         }
-#pragma unroll
-        for (int iz = 0; iz < 3; ++iz)
-#pragma unroll
-          for (int iy = 0; iy < 3; ++iy)
-            o[iz][iy] = fmaf(cB[qz][iz], ua[iy], fmaf(cD[qz][iz], ub[iy], o[iz][iy]));
       }
-      if (part == 1) {
-#pragma unroll
-        for (int iz = 0; iz < 3; ++iz)
-#pragma unroll
-          for (int iy = 0; iy < 3; ++iy) o[iz][iy] = -o[iz][iy];
-      }
-      float* out = S + oTZ + cp * 27 + ix;
+      // this plane's z contribution to all 27 outputs, index b = 9 iz + 3 iy + ix
+      const float bz0 = cB[qz][0], bz1 = cB[qz][1], bz2 = cB[qz][2];
+      const float dz0 = cD[qz][0], dz1 = cD[qz][1], dz2 = cD[qz][2];
+      const float bz[3] = {bz0, bz1, bz2}, dz[3] = {dz0, dz1, dz2};
+      float o[28];
 #pragma unroll
       for (int iz = 0; iz < 3; ++iz)
 #pragma unroll
-        for (int iy = 0; iy < 3; ++iy) out[9 * iz + 3 * iy] = o[iz][iy];
+        for (int iy = 0; iy < 3; ++iy)
+#pragma unroll
+          for (int ix = 0; ix < 3; ++ix)
+            o[9 * iz + 3 * iy + ix] = fmaf(bz[iz], ua[iy][ix], dz[iz] * ub[iy][ix]);
+      o[27] = 0.f;
+      // reduce-scatter over the four qz lanes of this cp: lane bit 1 picks the half [0,14) or
+      // [14,28), lane bit 0 the quarter [0,7) or [7,14) of that half
+      const bool hi1 = (t & 2) != 0, hi0 = (t & 1) != 0;
+      float k14[14];
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+        const float send = hi1 ? o[k] : o[14 + k];
+        const float keep = hi1 ? o[14 + k] : o[k];
+        k14[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      const float sgn = part ? -1.f : 1.f;
+      float* out = S + oTZ + cp * 27 + (hi1 ? 14 : 0) + (hi0 ? 7 : 0);
+      const int nvalid = (hi1 && hi0) ? 6 : 7;  // 27 = 7 + 7 + 7 + 6
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        const float send = hi0 ? k14[k] : k14[7 + k];
+        const float keep = hi0 ? k14[7 + k] : k14[k];
+        const float v = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        if (k < nvalid) out[k] = sgn * v;
+      }
     }
     __syncwarp();
     // ---------------- output: direct + PI^T * (LPS part), one float4 per node ----------------

@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
 
   for (; c < A.n_cells; c += stride) {
     // ---------------- gather (prefetched one cell ahead), stab ----------------
-    float vmag = 0.f;
+    float vsq = 0.f;  // |v|^2 of this lane's node; vmax = sqrt(max |v|^2) (sqrt is monotone)
     if (t < 27) {
       S[oU + 0 * 27 + t] = float(raw.X[0] - raw.X0[0]);
       S[oU + 1 * 27 + t] = float(raw.X[1] - raw.X0[1]);
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       S[oU + 4 * 27 + t] = raw.xv.y;
       S[oU + 5 * 27 + t] = raw.xv.z;
       S[oU + 6 * 27 + t] = raw.xv.w;
-      vmag = sqrtf(raw.xv.y * raw.xv.y + raw.xv.z * raw.xv.z + raw.xv.w * raw.xv.w);
+      vsq = raw.xv.y * raw.xv.y + raw.xv.z * raw.xv.z + raw.xv.w * raw.xv.w;
     }
     const float hT = raw.hT;
     if (c + stride < A.n_cells) {  // issue the loads of the next cell (consumed next iteration)
@@ -306,8 +306,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       if (c + 2 * stride < A.n_cells && t < 27)
         idx_next = __ldg(A.cell_nodes + (int64_t)(c + 2 * stride) * 27 + t);
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) vmag = fmaxf(vmag, __shfl_xor_sync(0xffffffffu, vmag, off));
+    // non-negative floats order like their bit patterns: one warp-wide integer max
+    const float vmag = sqrtf(__uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(vsq))));
     float aT, dT;
     if (A.alpha_in) {
       aT = A.alpha_in[c];
@@ -471,22 +471,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     // ---------------- output: direct + PI^T * (LPS part), one float4 per node ----------------
     if (t < 27) {
       float e[4];
-      const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
-      const bool vertex = it0 != 1 && it1 != 1 && it2 != 1;
 #pragma unroll
-      for (int comp = 0; comp < 4; ++comp) {
-        float sacc = S[oTZ + (comp * 2) * 27 + t];
-        if (MODE == MODE_OPERATOR && vertex) {
-          // PI[b][t] != 0 only for the 8 nodes b with b_k in {t_k, 1} (weight 1/2 per mid index)
+      for (int comp = 0; comp < 4; ++comp) e[comp] = S[oTZ + (comp * 2) * 27 + t];
+      const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
+      if (MODE == MODE_OPERATOR && it0 != 1 && it1 != 1 && it2 != 1) {
+        // vertex: PI[b][t] != 0 only for the 8 nodes b with b_k in {t_k, 1} (weight 1/2
+        // per mid index)
+#pragma unroll
+        for (int comp = 0; comp < 4; ++comp) {
           const float* gp = S + oTZ + (comp * 2 + 1) * 27;
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
             const int b0 = (m & 1) ? 1 : it0, b1 = (m & 2) ? 1 : it1, b2 = (m & 4) ? 1 : it2;
             const float wgt = ((m & 1) ? 0.5f : 1.f) * ((m & 2) ? 0.5f : 1.f) * ((m & 4) ? 0.5f : 1.f);
-            sacc = fmaf(wgt, gp[b0 + 3 * b1 + 9 * b2], sacc);
+            e[comp] = fmaf(wgt, gp[b0 + 3 * b1 + 9 * b2], e[comp]);
           }
         }
-        e[comp] = sacc;
       }
       A.elem[(int64_t)c * 27 + t] = make_float4(e[0], e[1], e[2], e[3]);
     }

@@ -220,18 +220,12 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
       float pv[3];
 #pragma unroll
       for (int i = 0; i < 3; ++i) pv[i] = PQ[1 + i][0];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        float sacc = 0.f;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const float gpv = PQ[1 + i][1] * Ji[0][j] + PQ[1 + i][2] * Ji[1][j] + PQ[1 + i][3] * Ji[2][j];
-          sacc = fmaf(pv[j], gpv, sacc);
-        }
-        g[i] = conv[i] - sacc;
-      }
+      // pvr = J^-1 pi v; (pi v . grad) pi v_i = sum_m d(pi v_i)/dxi_m pvr_m
 #pragma unroll
       for (int kk = 0; kk < 3; ++kk) pvr[kk] = Ji[kk][0] * pv[0] + Ji[kk][1] * pv[1] + Ji[kk][2] * pv[2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        g[i] = conv[i] - (PQ[1 + i][1] * pvr[0] + PQ[1 + i][2] * pvr[1] + PQ[1 + i][3] * pvr[2]);
     }
     const float div = gv[0][0] + gv[1][1] + gv[2][2];
     float E[3];

@@ -208,12 +208,11 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
       PQ[f][2] = fmaf(lz1, by[1] - by[0], by[0]);
       PQ[f][3] = b[1] - b[0];
     }
-    float gp[3], gpp[3];
+    // physical gradient of the pressure fluctuation p - pi p
+    const float dd0 = F[3][1] - PQ[0][1], dd1 = F[3][2] - PQ[0][2], dd3 = F[3][3] - PQ[0][3];
+    float gdp[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      gp[j] = F[3][1] * Ji[0][j] + F[3][2] * Ji[1][j] + F[3][3] * Ji[2][j];
-      gpp[j] = PQ[0][1] * Ji[0][j] + PQ[0][2] * Ji[1][j] + PQ[0][3] * Ji[2][j];
-    }
+    for (int j = 0; j < 3; ++j) gdp[j] = dd0 * Ji[0][j] + dd1 * Ji[1][j] + dd3 * Ji[2][j];
     const bool use_d = A.convection && dT != 0.f;
     float g[3] = {0.f, 0.f, 0.f}, pvr[3] = {0.f, 0.f, 0.f};
     if (use_d) {
@@ -230,7 +229,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
     const float div = gv[0][0] + gv[1][1] + gv[2][2];
     float E[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) E[j] = aT * w * (gp[j] - gpp[j]);
+    for (int j = 0; j < 3; ++j) E[j] = aT * w * gdp[j];
     CFW(CA + 0) = w * div;
 #pragma unroll
     for (int kk = 0; kk < 3; ++kk) CFW(CB + kk) = Ji[kk][0] * E[0] + Ji[kk][1] * E[1] + Ji[kk][2] * E[2];

@@ -523,6 +523,18 @@ def run_ours(args, rank, world, local):
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": f"{peak_kind} hbm copy"}
+    # DRAM traffic per launch of each stage from the committed ncu capture (round-1 profile)
+    try:
+        with open(os.path.join(REPO, "profiles", "r1_dram_traffic.json")) as f:
+            traffic = json.load(f)
+    except Exception:
+        traffic = {}
+    if isinstance(traffic.get(dom), (int, float)):
+        roof["traffic"] = traffic[dom]
+        roof["traffic_source"] = "profiles/r1_dram_traffic.json (ncu --set full, per launch)"
+    for nm, entry in per_kernel.items():
+        if isinstance(traffic.get(nm), (int, float)):
+            entry["dram_bytes_ncu"] = traffic[nm]
     cpu = None
     if not args.no_cpu_baseline:
         rate, n_s, t_s = cpu_oracle_rate(cfg, args.cpu_sample, 2, 1)

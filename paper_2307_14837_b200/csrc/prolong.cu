@@ -90,47 +90,126 @@ __global__ void __launch_bounds__(256) dirichlet_kernel(int n, const uint8_t* __
   }
 }
 
-// v2: one warp per parent cell C.  The fine nodes whose first-appearance parent is C
-// (owner list, CSR by C) are computed from C's 27 coarse values staged in shared
-// memory once, instead of every fine node re-gathering its coarse row.
+// v3: one warp per parent cell C, separable.  The 27 coarse values of C are staged in
+// shared memory (prefetched one cell ahead), interpolated to the 5 x 5 x 5 lattice of the
+// refined cell in three 1-D stages (x: 45 values, y: 75, z: 125; an odd lattice position
+// takes the 3-tap quarter-point stencil, an even one copies), and the fine nodes whose
+// first-appearance parent is C (owner list, CSR by C) are written from the lattice.
 constexpr int kProlongWarps = 8;
+
+__device__ __forceinline__ float4 lerp3(int p, const float4& a, const float4& b, const float4& c) {
+  // p = 1: (3/8, 3/4, -1/8); p = 3: (-1/8, 3/4, 3/8) -- dyadic, as the 1-D Q2 basis at 1/4, 3/4
+  const float w0 = p == 1 ? 0.375f : -0.125f, w2 = p == 1 ? -0.125f : 0.375f;
+  float4 r;
+  r.x = fmaf(w2, c.x, fmaf(0.75f, b.x, w0 * a.x));
+  r.y = fmaf(w2, c.y, fmaf(0.75f, b.y, w0 * a.y));
+  r.z = fmaf(w2, c.z, fmaf(0.75f, b.z, w0 * a.z));
+  r.w = fmaf(w2, c.w, fmaf(0.75f, b.w, w0 * a.w));
+  return r;
+}
 
 __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
     int n_coarse_cells, const int32_t* __restrict__ ctab, const int32_t* __restrict__ owner_ptr,
     const int32_t* __restrict__ owner_node, const uint8_t* __restrict__ owner_code,
     const float4* __restrict__ xc, float4* __restrict__ xf, const uint8_t* __restrict__ bc_code,
     const float* __restrict__ bc_values) {
-  __shared__ float4 cv[kProlongWarps][27];
+  __shared__ float4 sm[kProlongWarps][27 + 45 + 75 + 125];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int C = blockIdx.x * kProlongWarps + w; C < n_coarse_cells; C += gridDim.x * kProlongWarps) {
-    if (lane < 27) cv[w][lane] = __ldg(xc + __ldg(ctab + (int64_t)C * 27 + lane));
+  float4* cv = sm[w];        // [iz][iy][ix]
+  float4* X1 = cv + 27;      // [iz][iy][px]
+  float4* X2 = X1 + 45;      // [iz][py][px]
+  float4* X3 = X2 + 75;      // [pz][py][px]
+  const int stride = gridDim.x * kProlongWarps;
+  int C = blockIdx.x * kProlongWarps + w;
+  constexpr int kMaxOwned = 96;  // owned fine nodes per parent cell: <= 64 + faces (checked on host)
+  float4 nxt = make_float4(0.f, 0.f, 0.f, 0.f);
+  int s_nxt = 0, e_nxt = 0;
+  if (C < n_coarse_cells) {
+    if (lane < 27) nxt = __ldg(xc + __ldg(ctab + (int64_t)C * 27 + lane));
+    s_nxt = __ldg(owner_ptr + C);
+    e_nxt = __ldg(owner_ptr + C + 1);
+  }
+  for (; C < n_coarse_cells; C += stride) {
+    if (lane < 27) cv[lane] = nxt;
+    const int s = s_nxt, e = e_nxt;
+    // this cell's owned nodes, their lattice codes and Dirichlet codes: loads in flight
+    // under the interpolation stages
+    int nn[kMaxOwned / 32], cc[kMaxOwned / 32], bb[kMaxOwned / 32];
+#pragma unroll
+    for (int k = 0; k < kMaxOwned / 32; ++k) {
+      const int i = s + lane + 32 * k;
+      nn[k] = i < e ? __ldg(owner_node + i) : -1;
+      cc[k] = i < e ? __ldg(owner_code + i) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxOwned / 32; ++k) bb[k] = (bc_code && nn[k] >= 0) ? bc_code[nn[k]] : 0;
+    if (C + stride < n_coarse_cells) {
+      if (lane < 27) nxt = __ldg(xc + __ldg(ctab + (int64_t)(C + stride) * 27 + lane));
+      s_nxt = __ldg(owner_ptr + C + stride);
+      e_nxt = __ldg(owner_ptr + C + stride + 1);
+    }
     __syncwarp();
-    const int s = __ldg(owner_ptr + C), e = __ldg(owner_ptr + C + 1);
-    for (int i = s + lane; i < e; i += 32) {
+    // x stage: 45 = 9 lines x 5 positions
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int l = lane + 32 * r;
+      if (l < 45) {
+        const int line = l / 5, px = l - 5 * line;
+        const float4* c = cv + 3 * line;
+        X1[l] = (px & 1) ? lerp3(px, c[0], c[1], c[2]) : c[px >> 1];
+      }
+    }
+    __syncwarp();
+    // y stage: 75 = 3 iz x 5 py x 5 px
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int l = lane + 32 * r;
+      if (l < 75) {
+        const int iz = l / 25, py = (l / 5) % 5, px = l % 5;
+        const float4* c = X1 + 15 * iz + px;  // [iy] stride 5
+        X2[l] = (py & 1) ? lerp3(py, c[0], c[5], c[10]) : c[5 * (py >> 1)];
+      }
+    }
+    __syncwarp();
+    // z stage: 125 = 5 pz x 25
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int l = lane + 32 * r;
+      if (l < 125) {
+        const int pz = l / 25, yx = l % 25;
+        const float4* c = X2 + yx;  // [iz] stride 25
+        X3[l] = (pz & 1) ? lerp3(pz, c[0], c[25], c[50]) : c[25 * (pz >> 1)];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kMaxOwned / 32; ++k) {
+      const int n = nn[k];
+      if (n >= 0) {
+        const int oa = cc[k];
+        const int o = oa / 27, a = oa - 27 * o;
+        const int px = 2 * (o & 1) + a % 3;
+        const int py = 2 * ((o >> 1) & 1) + (a / 3) % 3;
+        const int pz = 2 * (o >> 2) + a / 9;
+        float4 acc = X3[25 * pz + 5 * py + px];
+        if (bb[k] == 1) {
+          acc.y = acc.z = acc.w = 0.f;
+        } else if (bb[k] == 2) {
+          acc.y = bc_values[3 * (int64_t)n];
+          acc.z = bc_values[3 * (int64_t)n + 1];
+          acc.w = bc_values[3 * (int64_t)n + 2];
+        }
+        xf[n] = acc;
+      }
+    }
+    for (int i = s + kMaxOwned + lane; i < e; i += 32) {  // (never taken for box meshes)
       const int n = __ldg(owner_node + i);
       const int oa = __ldg(owner_code + i);
       const int o = oa / 27, a = oa - 27 * o;
       const int px = 2 * (o & 1) + a % 3;
       const int py = 2 * ((o >> 1) & 1) + (a / 3) % 3;
       const int pz = 2 * (o >> 2) + a / 9;
-      int ix[3], iy[3], iz[3];
-      float wx[3], wy[3], wz[3];
-      const int nx = stencil_1d(px, ix, wx);
-      const int ny = stencil_1d(py, iy, wy);
-      const int nz = stencil_1d(pz, iz, wz);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int kz = 0; kz < nz; ++kz)
-        for (int ky = 0; ky < ny; ++ky) {
-          const float wyz = wy[ky] * wz[kz];
-          for (int kx = 0; kx < nx; ++kx) {
-            const float wgt = wx[kx] * wyz;
-            const float4 v = cv[w][ix[kx] + 3 * iy[ky] + 9 * iz[kz]];
-            acc.x = fmaf(wgt, v.x, acc.x);
-            acc.y = fmaf(wgt, v.y, acc.y);
-            acc.z = fmaf(wgt, v.z, acc.z);
-            acc.w = fmaf(wgt, v.w, acc.w);
-          }
-        }
+      float4 acc = X3[25 * pz + 5 * py + px];
       if (bc_code) {
         const uint8_t code = bc_code[n];
         if (code == 1) {
@@ -164,7 +243,7 @@ int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float
   }
   if (P->n_fine_nodes == 0) return DNNMG_OK;
   if (P->owner_ptr && P->owner_node && P->owner_code) {
-    const int blocks = grid_for((P->n_coarse_cells + kProlongWarps - 1) / kProlongWarps, 1, 8);
+    const int blocks = grid_for((P->n_coarse_cells + kProlongWarps - 1) / kProlongWarps, 1, 4);
     prolongate_owner_kernel<<<blocks, 32 * kProlongWarps, 0, s>>>(
         P->n_coarse_cells, P->coarse_cell_nodes, P->owner_ptr, P->owner_node, P->owner_code,
         reinterpret_cast<const float4*>(x_coarse), reinterpret_cast<float4*>(x_fine), code, vals);

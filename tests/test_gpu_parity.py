@@ -302,3 +302,27 @@ def test_host_pipeline_matches_run(precision):
     torch.cuda.synchronize()
     for o, r in zip(outs, ref):
         assert torch.equal(o, r)
+
+
+@pytest.mark.parametrize("wscale", [1e-6, 1.0, 3e3])
+def test_f16x3_weight_scaling(wscale):
+    """f16x3 keeps fp32-level accuracy for tiny and large weights: each GEMM's weights
+    are rescaled by an exact power of two at pack time (mlp_tc.cu pack_scale_kernel)
+    and the inverse is folded into the BN scale / head output."""
+    from oracle import dnnmg_oracle as orc
+    rng = np.random.default_rng(11)
+    n_in, depth, n_out, rows = 240, 3, 81, 777
+    m = net.MlpModel(net.Architecture(n_in, 256, depth, n_out), activation="tanh", seed=3)
+    dims = [n_in] + [256] * depth + [n_out]
+    m.W = [rng.uniform(-1, 1, (a, b)) * np.sqrt(6.0 / (a + b)) * wscale for a, b in zip(dims[:-1], dims[1:])]
+    # keep the pre-activations O(1): BN scale undoes the weight scale of the hidden layers
+    m.gamma = [np.full(256, 1.0 / wscale) for _ in range(depth)]
+    m.beta = [rng.normal(0, 0.1, 256) for _ in range(depth)]
+    m.running_mean = [np.zeros(256) for _ in range(depth)]
+    m.running_var = [np.ones(256) - m.bn_eps for _ in range(depth)]
+    m.eval()
+    X = rng.standard_normal((rows, n_in))
+    ref = orc.mlp_forward(orc.Mlp(m.W, "tanh", m.gamma, m.beta, m.running_mean, m.running_var,
+                                  m.input_mean, m.input_std), X)
+    Y = net.forward(m, X, precision="f16x3")
+    assert rel(Y, ref) < 1e-5, rel(Y, ref)

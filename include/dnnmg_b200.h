@@ -8,6 +8,7 @@
  *
  *   dnnmg_prolongate        space.prolongate            space.py:177-185 (+ apply_dirichlet 245-255)
  *   dnnmg_apply_dirichlet   space.apply_dirichlet       space.py:245-255
+ *   dnnmg_restrict          space.restrict_rhs          space.py:188-196 (P^T, Alg. 1 line 9)
  *   dnnmg_stab              Assembler.stab              assembly.py:169-178, 55-59
  *   dnnmg_residual          Assembler.assemble_residual assembly.py:261-267 (apply_operator 212-240)
  *   dnnmg_rhs_next          Assembler.assemble_rhs_next assembly.py:242-259
@@ -81,6 +82,18 @@ typedef struct {
   const uint8_t* owner_code;        /* [n_fine_nodes] */
 } dnnmg_prolong_t;
 
+/* Restriction level l+1 -> l of a dual (RHS) vector: b_coarse = P^T b_fine
+ * (space.py:188-196), the transpose of the K1 stencil as a coarse-node CSR whose rows
+ * list the fine nodes in ascending order with their dyadic weights.  Owner-computes on
+ * coarse nodes: deterministic, no atomics. */
+typedef struct {
+  int32_t n_coarse_nodes;
+  int32_t n_fine_nodes;
+  const int32_t* ptr;   /* [n_coarse_nodes+1] */
+  const int32_t* fine;  /* [nnz] */
+  const float* w;       /* [nnz] */
+} dnnmg_restrict_t;
+
 /* Dirichlet data of one level (space.py:245-255): bc_code[n] = 0 untouched,
  * 1 velocity := 0 (no-slip), 2 velocity := bc_values[n]. */
 typedef struct {
@@ -145,6 +158,9 @@ const char* dnnmg_last_error(void);   /* detail of the last failing call (host s
 int32_t dnnmg_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float* x_fine,
                          const dnnmg_dirichlet_t* bc /* nullable */, dnnmg_stream_t stream);
 int32_t dnnmg_apply_dirichlet(const dnnmg_dirichlet_t* bc, float* x, dnnmg_stream_t stream);
+/* restriction (next row #1, Alg. 1 line 9): b_coarse = P^T b_fine, node-major float4 */
+int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* b_fine, float* b_coarse,
+                       dnnmg_stream_t stream);
 
 /* ---- K2: stabilisation, residual, next RHS ---------------------------------- */
 int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph,

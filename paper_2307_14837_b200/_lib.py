@@ -54,6 +54,11 @@ class Mlp(ctypes.Structure):
                 ("packed", c_vp)]
 
 
+class Restrict(ctypes.Structure):
+    _fields_ = [("n_coarse_nodes", c_i32), ("n_fine_nodes", c_i32), ("ptr", c_vp), ("fine", c_vp),
+                ("w", c_vp)]
+
+
 class StepBuffers(ctypes.Structure):
     _fields_ = [("x_tilde", c_vp), ("r", c_vp), ("elem", c_vp), ("X", c_vp), ("Y", c_vp),
                 ("d", c_vp), ("x_mid", c_vp)]
@@ -65,6 +70,7 @@ EXPORTS = {
     "dnnmg_last_error": (ctypes.c_char_p, []),
     "dnnmg_prolongate": (c_i32, [ctypes.POINTER(Prolong), c_vp, c_vp, ctypes.POINTER(Dirichlet), c_vp]),
     "dnnmg_apply_dirichlet": (c_i32, [ctypes.POINTER(Dirichlet), c_vp, c_vp]),
+    "dnnmg_restrict": (c_i32, [ctypes.POINTER(Restrict), c_vp, c_vp, c_vp]),
     "dnnmg_stab": (c_i32, [ctypes.POINTER(Level), c_vp, ctypes.POINTER(Phys), c_vp, c_vp, c_vp]),
     "dnnmg_residual": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(Phys),
                                c_vp, c_vp, c_i32, c_vp]),

@@ -18,6 +18,7 @@ int32_t set_error(int32_t status, const char* fmt, ...) {
 int32_t launch_prolongate(const dnnmg_prolong_t*, const float*, float*, const dnnmg_dirichlet_t*,
                           cudaStream_t);
 int32_t launch_dirichlet(const dnnmg_dirichlet_t*, float*, cudaStream_t);
+int32_t launch_restrict(const dnnmg_restrict_t*, const float*, float*, cudaStream_t);
 int32_t launch_stab(const dnnmg_level_t*, const float*, const dnnmg_phys_t*, float*, float*,
                     cudaStream_t);
 int32_t launch_residual(const dnnmg_level_t*, const float*, const float*, const float*,
@@ -76,6 +77,10 @@ int32_t dnnmg_prolongate(const dnnmg_prolong_t* P, const float* xc, float* xf,
 
 int32_t dnnmg_apply_dirichlet(const dnnmg_dirichlet_t* bc, float* x, dnnmg_stream_t s) {
   return launch_dirichlet(bc, x, as_stream(s));
+}
+
+int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* bf, float* bc, dnnmg_stream_t s) {
+  return launch_restrict(R, bf, bc, as_stream(s));
 }
 
 int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph, float* aT,

@@ -257,6 +257,40 @@ int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float
   return DNNMG_OK;
 }
 
+// K6: b_coarse[m] = sum_{i in row m, ascending fine node} w_i * b_fine[fine_i] (P^T b)
+__global__ void __launch_bounds__(256) restrict_kernel(int n_coarse, const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ fine,
+                                                       const float* __restrict__ w,
+                                                       const float4* __restrict__ bf,
+                                                       float4* __restrict__ bc) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n_coarse; m += gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int s = __ldg(ptr + m), e = __ldg(ptr + m + 1);
+    for (int i = s; i < e; ++i) {
+      const float wi = __ldg(w + i);
+      const float4 v = __ldg(bf + __ldg(fine + i));
+      acc.x = fmaf(wi, v.x, acc.x);
+      acc.y = fmaf(wi, v.y, acc.y);
+      acc.z = fmaf(wi, v.z, acc.z);
+      acc.w = fmaf(wi, v.w, acc.w);
+    }
+    bc[m] = acc;
+  }
+}
+
+int32_t launch_restrict(const dnnmg_restrict_t* R, const float* bf, float* bc, cudaStream_t s) {
+  DNNMG_REQUIRE(R && R->ptr && R->fine && R->w && bf && bc, DNNMG_ERR_ARG,
+                "restrict: null argument");
+  DNNMG_REQUIRE(((uintptr_t)bf & 15) == 0 && ((uintptr_t)bc & 15) == 0, DNNMG_ERR_ARG,
+                "restrict: vectors must be 16-byte aligned");
+  if (R->n_coarse_nodes == 0) return DNNMG_OK;
+  restrict_kernel<<<grid_for(R->n_coarse_nodes, 256), 256, 0, s>>>(
+      R->n_coarse_nodes, R->ptr, R->fine, R->w, reinterpret_cast<const float4*>(bf),
+      reinterpret_cast<float4*>(bc));
+  DNNMG_CHECK_LAUNCH("restrict_kernel");
+  return DNNMG_OK;
+}
+
 int32_t launch_dirichlet(const dnnmg_dirichlet_t* bc, float* x, cudaStream_t s) {
   DNNMG_REQUIRE(bc && x && bc->bc_code, DNNMG_ERR_ARG, "apply_dirichlet: null argument");
   if (bc->n_nodes == 0) return DNNMG_OK;

@@ -119,6 +119,44 @@ class DeviceProlong:
         return store[key]
 
 
+class DeviceRestrict:
+    """K6 tables for level+1 -> level: P^T as a coarse-node CSR (rows ascending fine node)."""
+
+    def __init__(self, hierarchy, level):
+        from .space import prolongation_matrix
+        PT = prolongation_matrix(hierarchy, level).T.tocsr()
+        PT.sort_indices()
+        self.n_coarse, self.n_fine = int(PT.shape[0]), int(PT.shape[1])
+        self.ptr = upload(PT.indptr, np.int32)
+        self.fine = upload(PT.indices, np.int32)
+        self.w = upload(PT.data, np.float32)   # dyadic weights: exact in fp32
+        self.struct = _lib.Restrict(self.n_coarse, self.n_fine, ptr(self.ptr), ptr(self.fine),
+                                    ptr(self.w))
+
+    @staticmethod
+    def get(hierarchy, level):
+        store, key = _cache(hierarchy, ("restrict", level))
+        if key not in store:
+            store[key] = DeviceRestrict(hierarchy, level)
+        return store[key]
+
+
+def restrict_vector(hierarchy, b, level_fine, levels_down=1):
+    """b_coarse = (P^T)^levels_down b on the device (space.py:188-196)."""
+    v = f32(b)
+    lvl = level_fine
+    for _ in range(levels_down):
+        R = DeviceRestrict.get(hierarchy, lvl - 1)
+        if v.numel() != 4 * R.n_fine:
+            raise ValueError(f"vector length {v.numel()} does not match level {lvl} "
+                             f"({4 * R.n_fine} dofs)")
+        out = torch.empty(4 * R.n_coarse, dtype=torch.float32, device=v.device)
+        _lib.call("dnnmg_restrict", ctypes.byref(R.struct), ptr(v), ptr(out), stream_handle())
+        v = out
+        lvl -= 1
+    return like_input(v, b)
+
+
 class DeviceLevel:
     """K2 tables of one level: cell nodes, fp64 coordinates, h_T, node->cell CSR."""
 

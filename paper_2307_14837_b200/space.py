@@ -157,8 +157,9 @@ def inject(space_coarse, x_fine):
 
 
 def restrict_rhs(hierarchy, b, level_fine, levels_down=1):
-    """P^T restriction of a dual vector (space.py:188-196) — next-row #1, GPU pending."""
-    raise NotImplementedError("restrict_rhs is outside the correction step (SURVEY §8(f) #1)")
+    """P^T restriction of a dual vector on the GPU (space.py:188-196, Alg. 1 line 9)."""
+    from . import device
+    return device.restrict_vector(hierarchy, b, level_fine, levels_down)
 
 
 # -- Dirichlet data ---------------------------------------------------------------------

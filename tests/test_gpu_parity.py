@@ -326,3 +326,45 @@ def test_f16x3_weight_scaling(wscale):
                                   m.input_mean, m.input_std), X)
     Y = net.forward(m, X, precision="f16x3")
     assert rel(Y, ref) < 1e-5, rel(Y, ref)
+
+
+# ---- restriction P^T (next row #1, space.py:188-196) ---------------------------------------
+
+def _golden_P(g, i):
+    import scipy.sparse as sp
+    ind = g[f"P{i}_indptr"]
+    nf = ind.size - 1
+    nc = int(g[f"P{i}_indices"].max()) + 1 if g[f"P{i}_indices"].size else 0
+    return sp.csr_matrix((g[f"P{i}_data"], g[f"P{i}_indices"], ind), shape=(nf, nc))
+
+
+@pytest.mark.parametrize("name", ["cfg0", "jit", "j2", "lvl1"])
+def test_restrict_rhs_is_Pt(name):
+    """restrict_rhs(b, L+J, J) == (P^T)^J b with the reference's own P (golden CSR)."""
+    import scipy.sparse as sp
+    g = load_golden(name)
+    h = product_hierarchy(g)
+    L, J = int(g["L"]), int(g["J"])
+    ref = g["b_next"].astype(float)
+    for i in reversed(range(L, L + J)):
+        P = _golden_P(g, i)
+        ref = sp.kron(P, sp.identity(4, format="csr"), format="csr").T @ ref
+    got = spmod.restrict_rhs(h, g["b_next"], L + J, J)
+    assert got.shape == ref.shape
+    assert rel(got, ref) < 1e-6, rel(got, ref)
+    assert np.all(spmod.restrict_rhs(h, np.zeros_like(g["b_next"]), L + J, J) == 0.0)
+
+
+def test_restrict_transpose_pairing():
+    """test_space.py:52-59 on the GPU: b . (P x) == (P^T b) . x."""
+    g = load_golden("jit")
+    h = product_hierarchy(g)
+    rng = np.random.default_rng(3)
+    nc = 4 * h.scalar_nodes(0)[0].shape[0]
+    nf = 4 * h.scalar_nodes(1)[0].shape[0]
+    x = rng.standard_normal(nc)
+    b = rng.standard_normal(nf)
+    Px = spmod.prolongate(h, spmod.StateVector(0, x, 0.0)).values
+    Ptb = spmod.restrict_rhs(h, b, 1, 1)
+    lhs, rhs = b @ Px, Ptb @ x
+    assert abs(lhs - rhs) < 1e-5 * (np.abs(b) @ np.abs(Px) + 1.0), (lhs, rhs)

@@ -422,6 +422,29 @@ def run_ours(args, rank, world, local):
     f1.record()
     barrier()
     ms_fused = f0.elapsed_time(f1)
+    # Alg. 1 lines 8-9 around the step (not part of `value`): next-step fine RHS from the
+    # corrected state (K2 in RHS form + node sum) and its restriction to the coarse level (K6)
+    aux = {}
+    try:
+        from paper_2307_14837_b200 import device as dvm
+        xc_out = step(*pairs[0])
+        b_next = step.rhs_next(xc_out)
+        dvm.restrict_vector(h, b_next, step.L + step.J, step.J)   # builds the K6 tables
+        barrier()
+        a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a0.record()
+        for _ in range(args.steps):
+            step.rhs_next(xc_out, b_next)
+        a1.record()
+        for _ in range(args.steps):
+            dvm.restrict_vector(h, b_next, step.L + step.J, step.J)
+        a2.record()
+        barrier()
+        aux = {"rhs_next_ms": a0.elapsed_time(a1) / args.steps,
+               "restrict_ms": a1.elapsed_time(a2) / args.steps,
+               "note": "Alg. 1 lines 8-9 (next-step RHS, P^T restriction); outside the timed step"}
+    except Exception as exc:  # pragma: no cover - auxiliary numbers only
+        aux = {"error": str(exc)[:200]}
     # the same step replayed from CUDA graphs (one per input pair): removes launch gaps,
     # which dominate for the small configs
     graphs = []
@@ -558,6 +581,7 @@ def run_ours(args, rank, world, local):
         "kernels": per_kernel,
         "ms_per_step_fused": ms_fused / args.steps, "ms_per_step_staged": ms / args.steps,
         "ms_per_step_graph": ms_graph / args.steps,
+        "aux": aux,
         "cpu_baseline": cpu,
         "clocks": sampler.summary(),
     }

@@ -116,3 +116,71 @@ def forward(model, X, precision=None):
     Y = torch.empty((Xd.shape[0], model.arch.n_out), dtype=torch.float32, device=Xd.device)
     dm.forward(Xd, Xd.shape[0], Y)
     return dv.like_input(Y, X)
+
+
+# -- "DNMG" model file (net.py:337-392): trained weights for the correction path ----------
+#
+# Little-endian layout: b"DNMG", u32 version (= 1), u32 n_in, n_hidden, depth, n_out,
+# u32 len(activation), the activation name, f64 bn_eps, f64 bn_momentum, then float64
+# arrays: input_mean[n_in], input_std[n_in], W_0..W_depth (row-major, fan_in x fan_out),
+# and per hidden layer gamma, beta, running_mean, running_var [n_hidden].
+
+_DNMG_MAGIC = b"DNMG"
+_DNMG_VERSION = 1
+
+
+def _dnmg_shapes(arch):
+    dims = [arch.n_in] + [arch.n_hidden] * arch.depth + [arch.n_out]
+    shapes = [("input_mean", None, (arch.n_in,)), ("input_std", None, (arch.n_in,))]
+    shapes += [("W", i, (dims[i], dims[i + 1])) for i in range(arch.depth + 1)]
+    for i in range(arch.depth):
+        shapes += [(name, i, (arch.n_hidden,)) for name in ("gamma", "beta", "running_mean",
+                                                            "running_var")]
+    return shapes
+
+
+def load_model(path):
+    """Read a DNMG model file into an eval-mode MlpModel."""
+    raw = open(path, "rb").read()
+    if raw[:4] != _DNMG_MAGIC:
+        raise ValueError(f"not a model file: bad magic {raw[:4]!r}")
+    head = np.frombuffer(raw, dtype="<u4", count=6, offset=4)
+    if int(head[0]) != _DNMG_VERSION:
+        raise ValueError(f"unsupported model file version {int(head[0])}")
+    n_in, n_hidden, depth, n_out, tag_len = (int(v) for v in head[1:])
+    off = 28
+    activation = raw[off:off + tag_len].decode()
+    off += tag_len
+    bn_eps, bn_momentum = (float(v) for v in np.frombuffer(raw, dtype="<f8", count=2, offset=off))
+    off += 16
+    arch = Architecture(n_in, n_hidden, depth, n_out)
+    model = MlpModel(arch, activation=activation, bn_eps=bn_eps, bn_momentum=bn_momentum)
+    for name, i, shape in _dnmg_shapes(arch):
+        n = int(np.prod(shape))
+        if off + 8 * n > len(raw):
+            raise ValueError("model file truncated")
+        arr = np.frombuffer(raw, dtype="<f8", count=n, offset=off).reshape(shape).astype(np.float64)
+        off += 8 * n
+        if i is None:
+            setattr(model, name, arr)
+        else:
+            getattr(model, name)[i] = arr
+    return model.eval()
+
+
+def save_model(model, path):
+    """Write a DNMG model file (the reference's format, readable by its load_model)."""
+    a = model.arch
+    tag = model.activation.encode()
+    parts = [_DNMG_MAGIC,
+             np.array([_DNMG_VERSION, a.n_in, a.n_hidden, a.depth, a.n_out, len(tag)],
+                      dtype="<u4").tobytes(),
+             tag, np.array([model.bn_eps, model.bn_momentum], dtype="<f8").tobytes()]
+    for name, i, shape in _dnmg_shapes(a):
+        arr = getattr(model, name) if i is None else getattr(model, name)[i]
+        arr = np.asarray(arr, dtype="<f8")
+        if arr.shape != shape:
+            raise ValueError(f"{name}[{i}] has shape {arr.shape}, expected {shape}")
+        parts.append(np.ascontiguousarray(arr).tobytes())
+    with open(path, "wb") as f:
+        f.write(b"".join(parts))

@@ -546,6 +546,17 @@ def run_ours(args, rank, world, local):
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": f"{peak_kind} hbm copy"}
+    # K2 is FP32-issue-bound, not HBM-bound: its compute roofline against the measured
+    # 3-register FFMA throughput of this GPU (tools/ubench/ffma2.cu: 49.3 TFLOP/s).  FLOPs per
+    # cell of this kernel's formulation from its executed SASS mix (FFMA 769, FMUL 347,
+    # FADD 90 warp-instructions per cell x 32 lanes; profiles/r1_kernels_cfg3_ncu.txt)
+    if "K2_residual" in per_kernel:
+        k2_flop = 32 * (2 * 769 + 347 + 90) * step.level.n_cells
+        ach2 = k2_flop / (per_kernel["K2_residual"]["ms"] / 1e3) / 1e12
+        per_kernel["K2_residual"]["fp32_roofline"] = {
+            "bound": "fp32 issue", "achieved": ach2, "peak": 49.3, "unit": "TFLOP/s",
+            "frac": ach2 / 49.3,
+            "peak_source": "measured FFMA (register form) throughput, tools/ubench/ffma2.cu"}
     # DRAM traffic per launch of each stage from the committed ncu capture (round-1 profile)
     try:
         with open(os.path.join(REPO, "profiles", "r1_dram_traffic.json")) as f:

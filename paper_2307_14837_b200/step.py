@@ -87,6 +87,27 @@ class CorrectionStep:
     def n_patches(self):
         return self.ps.n_patches
 
+    def twin(self):
+        """A second workspace for the same problem: shares every device table and the
+        packed model, owns its work buffers, so two steps can be in flight on two
+        streams (HostPipeline(lanes=2))."""
+        import copy
+        t = copy.copy(self)
+        dev = self.x_tilde.device
+        f = torch.float32
+        t.x_tilde = torch.empty_like(self.x_tilde)
+        t.r = torch.empty_like(self.r)
+        t.d = torch.empty_like(self.d)
+        t.x_corr = torch.empty_like(self.x_corr)
+        t.elem = torch.empty_like(self.elem)
+        t.X = torch.empty(0 if self.fused_gather else self.X.numel(), dtype=f, device=dev)
+        t.Y = torch.empty_like(self.Y)
+        t.x_mid = None if self.x_mid is None else torch.empty_like(self.x_mid)
+        t.buf = _lib.StepBuffers(dv.ptr(t.x_tilde), dv.ptr(t.r), dv.ptr(t.elem), dv.ptr(t.X),
+                                 dv.ptr(t.Y), dv.ptr(t.d), dv.ptr(t.x_mid))
+        t.graph = None
+        return t
+
     @property
     def launches(self):
         return int(_lib.load().dnnmg_correction_step_launches(self.J, ctypes.byref(self.model.struct)))
@@ -209,16 +230,22 @@ class HostPipeline:
     at config 3, serialising copies and kernels would make the PCIe transfers,
     not the kernels, the step time."""
 
-    def __init__(self, step, depth=2):
+    def __init__(self, step, depth=2, lanes=1):
+        """lanes = 2 runs consecutive steps on two compute streams with two workspaces
+        (CorrectionStep.twin), so one step's memory-bound tail kernels can overlap the
+        next step's head."""
+        if lanes not in (1, 2) or depth % lanes:
+            raise ValueError("lanes must be 1 or 2 and divide depth")
         self.step = step
         self.depth = depth
+        self.steps = [step] + [step.twin() for _ in range(lanes - 1)]
         dev = step.x_tilde.device
         f = torch.float32
         self.dx = [torch.empty(step.coarse_ndof, dtype=f, device=dev) for _ in range(depth)]
         self.db = [torch.empty_like(step.x_tilde) for _ in range(depth)]
         self.dout = [torch.empty_like(step.x_tilde) for _ in range(depth)]
         self.s_in = torch.cuda.Stream(device=dev)
-        self.s_run = torch.cuda.Stream(device=dev)
+        self.s_runs = [torch.cuda.Stream(device=dev) for _ in range(lanes)]
         self.s_out = torch.cuda.Stream(device=dev)
         self.ev_in = [torch.cuda.Event() for _ in range(depth)]
         self.ev_run = [torch.cuda.Event() for _ in range(depth)]
@@ -229,7 +256,7 @@ class HostPipeline:
     def begin(self):
         """Order the pipeline after everything already queued on the current stream."""
         cur = torch.cuda.current_stream()
-        for s in (self.s_in, self.s_run, self.s_out):
+        for s in [self.s_in, self.s_out] + self.s_runs:
             s.wait_stream(cur)
 
     def submit(self, x_host, b_host, out_host):
@@ -240,11 +267,13 @@ class HostPipeline:
             self.dx[k].copy_(x_host, non_blocking=True)
             self.db[k].copy_(b_host, non_blocking=True)
             self.ev_in[k].record()
-        with torch.cuda.stream(self.s_run):
-            self.s_run.wait_event(self.ev_in[k])
+        lane = self.i % len(self.steps)
+        s_run = self.s_runs[lane]
+        with torch.cuda.stream(s_run):
+            s_run.wait_event(self.ev_in[k])
             if self._used[k]:
-                self.s_run.wait_event(self.ev_out[k])     # dout[k] has been copied out
-            self.step.run(self.dx[k], self.db[k], self.dout[k])
+                s_run.wait_event(self.ev_out[k])          # dout[k] has been copied out
+            self.steps[lane].run(self.dx[k], self.db[k], self.dout[k])
             self.ev_run[k].record()
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_run[k])
@@ -255,5 +284,5 @@ class HostPipeline:
 
     def join(self):
         cur = torch.cuda.current_stream()
-        for s in (self.s_in, self.s_run, self.s_out):
+        for s in [self.s_in, self.s_out] + self.s_runs:
             cur.wait_stream(s)

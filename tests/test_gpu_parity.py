@@ -274,8 +274,9 @@ def test_tc_rejects_unsupported_width():
         net.forward(m, np.zeros((4, 240)), precision="bf16")
 
 
+@pytest.mark.parametrize("lanes", [1, 2])
 @pytest.mark.parametrize("precision", ["fp32", "f16x3"])
-def test_host_pipeline_matches_run(precision):
+def test_host_pipeline_matches_run(precision, lanes):
     """step.HostPipeline (H2D / kernels / D2H overlapped on three streams,
     double-buffered) returns exactly what CorrectionStep.run returns per step."""
     from paper_2307_14837_b200.step import HostPipeline
@@ -294,7 +295,7 @@ def test_host_pipeline_matches_run(precision):
     for xc, b in ins:
         ref.append(step(xc.cuda(), b.cuda()).cpu().clone())
     outs = [torch.empty_like(ref[0]).pin_memory() for _ in ins]
-    pipe = HostPipeline(step)
+    pipe = HostPipeline(step, lanes=lanes)
     pipe.begin()
     for (xc, b), o in zip(ins, outs):
         pipe.submit(xc, b, o)

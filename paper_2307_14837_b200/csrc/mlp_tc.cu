@@ -329,9 +329,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   float* p_mean = p_shift + A.depth * kTcH;
   float* p_rstd = p_mean + kTcH;
   const PackHdr* hdr = reinterpret_cast<const PackHdr*>(A.packed);
+  // fp32-accuracy tanh takes 2^(2 log2(e) z): fold 2 log2(e) into the BN scale and shift so
+  // that the epilogue needs one FFMA before ex2 (the activation never needs z itself)
+  const bool fold = MODE != DNNMG_PREC_BF16 && A.act == DNNMG_ACT_TANH;
+  const float k2 = fold ? 2.8853900817779268f : 1.0f;
   for (int i = threadIdx.x; i < A.depth * kTcH; i += blockDim.x) {
-    p_scale[i] = A.scale[i] * hdr->unscale[i / kTcH];  // 2^-s: exact
-    p_shift[i] = A.shift[i];
+    p_scale[i] = A.scale[i] * hdr->unscale[i / kTcH] * k2;  // 2^-s: exact
+    p_shift[i] = A.shift[i] * k2;
   }
   const float y_unscale = hdr->unscale[A.depth];
   float* y_stage = p_rstd + kTcH;
@@ -569,7 +573,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
             const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float a = act_fast(fmaf(v[e + u], sv[u], tv[u]), A.act, accurate);
+              const float z = fmaf(v[e + u], sv[u], tv[u]);
+              float a;
+              if (fold) {  // z = 2 log2(e) * BN(acc): tanh = 1 - 2 / (1 + 2^z)
+                float ez, r;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ez) : "f"(z));
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + ez));
+                a = fmaf(-2.0f, r, 1.0f);
+              } else {
+                a = act_fast(z, A.act, accurate);
+              }
               h[c][e + u] = a + h[c][e + u];
               v[e + u] = h[c][e + u];
             }

@@ -199,11 +199,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return r;
 }
 // x = hi + lo for a pair of values: hi = fp16(x), lo = fp16(x - hi) (x - hi is exact)
+// hi = x with its fp32 mantissa truncated to the 10 bits fp16 keeps (exact in fp16 for
+// |x| >= 2^-14), lo = x - hi (exact) rounded to fp16: |x - hi - lo| <= 2^-21 |x|
 __device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
-  const __half2 h2 = *reinterpret_cast<const __half2*>(&hi);
-  const float2 hf = __half22float2(h2);
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - hf.y), "f"(a - hf.x));
+  const float ha = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+  const float hb = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(hb), "f"(ha));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - hb), "f"(a - ha));
 }
 
 // canonical K-major no-swizzle shared-memory matrix descriptor

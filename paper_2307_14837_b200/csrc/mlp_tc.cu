@@ -52,7 +52,7 @@ template <> struct TcCfg<DNNMG_PREC_TF32X3> {
   static constexpr int ESZ = 4, PARTS = 2, NW = 3, NA = 4, KSTEP = 8, KC = 16;
 };
 template <> struct TcCfg<DNNMG_PREC_F16X3> {
-  static constexpr int ESZ = 2, PARTS = 2, NW = 3, NA = 4, KSTEP = 16, KC = 32;
+  static constexpr int ESZ = 2, PARTS = 2, NW = 2, NA = 4, KSTEP = 16, KC = 32;
 };
 static int kc_of(int precision) { return precision == DNNMG_PREC_TF32X3 ? 16 : 32; }
 // packed weight image: header (per-GEMM output unscale 2^-s and shift s), then the chunks

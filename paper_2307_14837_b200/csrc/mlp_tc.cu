@@ -623,32 +623,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
             }
           }
         } else {
-        // stage the 128 x n_out tile in the dedicated SMEM buffer (the A ring already
-        // carries the next tile's layer-0 chunks), then one coalesced block copy
+        // stage the 128 x n_out tile through a 64-row SMEM buffer in two halves (the A ring
+        // already carries the next tile's layer-0 chunks; a small buffer leaves more L1 for
+        // the fused gather), each followed by one coalesced block copy
         float* ys = y_stage;
-        for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
-          float v[16];
-          tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
+        const int64_t r0 = tile * kTcM;
+        const int nvalid = (int)((A.n_rows - r0) < kTcM ? (A.n_rows - r0) : kTcM);
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          if ((quad >> 1) == half) {
+            for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
+              float v[16];
+              tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int col = sl * 16 + e;
-            if (col < A.n_out) ys[row_in_tile * A.n_out + col] = v[e] * y_unscale;
+              for (int e = 0; e < 16; ++e) {
+                const int col = sl * 16 + e;
+                if (col < A.n_out) ys[(row_in_tile - 64 * half) * A.n_out + col] = v[e] * y_unscale;
+              }
+            }
           }
+          tc_fence_before();
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          {  // coalesced copy of this half's contiguous Y block
+            const int nh = nvalid - 64 * half;
+            const int nf = (nh < 0 ? 0 : nh > 64 ? 64 : nh) * A.n_out;
+            float* dst = A.Y + (r0 + 64 * half) * A.n_out;
+            const int tid = threadIdx.x;
+            const int n4 = nf >> 2;
+            for (int i = tid; i < n4; i += 256)
+              reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(ys)[i];
+            for (int i = 4 * n4 + tid; i < nf; i += 256) dst[i] = ys[i];
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
         }
-        tc_fence_before();
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        {  // coalesced copy of the contiguous Y block of this tile
-          const int64_t r0 = tile * kTcM;
-          const int nvalid = (int)((A.n_rows - r0) < kTcM ? (A.n_rows - r0) : kTcM);
-          const int nf = nvalid * A.n_out;
-          float* dst = A.Y + r0 * A.n_out;
-          const int tid = threadIdx.x;
-          const int n4 = nf >> 2;
-          for (int i = tid; i < n4; i += 256)
-            reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(ys)[i];
-          for (int i = 4 * n4 + tid; i < nf; i += 256) dst[i] = ys[i];
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
         }
         tc_fence_before();
         __syncwarp();
@@ -827,7 +834,7 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
   size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 4) + 16 +
                 sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
-  const size_t ybytes = (size_t)kTcM * m->n_out * 4;
+  const size_t ybytes = (size_t)(kTcM / 2) * m->n_out * 4;  // staged in two 64-row halves
   if (smem + ybytes <= 225 * 1024) {
     A.y_mode = 2;
     smem += ybytes;

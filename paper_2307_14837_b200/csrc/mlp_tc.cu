@@ -324,7 +324,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   uint64_t* a_empty = bars + 2 * C::NW + C::NA;
   uint64_t* acc_full = bars + 2 * C::NW + 2 * C::NA;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* idx_full = acc_empty + 2;   // fused gather: next tile's node indices staged by TMA
+  uint64_t* idx_empty = idx_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(idx_empty + 1);
   // BN scale/shift per hidden layer and the input normalisation, staged once per CTA
   float* p_scale = reinterpret_cast<float*>(tmem_slot + 4);
   float* p_shift = p_scale + A.depth * kTcH;
@@ -340,7 +342,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     p_shift[i] = A.shift[i] * k2;
   }
   const float y_unscale = hdr->unscale[A.depth];
-  float* y_stage = p_rstd + kTcH;
+  int32_t* idx_s = reinterpret_cast<int32_t*>(p_rstd + kTcH);  // [kTcM][npp] (GATHER only)
+  float* y_stage = p_rstd + kTcH + (GATHER ? kTcM * A.npp : 0);
   for (int i = threadIdx.x; i < kTcH; i += blockDim.x) {
     p_mean[i] = i < A.n_in ? A.in_mean[i] : 0.f;
     p_rstd[i] = i < A.n_in ? 1.0f / A.in_std[i] : 0.f;
@@ -364,6 +367,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 8);
     }
+    mbar_init(smem_u32(idx_full), 1);
+    mbar_init(smem_u32(idx_empty), 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kProducerWarp) {
@@ -381,7 +386,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     // ---------------- weight producer ----------------
     if (lane == 0) {
       uint32_t item = 0;
+      // fused gather: each full tile's node-index block (kTcM x npp int32, contiguous) is
+      // copied into shared memory one tile ahead (partial tiles read the indices directly)
+      const uint32_t idx_bytes = (uint32_t)kTcM * A.npp * 4;
+      auto full_tile = [&](int64_t t) { return t < n_tiles && (t + 1) * kTcM <= A.n_rows; };
+      uint32_t icopy = 0;
+      auto stage_idx = [&](int64_t t) {
+        if (!GATHER || !full_tile(t) || (idx_bytes & 15)) return;
+        if (icopy > 0) mbar_wait(smem_u32(idx_empty), (icopy - 1) & 1);
+        mbar_expect_tx(smem_u32(idx_full), idx_bytes);
+        bulk_g2s(smem_u32(idx_s), A.node_table + t * kTcM * A.npp, idx_bytes, smem_u32(idx_full));
+        ++icopy;
+      };
+      stage_idx(blockIdx.x);
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        stage_idx(tile + gridDim.x);
         for (int g = 0; g < G; ++g) {
           const int N = g < A.depth ? kTcH : A.Nhead;
           const int nk = (g == 0 ? A.K0p : kTcH) / KC;
@@ -466,8 +485,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     const int nck0 = A.K0p / KC;
     const bool vec_x = (A.n_in & 3) == 0;
     float xin[NCH][HC];                 // raw input row slice of the next tile (prefetched)
+    uint32_t iload = 0;                 // staged index blocks consumed
+    const bool idx_staged = GATHER && ((kTcM * A.npp * 4) & 15) == 0;
     auto load_x = [&](int64_t tile) {
       const int64_t row = tile * kTcM + row_in_tile;
+      const bool from_smem = idx_staged && tile < n_tiles && (tile + 1) * kTcM <= A.n_rows;
+      if (from_smem) mbar_wait(smem_u32(idx_full), iload & 1);
       const bool ok = tile < n_tiles && row < A.n_rows;
       if constexpr (GATHER) {
         // fused gather (patch_ops.py:49-53): float4 slot s of the row is x~ of node s,
@@ -481,8 +504,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           for (int j = 0; j < HC / 4; ++j) {
             const int f4 = (KC / 4) * c + (HC / 4) * hh + j;
             const int s = f4 < A.npp ? f4 : f4 - A.npp;
-            nidx[c][j] = (ok && c < nck0 && f4 < 2 * A.npp) ? __ldg(nt + s) : 0;
+            nidx[c][j] = (ok && c < nck0 && f4 < 2 * A.npp)
+                             ? (from_smem ? idx_s[row_in_tile * A.npp + s] : __ldg(nt + s))
+                             : 0;
           }
+        if (from_smem) {  // the index block may be overwritten with the next tile's
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(idx_empty));
+          ++iload;
+        }
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
@@ -832,7 +862,8 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.in_std = m->in_std;
   constexpr int WST = kTcH * C::KC * C::ESZ * C::PARTS;
   constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
-  size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 4) + 16 +
+  size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 6) + 16 +
+                (g ? (size_t)kTcM * g->npp * 4 : 0) +
                 sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
   const size_t ybytes = (size_t)(kTcM / 2) * m->n_out * 4;  // staged in two 64-row halves
   if (smem + ybytes <= 225 * 1024) {

@@ -113,6 +113,9 @@ typedef struct {
   const int32_t* node_cell_ptr;  /* [n_nodes+1] CSR node -> incident (cell*27 + a), */
   const int32_t* node_cell_idx;  /*   cells ascending (= the reference bincount order) */
   const uint8_t* dof_mask;       /* [n_nodes] bit c set <=> dof 4n+c constrained; NULL = none */
+  const float* geo_q;            /* per-mesh geometry cache from dnnmg_level_geometry
+                                    ([n_cells][10][64]: J^-1 row-major, w) or NULL: K2 then
+                                    recomputes the isoparametric geometry every call */
 } dnnmg_level_t;
 
 typedef struct {
@@ -163,6 +166,9 @@ int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* b_fine, float* b_
                        dnnmg_stream_t stream);
 
 /* ---- K2: stabilisation, residual, next RHS ---------------------------------- */
+/* geometry cache of a level (constant mesh): geo_out = [n_cells][10][64] float32, i.e.
+ * 2,560 bytes per cell; set lv->geo_q = geo_out to let K2 skip the geometry work */
+int32_t dnnmg_level_geometry(const dnnmg_level_t* lv, float* geo_out, dnnmg_stream_t stream);
 int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph,
                    float* alpha_T, float* delta_T, dnnmg_stream_t stream);
 /* r = b_prev - A_h(x); rows with dof_mask bits set are zeroed when apply_mask != 0.

@@ -33,7 +33,7 @@ class Dirichlet(ctypes.Structure):
 class Level(ctypes.Structure):
     _fields_ = [("n_nodes", c_i32), ("n_cells", c_i32), ("cell_nodes", c_vp), ("coords", c_vp),
                 ("h_T", c_vp), ("node_cell_ptr", c_vp), ("node_cell_idx", c_vp),
-                ("dof_mask", c_vp)]
+                ("dof_mask", c_vp), ("geo_q", c_vp)]
 
 
 class Phys(ctypes.Structure):
@@ -71,6 +71,7 @@ EXPORTS = {
     "dnnmg_prolongate": (c_i32, [ctypes.POINTER(Prolong), c_vp, c_vp, ctypes.POINTER(Dirichlet), c_vp]),
     "dnnmg_apply_dirichlet": (c_i32, [ctypes.POINTER(Dirichlet), c_vp, c_vp]),
     "dnnmg_restrict": (c_i32, [ctypes.POINTER(Restrict), c_vp, c_vp, c_vp]),
+    "dnnmg_level_geometry": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp]),
     "dnnmg_stab": (c_i32, [ctypes.POINTER(Level), c_vp, ctypes.POINTER(Phys), c_vp, c_vp, c_vp]),
     "dnnmg_residual": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(Phys),
                                c_vp, c_vp, c_i32, c_vp]),

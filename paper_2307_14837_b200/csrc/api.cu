@@ -19,6 +19,7 @@ int32_t launch_prolongate(const dnnmg_prolong_t*, const float*, float*, const dn
                           cudaStream_t);
 int32_t launch_dirichlet(const dnnmg_dirichlet_t*, float*, cudaStream_t);
 int32_t launch_restrict(const dnnmg_restrict_t*, const float*, float*, cudaStream_t);
+int32_t launch_level_geometry(const dnnmg_level_t*, float*, cudaStream_t);
 int32_t launch_stab(const dnnmg_level_t*, const float*, const dnnmg_phys_t*, float*, float*,
                     cudaStream_t);
 int32_t launch_residual(const dnnmg_level_t*, const float*, const float*, const float*,
@@ -81,6 +82,10 @@ int32_t dnnmg_apply_dirichlet(const dnnmg_dirichlet_t* bc, float* x, dnnmg_strea
 
 int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* bf, float* bc, dnnmg_stream_t s) {
   return launch_restrict(R, bf, bc, as_stream(s));
+}
+
+int32_t dnnmg_level_geometry(const dnnmg_level_t* lv, float* geo, dnnmg_stream_t s) {
+  return launch_level_geometry(lv, geo, as_stream(s));
 }
 
 int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph, float* aT,

@@ -75,6 +75,19 @@ constexpr int oTZ = oSY;              // tz[4][2][27] aliases sy (dead after the
 constexpr int kCellFloats = (oCF + kNCF * kCFS + 3) / 4 * 4;
 static_assert(oTZ + 4 * 2 * 27 <= oCF, "tz must fit in sy");
 static_assert(oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
+
+// Layout of the geometry-cached form: J^-1 and w per Gauss point come from a per-mesh
+// cache (geometry_kernel), so only p and v (4 fields) go through the forward stages and
+// the cell's cached block [10][64] is staged by cp.async one cell ahead.
+template <bool CACHED>
+struct KLay {
+  static constexpr int NF = CACHED ? 4 : kNF;         // Q2 fields through the forward stages
+  static constexpr int FO = NF - 4;                    // index of p among them
+  static constexpr int oCF = oSY + NF * kSYF;
+  static constexpr int oGQ = oCF + kNCF * kCFS;        // cached [J^-1 (9) | w][64]
+  static constexpr int kFloats = (oGQ + (CACHED ? 10 * 64 : 0) + 3) / 4 * 4;
+  static_assert(oTZ + 4 * 2 * 27 <= oCF && oCF % 4 == 0 && oGQ % 4 == 0, "layout");
+};
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
 constexpr int CB = 4;        // B[c][k]   reference-gradient test
@@ -93,6 +106,7 @@ struct ResidualArgs {
   const float* delta_in;
   float nu, k, alpha0, delta0;
   float ik;  // 1/k
+  const float* geo_q;  // per-mesh geometry cache [n_cells][10][64] (J^-1 row-major, w) or NULL
   int convection;
   int mode;
   float4* elem;
@@ -123,55 +137,82 @@ struct NodeRaw {
   float hT;
 };
 
+template <bool CACHED>
 __device__ __forceinline__ void load_raw(const ResidualArgs& A, int c, int node, int t, NodeRaw& r) {
-  const int n0 = __shfl_sync(0xffffffffu, node, 0);
-  const double* X = A.coords + 3 * (int64_t)node;
-  const double* X0 = A.coords + 3 * (int64_t)n0;
-  if (t < 27) {
-    r.X[0] = __ldg(X);
-    r.X[1] = __ldg(X + 1);
-    r.X[2] = __ldg(X + 2);
-    r.X0[0] = __ldg(X0);
-    r.X0[1] = __ldg(X0 + 1);
-    r.X0[2] = __ldg(X0 + 2);
-    r.xv = __ldg(A.x + node);
+  if constexpr (!CACHED) {
+    const int n0 = __shfl_sync(0xffffffffu, node, 0);
+    const double* X = A.coords + 3 * (int64_t)node;
+    const double* X0 = A.coords + 3 * (int64_t)n0;
+    if (t < 27) {
+      r.X[0] = __ldg(X);
+      r.X[1] = __ldg(X + 1);
+      r.X[2] = __ldg(X + 2);
+      r.X0[0] = __ldg(X0);
+      r.X0[1] = __ldg(X0 + 1);
+      r.X0[2] = __ldg(X0 + 2);
+    }
   }
+  if (t < 27) r.xv = __ldg(A.x + node);
   r.hT = __ldg(A.h_T + c);
 }
 
+// cp.async of cell c's cached geometry block (2560 B = 160 x 16 B, 5 per lane)
+__device__ __forceinline__ void stage_geo(const ResidualArgs& A, int c, int t, float* dst) {
+  const float4* src = reinterpret_cast<const float4*>(A.geo_q + (int64_t)c * 640);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + 4 * (t + 32 * k)));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + t + 32 * k)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // coefficients of one Gauss point (pointwise phase); F = Q2 fields at q
-template <int MODE>
+template <int MODE, bool CACHED>
 __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S, float* CF, int q,
-                                          float F[kNF][4], float aT, float dT) {
+                                          float F[KLay<CACHED>::NF][4], float aT, float dT) {
+  using L = KLay<CACHED>;
+  constexpr int FO = L::FO;
   const int qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
-  float J[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) J[i][j] = F[i][1 + j];
-  const float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-  const float c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-  const float c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-  const float det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-  const float id = 1.0f / det;
   float Ji[3][3];  // (J^-1)[k][j]: reference k -> physical j
-  Ji[0][0] = c00 * id;
-  Ji[1][0] = c01 * id;
-  Ji[2][0] = c02 * id;
-  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
-  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
-  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
-  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
-  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
-  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
-  const float w = cW[qx] * cW[qy] * cW[qz] * det;
+  float w;
+  if constexpr (CACHED) {
+    const float* G = S + L::oGQ;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Ji[k][j] = G[(3 * k + j) * 64 + q];
+    w = G[9 * 64 + q];
+  } else {
+    float J[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) J[i][j] = F[i][1 + j];
+    const float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const float c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const float c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    const float det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    const float id = 1.0f / det;
+    Ji[0][0] = c00 * id;
+    Ji[1][0] = c01 * id;
+    Ji[2][0] = c02 * id;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+    w = cW[qx] * cW[qy] * cW[qz] * det;
+  }
   float v[3], gv[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    v[i] = F[4 + i][0];
+    v[i] = F[FO + 1 + i][0];
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      gv[i][j] = F[4 + i][1] * Ji[0][j] + F[4 + i][2] * Ji[1][j] + F[4 + i][3] * Ji[2][j];
+      gv[i][j] = F[FO + 1 + i][1] * Ji[0][j] + F[FO + 1 + i][2] * Ji[1][j] + F[FO + 1 + i][3] * Ji[2][j];
   }
   float conv[3];
 #pragma unroll
@@ -180,13 +221,13 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #define CFW(arr) CF[(arr) * kCFS + q]
   const float ik = A.ik;
   if constexpr (MODE == MODE_OPERATOR) {
-    const float p = F[3][0];
+    const float p = F[FO][0];
     // Q1 (pi) fields: trilinear in the vertex values, at this Gauss point
     const float lx1 = cX[qx], ly1 = cX[qy], lz1 = cX[qz];
     float PQ[4][4];  // [p, vx, vy, vz][val, d/dxi, d/deta, d/dzeta]
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
-      const float* uf = S + oU + (3 + f) * 27;
+      const float* uf = S + oU + (FO + f) * 27;
       float a[2][2], ax[2][2];
 #pragma unroll
       for (int vz = 0; vz < 2; ++vz)
@@ -209,7 +250,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
       PQ[f][3] = b[1] - b[0];
     }
     // physical gradient of the pressure fluctuation p - pi p
-    const float dd0 = F[3][1] - PQ[0][1], dd1 = F[3][2] - PQ[0][2], dd3 = F[3][3] - PQ[0][3];
+    const float dd0 = F[FO][1] - PQ[0][1], dd1 = F[FO][2] - PQ[0][2], dd3 = F[FO][3] - PQ[0][3];
     float gdp[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) gdp[j] = dd0 * Ji[0][j] + dd1 * Ji[1][j] + dd3 * Ji[2][j];
@@ -264,38 +305,43 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #undef CFW
 }
 
-template <int MODE>
+template <int MODE, bool CACHED>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(ResidualArgs A) {
+  using L = KLay<CACHED>;
+  constexpr int NF = L::NF;
   extern __shared__ __align__(16) float smem[];
   const int wib = threadIdx.x >> 5;
   const int t = threadIdx.x & 31;
-  float* S = smem + wib * kCellFloats;
+  float* S = smem + wib * L::kFloats;
   const int stride = gridDim.x * kWarpsPerBlock;
   int c = blockIdx.x * kWarpsPerBlock + wib;
   NodeRaw raw;
   int idx_next = 0;  // node index of cell c + stride (lane t < 27)
   if (c < A.n_cells) {
     const int node = t < 27 ? __ldg(A.cell_nodes + (int64_t)c * 27 + t) : 0;
-    load_raw(A, c, node, t, raw);
+    load_raw<CACHED>(A, c, node, t, raw);
     if (c + stride < A.n_cells && t < 27) idx_next = __ldg(A.cell_nodes + (int64_t)(c + stride) * 27 + t);
+    if constexpr (CACHED) stage_geo(A, c, t, S + L::oGQ);
   }
 
   for (; c < A.n_cells; c += stride) {
     // ---------------- gather (prefetched one cell ahead), stab ----------------
     float vsq = 0.f;  // |v|^2 of this lane's node; vmax = sqrt(max |v|^2) (sqrt is monotone)
     if (t < 27) {
-      S[oU + 0 * 27 + t] = float(raw.X[0] - raw.X0[0]);
-      S[oU + 1 * 27 + t] = float(raw.X[1] - raw.X0[1]);
-      S[oU + 2 * 27 + t] = float(raw.X[2] - raw.X0[2]);
-      S[oU + 3 * 27 + t] = raw.xv.x;
-      S[oU + 4 * 27 + t] = raw.xv.y;
-      S[oU + 5 * 27 + t] = raw.xv.z;
-      S[oU + 6 * 27 + t] = raw.xv.w;
+      if constexpr (!CACHED) {
+        S[oU + 0 * 27 + t] = float(raw.X[0] - raw.X0[0]);
+        S[oU + 1 * 27 + t] = float(raw.X[1] - raw.X0[1]);
+        S[oU + 2 * 27 + t] = float(raw.X[2] - raw.X0[2]);
+      }
+      S[oU + (L::FO + 0) * 27 + t] = raw.xv.x;
+      S[oU + (L::FO + 1) * 27 + t] = raw.xv.y;
+      S[oU + (L::FO + 2) * 27 + t] = raw.xv.z;
+      S[oU + (L::FO + 3) * 27 + t] = raw.xv.w;
       vsq = raw.xv.y * raw.xv.y + raw.xv.z * raw.xv.z + raw.xv.w * raw.xv.w;
     }
     const float hT = raw.hT;
     if (c + stride < A.n_cells) {  // issue the loads of the next cell (consumed next iteration)
-      load_raw(A, c + stride, idx_next, t, raw);
+      load_raw<CACHED>(A, c + stride, idx_next, t, raw);
       if (c + 2 * stride < A.n_cells && t < 27)
         idx_next = __ldg(A.cell_nodes + (int64_t)(c + 2 * stride) * 27 + t);
     }
@@ -316,8 +362,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     // ---------------- forward x and y in registers: lane (f, qx) ----------------
     // x stage for this qx on the 9 (iz, iy) lines of field f, then the y stage for all four
     // qy -> sy[f][kind*3 + iz][qy*4 + qx]; kind 0 = B_x B_y, 1 = B_x D_y, 2 = D_x B_y
-    if (t < 4 * kNF) {
-      const int f = t >> 2, qx = t & 3;
+    // (cached form: 4 fields x 4 qx x 2 halves of qy -> all 32 lanes)
+    constexpr int QYH = CACHED ? 2 : 4;  // qy per lane
+    if (t < (CACHED ? 32 : 4 * NF)) {
+      const int f = CACHED ? t >> 3 : t >> 2, qx = CACHED ? (t >> 1) & 3 : t & 3;
+      const int qy0 = CACHED ? 2 * (t & 1) : 0;
       const float* u = S + oU + f * 27;
       const float bx0 = cB[qx][0], bx1 = cB[qx][1], bx2 = cB[qx][2];
       const float dx0 = cD[qx][0], dx1 = cD[qx][1], dx2 = cD[qx][2];
@@ -332,7 +381,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         }
       float* dst = S + oSY + f * kSYF + qx;
 #pragma unroll
-      for (int qy = 0; qy < 4; ++qy) {
+      for (int qq = 0; qq < QYH; ++qq) {
+        const int qy = qy0 + qq;
 #pragma unroll
         for (int iz = 0; iz < 3; ++iz) {
           dst[(0 + iz) * 16 + 4 * qy] =
@@ -348,9 +398,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     // ---------------- forward z + pointwise: Gauss points q = t and t + 32 (same qy, qx) ----------------
     {
       const int yx = t & 15, qz = t >> 4;  // second point: qz + 2
-      float F[kNF][4], G[kNF][4];
+      float F[NF][4], G[NF][4];
 #pragma unroll
-      for (int f = 0; f < kNF; ++f) {
+      for (int f = 0; f < NF; ++f) {
         const float* src = S + oSY + f * kSYF + yx;  // [(kind*3 + iz)*16]
         const float vv0 = src[0], vv1 = src[16], vv2 = src[32];
         const float vd0 = src[48], vd1 = src[64], vd2 = src[80];
@@ -370,10 +420,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
           G[f][3] = cD[qz + 2][0] * vv0 + cD[qz + 2][1] * vv1 + cD[qz + 2][2] * vv2;
         }
       }
-      pointwise<MODE>(A, S, S + oCF, t, F, aT, dT);
-      pointwise<MODE>(A, S, S + oCF, t + 32, G, aT, dT);
+      if constexpr (CACHED) {  // this cell's geometry block (staged one cell ahead)
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+      }
+      pointwise<MODE, CACHED>(A, S, S + L::oCF, t, F, aT, dT);
+      pointwise<MODE, CACHED>(A, S, S + L::oCF, t + 32, G, aT, dT);
     }
     __syncwarp();
+    if constexpr (CACHED) {
+      if (c + stride < A.n_cells) stage_geo(A, c + stride, t, S + L::oGQ);
+    }
     // ---------------- backward x, y, z in registers: lane (cp, qz), cp = (comp, part) ----------------
     // tz[cp][iz][iy][ix] = sum_q test(q; ix, iy, iz) . coefficients(cp, q).  Each of the 32
     // lanes contracts the four (qy) lines of one qz plane for all three ix (x stage), then qy
@@ -387,8 +444,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       const int comp = cp >> 1, part = cp & 1;
       // part 0: A_c, B_c0..2; part 1: comp 0 -> B_00..02, comps 1..3 -> P_(c-1)0..2; part 1 has
       // no value test and enters with a minus sign
-      const float* c0 = S + oCF + (CA + comp) * kCFS + 16 * qz;
-      const float* c1 = S + oCF +
+      const float* c0 = S + L::oCF + (CA + comp) * kCFS + 16 * qz;
+      const float* c1 = S + L::oCF +
                         (part == 0 || comp == 0 ? CB + 3 * comp : CP + 3 * (comp - 1)) * kCFS +
                         16 * qz;
       const float* c2 = c1 + kCFS;
@@ -566,27 +623,127 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
   A.convection = ph->convection;
   A.mode = mode;
   A.elem = reinterpret_cast<float4*>(elem);
-  const size_t smem = sizeof(float) * kCellFloats * kWarpsPerBlock;
+  A.geo_q = lv->geo_q;
+  if (lv->n_cells == 0) return DNNMG_OK;
+  const bool cached = lv->geo_q != nullptr;
+  const size_t smem =
+      sizeof(float) * (cached ? KLay<true>::kFloats : KLay<false>::kFloats) * kWarpsPerBlock;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(element_kernel<MODE_OPERATOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(element_kernel<MODE_RHS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(element_kernel<MODE_OPERATOR, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * KLay<false>::kFloats * kWarpsPerBlock));
+    cudaFuncSetAttribute(element_kernel<MODE_RHS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * KLay<false>::kFloats * kWarpsPerBlock));
+    cudaFuncSetAttribute(element_kernel<MODE_OPERATOR, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * KLay<true>::kFloats * kWarpsPerBlock));
+    cudaFuncSetAttribute(element_kernel<MODE_RHS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * KLay<true>::kFloats * kWarpsPerBlock));
     configured = true;
   }
   int blocks = (lv->n_cells + kWarpsPerBlock - 1) / kWarpsPerBlock;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel<MODE_OPERATOR>,
-                                                32 * kWarpsPerBlock, smem);
+  if (cached)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel<MODE_OPERATOR, true>,
+                                                  32 * kWarpsPerBlock, smem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel<MODE_OPERATOR, false>,
+                                                  32 * kWarpsPerBlock, smem);
   const int cap = kSMs * (per_sm > 0 ? per_sm : 1);
   if (blocks > cap) blocks = cap;
-  if (lv->n_cells == 0) return DNNMG_OK;
-  if (mode == MODE_OPERATOR)
-    element_kernel<MODE_OPERATOR><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
-  else
-    element_kernel<MODE_RHS><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+  if (mode == MODE_OPERATOR) {
+    if (cached)
+      element_kernel<MODE_OPERATOR, true><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+    else
+      element_kernel<MODE_OPERATOR, false><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+  } else {
+    if (cached)
+      element_kernel<MODE_RHS, true><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+    else
+      element_kernel<MODE_RHS, false><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+  }
   DNNMG_CHECK_LAUNCH("element_kernel");
+  return DNNMG_OK;
+}
+
+// ---- per-mesh geometry cache: J^-1 and w at every (cell, Gauss point) -----------------
+// Evaluated once per level in fp64 from the 27 cell nodes (isoparametric Q2 map,
+// assembly.py:77-90) and stored in fp32 as [cell][10][64]: (J^-1)[k][j] row-major, then
+// w = w_hat(q) det J.  The reference keeps the equivalent G tables (GeometryCache).
+__constant__ double dB[4][3] = {{tab::phi(0, tab::xg[0]), tab::phi(1, tab::xg[0]), tab::phi(2, tab::xg[0])},
+                                {tab::phi(0, tab::xg[1]), tab::phi(1, tab::xg[1]), tab::phi(2, tab::xg[1])},
+                                {tab::phi(0, tab::xg[2]), tab::phi(1, tab::xg[2]), tab::phi(2, tab::xg[2])},
+                                {tab::phi(0, tab::xg[3]), tab::phi(1, tab::xg[3]), tab::phi(2, tab::xg[3])}};
+__constant__ double dD[4][3] = {{tab::dphi(0, tab::xg[0]), tab::dphi(1, tab::xg[0]), tab::dphi(2, tab::xg[0])},
+                                {tab::dphi(0, tab::xg[1]), tab::dphi(1, tab::xg[1]), tab::dphi(2, tab::xg[1])},
+                                {tab::dphi(0, tab::xg[2]), tab::dphi(1, tab::xg[2]), tab::dphi(2, tab::xg[2])},
+                                {tab::dphi(0, tab::xg[3]), tab::dphi(1, tab::xg[3]), tab::dphi(2, tab::xg[3])}};
+__constant__ double dW[4] = {tab::wg[0], tab::wg[1], tab::wg[2], tab::wg[3]};
+
+__global__ void __launch_bounds__(128) geometry_kernel(int n_cells, const int32_t* __restrict__ cn,
+                                                       const double* __restrict__ coords,
+                                                       float* __restrict__ geo) {
+  __shared__ double X[4][27][3];
+  const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
+  for (int c = blockIdx.x * 4 + w; c < n_cells; c += gridDim.x * 4) {
+    if (t < 27) {
+      const int n = __ldg(cn + (int64_t)c * 27 + t), n0 = __ldg(cn + (int64_t)c * 27);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) X[w][t][i] = __ldg(coords + 3 * (int64_t)n + i) - __ldg(coords + 3 * (int64_t)n0 + i);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+      const int q = t + 32 * k, qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
+      double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // J[i][m] = dX_i / dxi_m
+      for (int a = 0; a < 27; ++a) {
+        const int ax = a % 3, ay = (a / 3) % 3, az = a / 9;
+        const double g0 = dD[qx][ax] * dB[qy][ay] * dB[qz][az];
+        const double g1 = dB[qx][ax] * dD[qy][ay] * dB[qz][az];
+        const double g2 = dB[qx][ax] * dB[qy][ay] * dD[qz][az];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double xi = X[w][a][i];
+          J[i][0] = fma(xi, g0, J[i][0]);
+          J[i][1] = fma(xi, g1, J[i][1]);
+          J[i][2] = fma(xi, g2, J[i][2]);
+        }
+      }
+      const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+      const double id = 1.0 / det;
+      double Ji[3][3];
+      Ji[0][0] = c00 * id;
+      Ji[1][0] = c01 * id;
+      Ji[2][0] = c02 * id;
+      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+      float* gq = geo + (int64_t)c * 640 + q;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) gq[(3 * kk + j) * 64] = (float)Ji[kk][j];
+      gq[9 * 64] = (float)(dW[qx] * dW[qy] * dW[qz] * det);
+    }
+    __syncwarp();
+  }
+}
+
+int32_t launch_level_geometry(const dnnmg_level_t* lv, float* geo, cudaStream_t s) {
+  DNNMG_REQUIRE(lv && lv->cell_nodes && lv->coords && geo, DNNMG_ERR_ARG,
+                "level_geometry: null argument");
+  DNNMG_REQUIRE(((uintptr_t)geo & 15) == 0, DNNMG_ERR_ARG, "level_geometry: unaligned output");
+  if (lv->n_cells == 0) return DNNMG_OK;
+  geometry_kernel<<<grid_for((lv->n_cells + 3) / 4, 1, 16), 128, 0, s>>>(lv->n_cells, lv->cell_nodes,
+                                                                          lv->coords, geo);
+  DNNMG_CHECK_LAUNCH("geometry_kernel");
   return DNNMG_OK;
 }
 

@@ -174,9 +174,19 @@ class DeviceLevel:
         self.csr_idx = upload(idx, np.int32)
         self.elem = None
 
-    def struct(self, dof_mask=None):
+    def struct(self, dof_mask=None, geometry=False):
         return _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
-                          ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask))
+                          ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask),
+                          ptr(self.geometry()) if geometry else None)
+
+    def geometry(self):
+        """Per-mesh cache of J^-1 and w at every (cell, Gauss point) (2,560 B per cell),
+        computed once in fp64 on the device (the reference's GeometryCache)."""
+        if getattr(self, "geo_q", None) is None:
+            self.geo_q = torch.empty(self.n_cells * 640, dtype=torch.float32, device=device())
+            _lib.call("dnnmg_level_geometry", ctypes.byref(self.struct()), ptr(self.geo_q),
+                      stream_handle())
+        return self.geo_q
 
     def scratch(self):
         if self.elem is None:

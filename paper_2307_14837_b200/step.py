@@ -41,7 +41,8 @@ class CorrectionStep:
         self.level = dv.DeviceLevel.get(self.space)
         self.mask = constrained_mask(self.space, self.bcs) if mask is None else np.asarray(mask)
         self.mask_bits = dv.upload(dv.dof_mask_bits(self.mask, self.space.n_nodes), np.uint8)
-        self.lv = self.level.struct(self.mask_bits)
+        # K2 reads J^-1 and w from the per-mesh geometry cache (the mesh is fixed in time)
+        self.lv = self.level.struct(self.mask_bits, geometry=True)
         self.patchset = patchset if patchset is not None else meshmod.build_patches(hierarchy, L, J)
         check_model(model, self.patchset)
         self.ps = dv.DevicePatchSet.get(self.patchset)
@@ -189,7 +190,7 @@ class CorrectionStep:
     def rhs_next(self, x, out=None):
         """Next-step fine RHS from a (corrected) fine state (assembly.py:242-259)."""
         out = torch.empty_like(self.x_tilde) if out is None else out
-        lv = self.level.struct()
+        lv = self.level.struct(geometry=True)
         _lib.call("dnnmg_rhs_next", ctypes.byref(lv), dv.ptr(x), ctypes.byref(self.phys),
                   dv.ptr(self.elem), dv.ptr(out), dv.stream_handle())
         return out

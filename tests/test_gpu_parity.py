@@ -369,3 +369,33 @@ def test_restrict_transpose_pairing():
     Ptb = spmod.restrict_rhs(h, b, 1, 1)
     lhs, rhs = b @ Px, Ptb @ x
     assert abs(lhs - rhs) < 1e-5 * (np.abs(b) @ np.abs(Px) + 1.0), (lhs, rhs)
+
+
+@pytest.mark.parametrize("name", ["cfg0", "jit", "chan"])
+def test_geometry_cache_matches_recomputed(name):
+    """K2 with the per-mesh geometry cache (J^-1, w per Gauss point, fp64 setup) gives the
+    same residual as the path that recomputes the isoparametric geometry per call, and
+    both match the reference."""
+    import ctypes
+    from paper_2307_14837_b200 import _lib, device as dv
+    g = load_golden(name)
+    h = product_hierarchy(g)
+    L, J = int(g["L"]), int(g["J"])
+    s = spmod.FeSpace(h, L + J)
+    lvl = dv.DeviceLevel.get(s)
+    mask = dv.upload(dv.dof_mask_bits(g["mask"], s.n_nodes), np.uint8)
+    xt = torch.tensor(g["x_tilde"], dtype=torch.float32, device="cuda")
+    b = torch.tensor(g["b_prev"], dtype=torch.float32, device="cuda")
+    ph = _lib.Phys(float(g["nu"]), float(g["k"]), float(g["alpha0"]), float(g["delta0"]), 1)
+    out = []
+    for geo in (False, True):
+        lv = lvl.struct(mask, geometry=geo)
+        r = torch.empty_like(xt)
+        _lib.call("dnnmg_residual", ctypes.byref(lv), dv.ptr(xt), dv.ptr(b), None, None,
+                  ctypes.byref(ph), dv.ptr(lvl.scratch()), dv.ptr(r), 1, dv.stream_handle())
+        torch.cuda.synchronize()
+        out.append(r.cpu().numpy().astype(float))
+    assert rel(out[1], out[0]) < 1e-5, rel(out[1], out[0])
+    # the cached geometry is formed in fp64: at least as close to the reference
+    assert rel(out[1], g["r"]) < 2e-5, rel(out[1], g["r"])
+    assert rel(out[1], g["r"]) <= 1.2 * rel(out[0], g["r"]) + 1e-9

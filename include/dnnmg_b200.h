@@ -134,6 +134,16 @@ typedef struct {
   const float* geom;              /* [n_patches][n_geo] */
   const int32_t* node_patch_ptr;  /* [n_nodes+1] CSR node -> (patch*npp + slot), ascending patch */
   const int32_t* node_patch_idx;
+  /* optional (all NULL/0 = absent): distinct nodes of every 128-patch tile of the fused
+   * tensor-core gather.  Tile t's distinct nodes are tile_nodes[t*tile_cap ..
+   * t*tile_cap + tile_count[t]) in ascending id; tile_slot[p*npp + s] is the position of
+   * node_table[p][s] in its tile's list.  With these, the MLP kernel stages each tile's
+   * distinct x~/r rows in shared memory one tile ahead (cp.async from a dedicated warp)
+   * instead of gathering every (patch, slot) from global memory at the tile boundary. */
+  int32_t tile_cap;               /* row stride of tile_nodes (>= max tile_count) */
+  const int32_t* tile_nodes;      /* [n_tiles][tile_cap], n_tiles = ceil(n_patches/128) */
+  const int32_t* tile_count;      /* [n_tiles] */
+  const uint16_t* tile_slot;      /* [n_tiles*128][npp] (rows past n_patches: any valid slot) */
 } dnnmg_patchset_t;
 
 #define DNNMG_MAX_LAYERS 16
@@ -208,6 +218,10 @@ int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, 
 int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
                                   const float* r, float* Y, dnnmg_stream_t stream);
 
+/* Which layer-0 source dnnmg_mlp_forward_patches uses for (m, ps): 1 = direct gather of
+ * every (patch, slot) at the tile boundary, 2 = staged gather of each tile's distinct nodes
+ * (needs ps->tile_* and enough shared memory), -1 = no tensor-core model.  Host only. */
+int32_t dnnmg_mlp_gather_mode(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps);
 /* ---- K5: averaging scatter + correction update ---------------------------------------- */
 /* d = mu * bincount(velocity rows Y); d[mask] = 0; pressure 0; x_corr = x_tilde + scale*d.
  * Y: [n_patches][3*npp].  x_tilde/x_corr may be NULL (then only d is written). */

@@ -44,7 +44,8 @@ class Phys(ctypes.Structure):
 class PatchSet(ctypes.Structure):
     _fields_ = [("n_patches", c_i32), ("nodes_per_patch", c_i32), ("n_geo", c_i32),
                 ("n_nodes", c_i32), ("node_table", c_vp), ("geom", c_vp),
-                ("node_patch_ptr", c_vp), ("node_patch_idx", c_vp)]
+                ("node_patch_ptr", c_vp), ("node_patch_idx", c_vp),
+                ("tile_cap", c_i32), ("tile_nodes", c_vp), ("tile_count", c_vp), ("tile_slot", c_vp)]
 
 
 class Mlp(ctypes.Structure):
@@ -86,6 +87,7 @@ EXPORTS = {
     "dnnmg_mlp_forward": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_i64, c_vp, c_vp]),
     "dnnmg_mlp_forward_patches": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet), c_vp, c_vp,
                                           c_vp, c_vp]),
+    "dnnmg_mlp_gather_mode": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet)]),
     "dnnmg_scatter_update": (c_i32, [ctypes.POINTER(PatchSet), c_vp, c_vp, c_vp, c_f32, c_vp, c_vp,
                                      c_vp]),
     "dnnmg_correction_step": (c_i32, [ctypes.POINTER(Prolong), c_i32, ctypes.POINTER(Dirichlet),

@@ -36,6 +36,7 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t*, void*, cudaStream_t);
 int32_t launch_mlp_tc(const dnnmg_mlp_t*, const float*, int64_t, float*, cudaStream_t);
 int32_t launch_mlp_tc_gather(const dnnmg_mlp_t*, const dnnmg_patchset_t*, const float*,
                              const float*, float*, cudaStream_t);
+int32_t mlp_tc_gather_mode(const dnnmg_mlp_t*, const dnnmg_patchset_t*);
 
 static int32_t check_mlp(const dnnmg_mlp_t* m) {
   DNNMG_REQUIRE(m, DNNMG_ERR_ARG, "mlp: null model");
@@ -171,6 +172,11 @@ int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* 
                 DNNMG_ERR_UNSUPPORTED, "mlp_forward_patches: needs a packed tensor-core model");
   if (ps->n_patches == 0) return DNNMG_OK;
   return launch_mlp_tc_gather(m, ps, x, r, Y, as_stream(s));
+}
+
+int32_t dnnmg_mlp_gather_mode(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps) {
+  if (!m || !ps || !m->packed || m->precision == DNNMG_PREC_FP32 || !mlp_tc_supported(m)) return -1;
+  return mlp_tc_gather_mode(m, ps);
 }
 
 int32_t dnnmg_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const uint8_t* mask,

@@ -38,9 +38,14 @@ namespace dnnmg {
 
 constexpr int kTcM = 128;
 constexpr int kTcH = 256;
-constexpr int kTcThreads = 320;
+constexpr int kTcThreads = 352;
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
+constexpr int kGatherWarp = 10;  // staged fused gather (GM_STAGED): cp.async of a tile's nodes
+// sources of the layer-0 operand
+enum { GM_X = 0,        // rows of a stored X
+       GM_DIRECT = 1,   // fused gather: per-(patch, slot) global loads at the tile boundary
+       GM_STAGED = 2 }; // fused gather: the tile's distinct nodes staged in SMEM one tile ahead
 
 template <int MODE> struct TcCfg;
 // KC: K elements per pipeline chunk (one TMA weight copy, one A-ring stage);
@@ -81,12 +86,18 @@ struct TcArgs {
   const float4* rg;           // r
   const float* geom;          // [n_rows][n_geo]
   int npp, n_geo;
+  // GM_STAGED: distinct nodes per tile (dnnmg_patchset_t.tile_*)
+  int tile_cap;
+  const int32_t* tile_nodes;
+  const int32_t* tile_count;
+  const uint16_t* tile_slot;
   long long* trace;  // debug timeline of CTA 0 (env DNNMG_MLP_TRACE=file), else NULL
 };
+constexpr int kTraceSlots = 12288;
 // timeline probe (tools/mlp_trace.py): one clock64() sample per slot, CTA 0 only
 #define TC_TRACE(slot)                                                              \
   do {                                                                              \
-    if (A.trace && blockIdx.x == 0 && (slot) < 8192) A.trace[(slot)] = clock64();   \
+    if (A.trace && blockIdx.x == 0 && (slot) < kTraceSlots) A.trace[(slot)] = clock64();   \
   } while (0)
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -117,6 +128,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_add_tx(uint32_t bar, uint32_t bytes) {  // no arrival
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
@@ -305,8 +324,15 @@ __device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const 
   }
 }
 
-template <int MODE, bool GATHER>
+// shared-memory bytes of the GM_STAGED staging area: slot block, geometry rows, x~/r rows
+__host__ __device__ inline uint32_t staged_slot_bytes(int npp) { return (kTcM * npp * 2 + 15) / 16 * 16; }
+__host__ __device__ inline uint32_t staged_bytes(int npp, int n_geo, int cap) {
+  return staged_slot_bytes(npp) + kTcM * n_geo * 4 + 2u * 16u * cap;
+}
+
+template <int MODE, int GM>
 __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
+  constexpr bool GATHER = GM != GM_X;
   using C = TcCfg<MODE>;
   constexpr int KC = C::KC;
   constexpr int HC = KC / 2;                       // K columns per thread per chunk
@@ -326,7 +352,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* idx_full = acc_empty + 2;   // fused gather: next tile's node indices staged by TMA
   uint64_t* idx_empty = idx_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(idx_empty + 1);
+  uint64_t* stage_full = idx_empty + 1;   // GM_STAGED: the tile's nodes are in SMEM
+  uint64_t* stage_empty = stage_full + 1; // GM_STAGED: layer 0 consumed them
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stage_empty + 1);
   // BN scale/shift per hidden layer and the input normalisation, staged once per CTA
   float* p_scale = reinterpret_cast<float*>(tmem_slot + 4);
   float* p_shift = p_scale + A.depth * kTcH;
@@ -342,8 +370,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     p_shift[i] = A.shift[i] * k2;
   }
   const float y_unscale = hdr->unscale[A.depth];
-  int32_t* idx_s = reinterpret_cast<int32_t*>(p_rstd + kTcH);  // [kTcM][npp] (GATHER only)
-  float* y_stage = p_rstd + kTcH + (GATHER ? kTcM * A.npp : 0);
+  int32_t* idx_s = reinterpret_cast<int32_t*>(p_rstd + kTcH);  // [kTcM][npp] (GM_DIRECT only)
+  // GM_STAGED: slot block [kTcM][npp] u16 | geometry rows [kTcM][n_geo] | x~ [cap] | r [cap]
+  uint8_t* st_base = reinterpret_cast<uint8_t*>(p_rstd + kTcH);
+  const uint16_t* slot_s = reinterpret_cast<const uint16_t*>(st_base);
+  float4* geo_s = reinterpret_cast<float4*>(st_base + staged_slot_bytes(A.npp));
+  float4* stx = geo_s + kTcM * A.n_geo / 4;
+  float4* str = stx + A.tile_cap;
+  float* y_stage = reinterpret_cast<float*>(
+      st_base + (GM == GM_DIRECT ? kTcM * A.npp * 4
+                                 : GM == GM_STAGED ? staged_bytes(A.npp, A.n_geo, A.tile_cap) : 0));
   for (int i = threadIdx.x; i < kTcH; i += blockDim.x) {
     p_mean[i] = i < A.n_in ? A.in_mean[i] : 0.f;
     p_rstd[i] = i < A.n_in ? 1.0f / A.in_std[i] : 0.f;
@@ -369,6 +405,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     }
     mbar_init(smem_u32(idx_full), 1);
     mbar_init(smem_u32(idx_empty), 8);
+    mbar_init(smem_u32(stage_full), 1);
+    mbar_init(smem_u32(stage_empty), 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kProducerWarp) {
@@ -392,7 +430,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       auto full_tile = [&](int64_t t) { return t < n_tiles && (t + 1) * kTcM <= A.n_rows; };
       uint32_t icopy = 0;
       auto stage_idx = [&](int64_t t) {
-        if (!GATHER || !full_tile(t) || (idx_bytes & 15)) return;
+        if (GM != GM_DIRECT || !full_tile(t) || (idx_bytes & 15)) return;
         if (icopy > 0) mbar_wait(smem_u32(idx_empty), (icopy - 1) & 1);
         mbar_expect_tx(smem_u32(idx_full), idx_bytes);
         bulk_g2s(smem_u32(idx_s), A.node_table + t * kTcM * A.npp, idx_bytes, smem_u32(idx_full));
@@ -460,6 +498,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         }
       }
     }
+  } else if (warp == kGatherWarp) {
+    // ---------------- staged gather (GM_STAGED) ----------------
+    // Tile t's distinct x~ and r rows (cp.async, 16 B each), its slot block and its geometry
+    // rows (bulk copies) land in SMEM while the compute warps run tile t - grid; the
+    // layer-0 operand of tile t is then built from SMEM (patch_ops.py:49-53).
+    if constexpr (GM == GM_STAGED) {
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        if (it > 0) mbar_wait(smem_u32(stage_empty), (it - 1) & 1);
+        const int64_t r0 = tile * kTcM;
+        const int nvalid = (int)((A.n_rows - r0) < kTcM ? (A.n_rows - r0) : kTcM);
+        if (lane == 0) {
+          const uint32_t sb = (uint32_t)kTcM * A.npp * 2, gb = (uint32_t)nvalid * A.n_geo * 4;
+          mbar_add_tx(smem_u32(stage_full), sb + gb);
+          bulk_g2s(smem_u32(slot_s), A.tile_slot + r0 * A.npp, sb, smem_u32(stage_full));
+          bulk_g2s(smem_u32(geo_s), A.geom + r0 * A.n_geo, gb, smem_u32(stage_full));
+        }
+        const int cnt = __ldg(A.tile_count + tile);
+        const int32_t* un = A.tile_nodes + tile * A.tile_cap;
+        for (int i0 = 0; i0 < cnt; i0 += 32 * 8) {
+          int u[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int i = i0 + 32 * k + lane;
+            u[k] = i < cnt ? __ldg(un + i) : -1;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int i = i0 + 32 * k + lane;
+            if (u[k] >= 0) {
+              cp_async16(stx + i, A.xg + u[k]);
+              cp_async16(str + i, A.rg + u[k]);
+            }
+          }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(stage_full));
+      }
+    }
   } else {
     // ---------------- compute warps ----------------
     const int quad = warp & 3;          // TMEM lane quadrant
@@ -473,6 +551,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     auto produce_chunk = [&](int c, const float* v) {
       const int s = aitem % C::NA;
       mbar_wait(smem_u32(&a_empty[s]), ((aitem / C::NA) & 1) ^ 1);
+      if (warp == 0 && lane == 0) TC_TRACE(8192 + aitem);
       put_row<MODE>(aring + s * AST, row_in_tile, HC * hh, v);
       fence_async_smem();
       __syncwarp();
@@ -492,7 +571,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       const bool from_smem = idx_staged && tile < n_tiles && (tile + 1) * kTcM <= A.n_rows;
       if (from_smem) mbar_wait(smem_u32(idx_full), iload & 1);
       const bool ok = tile < n_tiles && row < A.n_rows;
-      if constexpr (GATHER) {
+      if constexpr (GM == GM_DIRECT) {
         // fused gather (patch_ops.py:49-53): float4 slot s of the row is x~ of node s,
         // r of node s - npp, or geometry; indices first, then all value loads in flight
         const int32_t* nt = A.node_table + row * A.npp;
@@ -572,8 +651,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         }
       }
     };
-    load_x(blockIdx.x);
-    produce_layer0();
+    // GM_STAGED: layer-0 operand of `tile` from the staged nodes (gather warp)
+    uint32_t sit = 0;
+    auto produce_layer0_staged = [&](int64_t tile) {
+      mbar_wait(smem_u32(stage_full), sit & 1);
+      if (warp == 0 && lane == 0) TC_TRACE(6915 + 4 * (int)sit);
+      const bool ok = tile * kTcM + row_in_tile < A.n_rows;
+      const uint16_t* sl = slot_s + row_in_tile * A.npp;
+      const float4* gr = geo_s + row_in_tile * (A.n_geo / 4);
+      const int geo4 = A.n_geo / 4;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (c < nck0) {
+          float v[HC];
+#pragma unroll
+          for (int j = 0; j < HC / 4; ++j) {
+            const int f4 = (KC / 4) * c + (HC / 4) * hh + j;
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) {
+              if (f4 < A.npp) x = stx[sl[f4]];
+              else if (f4 < 2 * A.npp) x = str[sl[f4 - A.npp]];
+              else if (f4 < 2 * A.npp + geo4) x = gr[f4 - 2 * A.npp];
+            }
+            const int col = c * KC + HC * hh + 4 * j;
+            v[4 * j + 0] = (x.x - p_mean[col + 0]) * p_rstd[col + 0];
+            v[4 * j + 1] = (x.y - p_mean[col + 1]) * p_rstd[col + 1];
+            v[4 * j + 2] = (x.z - p_mean[col + 2]) * p_rstd[col + 2];
+            v[4 * j + 3] = (x.w - p_mean[col + 3]) * p_rstd[col + 3];
+          }
+          produce_chunk(c, v);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(stage_empty));
+      ++sit;
+    };
+    if constexpr (GM == GM_STAGED) {
+      produce_layer0_staged(blockIdx.x);
+    } else {
+      load_x(blockIdx.x);
+      produce_layer0();
+    }
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int64_t row = tile * kTcM + row_in_tile;
@@ -628,11 +746,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       }
       // the skip state is dead now: prefetch the next tile's input under the head GEMM
       if (warp == 0 && lane == 0) TC_TRACE(6912 + (int)((tile - blockIdx.x) / gridDim.x) * 4);
-      load_x(tile + gridDim.x);
+      if constexpr (GM != GM_STAGED) load_x(tile + gridDim.x);
       if (warp == 0 && lane == 0) TC_TRACE(6913 + (int)((tile - blockIdx.x) / gridDim.x) * 4);
       // the next tile's layer-0 operand goes into the ring right behind this tile's head
       // chunks: the MMA warp runs it while this tile's head epilogue is in progress
-      if (tile + gridDim.x < n_tiles) produce_layer0();
+      if (tile + gridDim.x < n_tiles) {
+        if constexpr (GM == GM_STAGED) produce_layer0_staged(tile + gridDim.x);
+        else produce_layer0();
+      }
       // head: Y = h W_depth
       {
         const int buf = j & 1;
@@ -825,7 +946,36 @@ struct GatherSrc {
   const float* r;
   const float* geom;
   int npp, n_geo;
+  int tile_cap;
+  const int32_t* tile_nodes;
+  const int32_t* tile_count;
+  const uint16_t* tile_slot;
 };
+constexpr size_t kSmemMax = 227 * 1024;
+
+template <int MODE>
+static size_t smem_base(const dnnmg_mlp_t* m) {
+  using C = TcCfg<MODE>;
+  constexpr int WST = kTcH * C::KC * C::ESZ * C::PARTS;
+  constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
+  return (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 8) + 16 +
+         sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
+}
+static size_t smem_base_of(const dnnmg_mlp_t* m) {
+  return m->precision == DNNMG_PREC_BF16 ? smem_base<DNNMG_PREC_BF16>(m)
+         : m->precision == DNNMG_PREC_F16X3 ? smem_base<DNNMG_PREC_F16X3>(m)
+                                            : smem_base<DNNMG_PREC_TF32X3>(m);
+}
+// layer-0 source: staged gather when the tile tables exist and the staging area fits next
+// to the rings (env DNNMG_NO_STAGED forces the direct gather, for A/B measurements)
+static int choose_gm(const dnnmg_mlp_t* m, const GatherSrc* g) {
+  if (!g) return GM_X;
+  if (g->tile_nodes && g->tile_count && g->tile_slot && g->tile_cap > 0 &&
+      smem_base_of(m) + staged_bytes(g->npp, g->n_geo, g->tile_cap) <= kSmemMax &&
+      !getenv("DNNMG_NO_STAGED"))
+    return GM_STAGED;
+  return GM_DIRECT;
+}
 
 template <int MODE>
 static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
@@ -839,12 +989,16 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.geom = g ? g->geom : nullptr;
   A.npp = g ? g->npp : 0;
   A.n_geo = g ? g->n_geo : 0;
+  A.tile_cap = g ? g->tile_cap : 0;
+  A.tile_nodes = g ? g->tile_nodes : nullptr;
+  A.tile_count = g ? g->tile_count : nullptr;
+  A.tile_slot = g ? g->tile_slot : nullptr;
   A.Y = Y;
   A.trace = nullptr;
   static const char* trace_file = getenv("DNNMG_MLP_TRACE");
   if (trace_file) {
-    cudaMalloc(&A.trace, 8192 * sizeof(long long));
-    cudaMemsetAsync(A.trace, 0, 8192 * sizeof(long long), s);
+    cudaMalloc(&A.trace, kTraceSlots * sizeof(long long));
+    cudaMemsetAsync(A.trace, 0, kTraceSlots * sizeof(long long), s);
   }
   A.n_rows = n_rows;
   A.n_in = m->n_in;
@@ -862,11 +1016,12 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.in_std = m->in_std;
   constexpr int WST = kTcH * C::KC * C::ESZ * C::PARTS;
   constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
-  size_t smem = (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 6) + 16 +
-                (g ? (size_t)kTcM * g->npp * 4 : 0) +
-                sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
+  const size_t base = smem_base<MODE>(m);
+  const int gm = choose_gm(m, g);
+  size_t smem = base + (gm == GM_DIRECT ? (size_t)kTcM * g->npp * 4
+                        : gm == GM_STAGED ? staged_bytes(g->npp, g->n_geo, g->tile_cap) : 0);
   const size_t ybytes = (size_t)(kTcM / 2) * m->n_out * 4;  // staged in two 64-row halves
-  if (smem + ybytes <= 225 * 1024) {
+  if (smem + ybytes <= kSmemMax && !getenv("DNNMG_Y_DIRECT")) {
     A.y_mode = 2;
     smem += ybytes;
   } else {
@@ -875,18 +1030,22 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: TMEM (512 columns) is per SM
   const int64_t tiles = (n_rows + kTcM - 1) / kTcM;
   const int grid = (int)(tiles < kSMs ? tiles : kSMs);
-  if (g) {
-    cudaFuncSetAttribute(mlp_tc_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (gm == GM_STAGED) {
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    mlp_tc_kernel<MODE, true><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_STAGED><<<grid, kTcThreads, smem, s>>>(A);
+  } else if (gm == GM_DIRECT) {
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    mlp_tc_kernel<MODE, GM_DIRECT><<<grid, kTcThreads, smem, s>>>(A);
   } else {
-    cudaFuncSetAttribute(mlp_tc_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_X>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    mlp_tc_kernel<MODE, false><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_X><<<grid, kTcThreads, smem, s>>>(A);
   }
   DNNMG_CHECK_LAUNCH("mlp_tc_kernel");
   if (A.trace) {  // debug only: synchronous copy-out of CTA 0's timeline
-    static long long host[8192];
+    static long long host[kTraceSlots];
     cudaMemcpyAsync(host, A.trace, sizeof(host), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     cudaFree(A.trace);
@@ -907,12 +1066,19 @@ int32_t launch_mlp_tc(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, floa
 
 // K3 fused into K4: the network input rows are gathered from x~, r and the patch
 // geometry while staging the layer-0 operand; X never touches HBM
+int32_t mlp_tc_gather_mode(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps) {
+  GatherSrc g{ps->node_table, nullptr,      nullptr,        ps->geom,      ps->nodes_per_patch,
+              ps->n_geo,      ps->tile_cap, ps->tile_nodes, ps->tile_count, ps->tile_slot};
+  return choose_gm(m, &g);
+}
+
 int32_t launch_mlp_tc_gather(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
                              const float* r, float* Y, cudaStream_t s) {
   DNNMG_REQUIRE(ps->n_geo % 4 == 0 && 8 * ps->nodes_per_patch + ps->n_geo == m->n_in &&
                     m->n_in <= kTcH,
                 DNNMG_ERR_UNSUPPORTED, "mlp_gather: needs 8*npp + n_geo == n_in <= 256");
-  GatherSrc g{ps->node_table, x, r, ps->geom, ps->nodes_per_patch, ps->n_geo};
+  GatherSrc g{ps->node_table, x,         r,        ps->geom,      ps->nodes_per_patch, ps->n_geo,
+              ps->tile_cap,   ps->tile_nodes, ps->tile_count, ps->tile_slot};
   if (m->precision == DNNMG_PREC_BF16)
     return launch_mode<DNNMG_PREC_BF16>(m, nullptr, ps->n_patches, Y, s, &g);
   if (m->precision == DNNMG_PREC_F16X3)

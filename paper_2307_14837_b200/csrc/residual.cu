@@ -519,26 +519,32 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     }
     __syncwarp();
     // ---------------- output: direct + PI^T * (LPS part), one float4 per node ----------------
-    if (t < 27) {
+    // PI[b][t] != 0 only for vertices t and the 8 nodes b with b_k in {t_k, 1} (weight 1/2 per
+    // mid index): lane (comp, vertex) = (t >> 3, t & 7) forms one PI^T sum, and the node lanes
+    // pick their four components up by shuffle
+    float lps = 0.f;
+    if constexpr (MODE == MODE_OPERATOR) {
+      const int comp = t >> 3, v = t & 7;
+      const int it0 = (v & 1) ? 2 : 0, it1 = (v & 2) ? 2 : 0, it2 = (v & 4) ? 2 : 0;
+      const float* gp = S + oTZ + (comp * 2 + 1) * 27;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int b0 = (m & 1) ? 1 : it0, b1 = (m & 2) ? 1 : it1, b2 = (m & 4) ? 1 : it2;
+        const float wgt = ((m & 1) ? 0.5f : 1.f) * ((m & 2) ? 0.5f : 1.f) * ((m & 4) ? 0.5f : 1.f);
+        lps = fmaf(wgt, gp[b0 + 3 * b1 + 9 * b2], lps);
+      }
+    }
+    {
+      const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
+      const bool vtx = MODE == MODE_OPERATOR && t < 27 && it0 != 1 && it1 != 1 && it2 != 1;
+      const int vid = (it0 >> 1) + 2 * (it1 >> 1) + 4 * (it2 >> 1);
       float e[4];
 #pragma unroll
-      for (int comp = 0; comp < 4; ++comp) e[comp] = S[oTZ + (comp * 2) * 27 + t];
-      const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
-      if (MODE == MODE_OPERATOR && it0 != 1 && it1 != 1 && it2 != 1) {
-        // vertex: PI[b][t] != 0 only for the 8 nodes b with b_k in {t_k, 1} (weight 1/2
-        // per mid index)
-#pragma unroll
-        for (int comp = 0; comp < 4; ++comp) {
-          const float* gp = S + oTZ + (comp * 2 + 1) * 27;
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const int b0 = (m & 1) ? 1 : it0, b1 = (m & 2) ? 1 : it1, b2 = (m & 4) ? 1 : it2;
-            const float wgt = ((m & 1) ? 0.5f : 1.f) * ((m & 2) ? 0.5f : 1.f) * ((m & 4) ? 0.5f : 1.f);
-            e[comp] = fmaf(wgt, gp[b0 + 3 * b1 + 9 * b2], e[comp]);
-          }
-        }
+      for (int comp = 0; comp < 4; ++comp) {
+        const float l = __shfl_sync(0xffffffffu, lps, comp * 8 + (vid & 7));
+        e[comp] = t < 27 ? S[oTZ + (comp * 2) * 27 + t] + (vtx ? l : 0.f) : 0.f;
       }
-      A.elem[(int64_t)c * 27 + t] = make_float4(e[0], e[1], e[2], e[3]);
+      if (t < 27) A.elem[(int64_t)c * 27 + t] = make_float4(e[0], e[1], e[2], e[3]);
     }
     __syncwarp();
   }

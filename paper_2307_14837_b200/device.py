@@ -70,6 +70,41 @@ def node_csr(table):
     return ptr_, order
 
 
+TILE_ROWS = 128  # patches per tensor-core MLP tile (kTcM in csrc/mlp_tc.cu)
+
+
+def tile_tables(table, rows=TILE_ROWS):
+    """Distinct nodes of every `rows`-patch tile of a node table, for the staged fused
+    gather of the MLP kernel: (cap, nodes [n_tiles][cap] int32 ascending, count [n_tiles],
+    slot [n_tiles*rows][npp] uint16 with nodes[t][slot[p][s]] == table[p][s]).  Rows past
+    the last patch repeat the last row.  Returns None when a tile has more than 65535
+    distinct nodes (not representable in uint16)."""
+    table = np.asarray(table, dtype=np.int64)
+    n, npp = table.shape
+    if n == 0:
+        return None
+    T = (n + rows - 1) // rows
+    pad = T * rows - n
+    a = np.concatenate([table, np.repeat(table[-1:], pad, 0)]) if pad else table
+    a = a.reshape(T, rows * npp)
+    order = np.argsort(a, axis=1, kind="stable")
+    srt = np.take_along_axis(a, order, 1)
+    first = np.ones(srt.shape, dtype=bool)
+    first[:, 1:] = srt[:, 1:] != srt[:, :-1]
+    rank = np.cumsum(first, axis=1) - 1
+    count = rank[:, -1] + 1
+    if count.max() > 65535:
+        return None
+    cap = int((count.max() + 7) // 8 * 8)
+    nodes = np.zeros((T, cap), dtype=np.int32)
+    ti, pos = np.nonzero(first)
+    nodes[ti, rank[ti, pos]] = srt[ti, pos]
+    nodes[:, :] = np.where(np.arange(cap)[None, :] < count[:, None], nodes, nodes[:, :1])
+    slot = np.empty_like(rank)
+    np.put_along_axis(slot, order, rank, 1)
+    return cap, nodes, count.astype(np.int32), slot.reshape(T * rows, npp).astype(np.uint16)
+
+
 def dof_mask_bits(mask, n_nodes):
     """bool dof mask -> per-node bit field (bit c <=> dof 4n+c constrained)."""
     if mask is None:
@@ -216,9 +251,19 @@ class DevicePatchSet:
             raise RuntimeError("patch union does not cover the fine level")
         self.csr_ptr = upload(p, np.int32)
         self.csr_idx = upload(idx, np.int32)
+        tt = tile_tables(ps.node_table)
+        self.tile_cap = 0
+        self.tile_nodes = self.tile_count = self.tile_slot = None
+        if tt is not None:
+            self.tile_cap = tt[0]
+            self.tile_nodes = upload(tt[1], np.int32)
+            self.tile_count = upload(tt[2], np.int32)
+            # uint16 has no torch dtype on every build: ship the raw bytes as int16
+            self.tile_slot = upload(tt[3].view(np.int16), np.int16)
         self.struct = _lib.PatchSet(self.n_patches, self.npp, self.n_geo, self.n_nodes,
                                     ptr(self.node_table), ptr(self.geom), ptr(self.csr_ptr),
-                                    ptr(self.csr_idx))
+                                    ptr(self.csr_idx), self.tile_cap, ptr(self.tile_nodes),
+                                    ptr(self.tile_count), ptr(self.tile_slot))
 
     @staticmethod
     def get(ps):

@@ -127,3 +127,20 @@ def test_prolongation_reproduces_quadratics():
 def test_non_box_templates_rejected():
     with pytest.raises(NotImplementedError):
         meshmod.build_template_mesh("channel_cylinder_3d")
+
+
+def test_tile_tables_cover_node_table():
+    """Per-tile distinct-node tables of the staged fused gather (device.tile_tables):
+    nodes[t][slot[p][s]] == node_table[p][s], lists ascending and duplicate-free."""
+    from paper_2307_14837_b200 import device as dv
+    h = meshmod.build_template_mesh("box", extent_lo=(0, 0, 0), extent_hi=(1, 1, 1),
+                                    n_cells=(5, 4, 3))
+    meshmod.refine_uniform(h)
+    nt = np.asarray(meshmod.build_patches(h, 0, 1).node_table)
+    cap, nodes, count, slot = dv.tile_tables(nt)
+    assert count.size == (nt.shape[0] + 127) // 128 and cap >= count.max()
+    for t in range(count.size):
+        rows = nt[128 * t:128 * (t + 1)]
+        assert np.array_equal(nodes[t][slot[128 * t:128 * t + len(rows)].astype(np.int64)], rows)
+        assert np.all(np.diff(nodes[t][:count[t]]) > 0)
+        assert count[t] == np.unique(rows).size

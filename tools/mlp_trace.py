@@ -19,8 +19,9 @@ for tile in range(3):
         rows = items[k:k + nk[g]] - t0
         print(f"tile {tile} gemm {g}: epi acc_full@{acc[j] - t0 if acc[j] else -1}")
         for c, r in enumerate(rows):
+            ae = t[8192 + k + c] - t0 if t.size > 8192 and t[8192 + k + c] else -1
             print(f"   c{c}: mma_wait@{r[0]:7d} a_full@{r[1]:7d} (+{r[1]-r[0]:5d}) issued@{r[2]:7d} "
-                  f"producer_arrive@{r[3]:7d}")
+                  f"producer a_empty ok@{ae:7d} arrive@{r[3]:7d}")
         k += nk[g]
         j += 1
 tot = items[n - 1, 2] - t0
@@ -34,4 +35,5 @@ for jj in range(12):
     print(f"  j{jj}: commit@{commit[jj] - t0:7d} epi_at_wait@{before[jj] - t0:7d} returns@{acc[jj] - t0:7d}")
 tl = t[6912:6912 + 40].reshape(-1, 4)
 for i in range(3):
-    print(f"tile {i}: load_x start@{tl[i,0]-t0} end@{tl[i,1]-t0} head epi done@{tl[i,2]-t0}")
+    print(f"tile {i}: load_x start@{tl[i,0]-t0} end@{tl[i,1]-t0} head epi done@{tl[i,2]-t0} "
+          f"stage ready (tile {i})@{tl[i,3]-t0 if tl[i,3] else -1}")

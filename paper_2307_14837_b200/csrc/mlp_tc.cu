@@ -643,9 +643,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         if (c < nck0) {
           float v[HC];
 #pragma unroll
-          for (int e = 0; e < HC; ++e) {
+          for (int e = 0; e < HC; e += 4) {
             const int col = c * KC + HC * hh + e;
-            v[e] = (xin[c][e] - p_mean[col]) * p_rstd[col];
+            const float4 mu = *reinterpret_cast<const float4*>(p_mean + col);
+            const float4 rs = *reinterpret_cast<const float4*>(p_rstd + col);
+            v[e + 0] = (xin[c][e + 0] - mu.x) * rs.x;
+            v[e + 1] = (xin[c][e + 1] - mu.y) * rs.y;
+            v[e + 2] = (xin[c][e + 2] - mu.z) * rs.z;
+            v[e + 3] = (xin[c][e + 3] - mu.w) * rs.w;
           }
           produce_chunk(c, v);
         }
@@ -674,10 +679,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
               else if (f4 < 2 * A.npp + geo4) x = gr[f4 - 2 * A.npp];
             }
             const int col = c * KC + HC * hh + 4 * j;
-            v[4 * j + 0] = (x.x - p_mean[col + 0]) * p_rstd[col + 0];
-            v[4 * j + 1] = (x.y - p_mean[col + 1]) * p_rstd[col + 1];
-            v[4 * j + 2] = (x.z - p_mean[col + 2]) * p_rstd[col + 2];
-            v[4 * j + 3] = (x.w - p_mean[col + 3]) * p_rstd[col + 3];
+            const float4 mu = *reinterpret_cast<const float4*>(p_mean + col);
+            const float4 rs = *reinterpret_cast<const float4*>(p_rstd + col);
+            v[4 * j + 0] = (x.x - mu.x) * rs.x;
+            v[4 * j + 1] = (x.y - mu.y) * rs.y;
+            v[4 * j + 2] = (x.z - mu.z) * rs.z;
+            v[4 * j + 3] = (x.w - mu.w) * rs.w;
           }
           produce_chunk(c, v);
         }

@@ -168,10 +168,48 @@ __device__ __forceinline__ void stage_geo(const ResidualArgs& A, int c, int t, f
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// coefficients of one Gauss point (pointwise phase); F = Q2 fields at q
+// Q1 (pi) fields p, vx, vy, vz at the two Gauss points (qx, qy, qz) and (qx, qy, qz + 2) of a
+// lane: trilinear in the 8 vertex values (elements.py:96-118); the x-y bilinear part is
+// shared by the two points.  PQ[f] = [value, d/dxi, d/deta, d/dzeta]
+__device__ __forceinline__ void pi_fields(const float* u, int qx, int qy, int qz, float PQa[4][4],
+                                          float PQb[4][4]) {
+  const float lx1 = cX[qx], ly1 = cX[qy], lza = cX[qz], lzb = cX[qz + 2];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const float* uf = u + f * 27;
+    float a[2][2], ax[2][2];
+#pragma unroll
+    for (int vz = 0; vz < 2; ++vz)
+#pragma unroll
+      for (int vy = 0; vy < 2; ++vy) {
+        const float g0 = uf[18 * vz + 6 * vy], g1 = uf[18 * vz + 6 * vy + 2];
+        a[vz][vy] = fmaf(lx1, g1 - g0, g0);
+        ax[vz][vy] = g1 - g0;
+      }
+    float b[2], bx[2], by[2];
+#pragma unroll
+    for (int vz = 0; vz < 2; ++vz) {
+      b[vz] = fmaf(ly1, a[vz][1] - a[vz][0], a[vz][0]);
+      bx[vz] = fmaf(ly1, ax[vz][1] - ax[vz][0], ax[vz][0]);
+      by[vz] = a[vz][1] - a[vz][0];
+    }
+    const float db = b[1] - b[0], dbx = bx[1] - bx[0], dby = by[1] - by[0];
+    PQa[f][0] = fmaf(lza, db, b[0]);
+    PQa[f][1] = fmaf(lza, dbx, bx[0]);
+    PQa[f][2] = fmaf(lza, dby, by[0]);
+    PQa[f][3] = db;
+    PQb[f][0] = fmaf(lzb, db, b[0]);
+    PQb[f][1] = fmaf(lzb, dbx, bx[0]);
+    PQb[f][2] = fmaf(lzb, dby, by[0]);
+    PQb[f][3] = db;
+  }
+}
+
+// coefficients of one Gauss point (pointwise phase); F = Q2 fields at q, PQ = pi fields at q
 template <int MODE, bool CACHED>
 __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S, float* CF, int q,
-                                          float F[KLay<CACHED>::NF][4], float aT, float dT) {
+                                          float F[KLay<CACHED>::NF][4], const float PQ[4][4],
+                                          float aT, float dT) {
   using L = KLay<CACHED>;
   constexpr int FO = L::FO;
   const int qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
@@ -222,33 +260,6 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
   const float ik = A.ik;
   if constexpr (MODE == MODE_OPERATOR) {
     const float p = F[FO][0];
-    // Q1 (pi) fields: trilinear in the vertex values, at this Gauss point
-    const float lx1 = cX[qx], ly1 = cX[qy], lz1 = cX[qz];
-    float PQ[4][4];  // [p, vx, vy, vz][val, d/dxi, d/deta, d/dzeta]
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const float* uf = S + oU + (FO + f) * 27;
-      float a[2][2], ax[2][2];
-#pragma unroll
-      for (int vz = 0; vz < 2; ++vz)
-#pragma unroll
-        for (int vy = 0; vy < 2; ++vy) {
-          const float g0 = uf[18 * vz + 6 * vy], g1 = uf[18 * vz + 6 * vy + 2];
-          a[vz][vy] = fmaf(lx1, g1 - g0, g0);
-          ax[vz][vy] = g1 - g0;
-        }
-      float b[2], bx[2], by[2];
-#pragma unroll
-      for (int vz = 0; vz < 2; ++vz) {
-        b[vz] = fmaf(ly1, a[vz][1] - a[vz][0], a[vz][0]);
-        bx[vz] = fmaf(ly1, ax[vz][1] - ax[vz][0], ax[vz][0]);
-        by[vz] = a[vz][1] - a[vz][0];
-      }
-      PQ[f][0] = fmaf(lz1, b[1] - b[0], b[0]);
-      PQ[f][1] = fmaf(lz1, bx[1] - bx[0], bx[0]);
-      PQ[f][2] = fmaf(lz1, by[1] - by[0], by[0]);
-      PQ[f][3] = b[1] - b[0];
-    }
     // physical gradient of the pressure fluctuation p - pi p
     const float dd0 = F[FO][1] - PQ[0][1], dd1 = F[FO][2] - PQ[0][2], dd3 = F[FO][3] - PQ[0][3];
     float gdp[3];
@@ -424,8 +435,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
       }
-      pointwise<MODE, CACHED>(A, S, S + L::oCF, t, F, aT, dT);
-      pointwise<MODE, CACHED>(A, S, S + L::oCF, t + 32, G, aT, dT);
+      float PQa[4][4], PQb[4][4];
+      if constexpr (MODE == MODE_OPERATOR)
+        pi_fields(S + oU + L::FO * 27, yx & 3, yx >> 2, qz, PQa, PQb);
+      pointwise<MODE, CACHED>(A, S, S + L::oCF, t, F, PQa, aT, dT);
+      pointwise<MODE, CACHED>(A, S, S + L::oCF, t + 32, G, PQb, aT, dT);
     }
     __syncwarp();
     if constexpr (CACHED) {

@@ -73,7 +73,9 @@ struct TcArgs {
   int64_t n_rows;
   int n_in, n_out, depth, act;
   int K0p, Nhead;
-  int y_mode;  // 0: direct stores, 2: staged in a dedicated shared-memory buffer
+  int y_mode;  // 0: direct stores, 2: staged in a dedicated shared-memory buffer,
+               // 3 (GM_STAGED): the whole 128-row tile staged in the gather staging area and
+               //   written by one bulk (TMA) store from the gather warp
   const uint8_t* packed;
   int64_t goff[DNNMG_MAX_LAYERS];
   const float* scale;
@@ -136,6 +138,13 @@ __device__ __forceinline__ void mbar_add_tx(uint32_t bar, uint32_t bytes) {  // 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
+}
+// shared -> global bulk copy (TMA), tracked by the issuing thread's bulk group
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
@@ -353,7 +362,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   uint64_t* idx_full = acc_empty + 2;   // fused gather: next tile's node indices staged by TMA
   uint64_t* idx_empty = idx_full + 1;
   uint64_t* stage_full = idx_empty + 1;   // GM_STAGED: the tile's nodes are in SMEM
-  uint64_t* stage_empty = stage_full + 1; // GM_STAGED: layer 0 consumed them
+  uint64_t* stage_empty = stage_full + 1; // GM_STAGED: staging area free (layer 0 consumed it,
+                                          // or, y_mode 3, the previous tile's Y written to it)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stage_empty + 1);
   // BN scale/shift per hidden layer and the input normalisation, staged once per CTA
   float* p_scale = reinterpret_cast<float*>(tmem_slot + 4);
@@ -504,9 +514,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     // rows (bulk copies) land in SMEM while the compute warps run tile t - grid; the
     // layer-0 operand of tile t is then built from SMEM (patch_ops.py:49-53).
     if constexpr (GM == GM_STAGED) {
+      // y_mode 3: the staging area alternates between staged nodes and the previous tile's
+      // Y; phase it-1 of stage_empty = area free (it = 1: tile 0 consumed; it >= 2: Y of the
+      // tile it-2 written), so store that Y, then stage tile it
+      const bool ystore = A.y_mode == 3;
+      const int64_t n_mine = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+      auto store_y = [&](int64_t yt) {
+        const int64_t r0 = yt * kTcM;
+        const int nv = (int)((A.n_rows - r0) < kTcM ? (A.n_rows - r0) : kTcM);
+        const uint32_t bytes = (uint32_t)nv * A.n_out * 4;
+        float* dst = A.Y + r0 * A.n_out;
+        const float* ys = reinterpret_cast<const float*>(st_base);
+        if ((bytes & 15) == 0) {
+          if (lane == 0) {
+            bulk_s2g(dst, smem_u32(ys), bytes);
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+        } else {
+          for (uint32_t i = lane; i < bytes / 4; i += 32) dst[i] = ys[i];
+        }
+        __syncwarp();
+      };
       uint32_t it = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
         if (it > 0) mbar_wait(smem_u32(stage_empty), (it - 1) & 1);
+        if (ystore && it >= 2) store_y(tile - 2 * gridDim.x);
         const int64_t r0 = tile * kTcM;
         const int nvalid = (int)((A.n_rows - r0) < kTcM ? (A.n_rows - r0) : kTcM);
         if (lane == 0) {
@@ -536,6 +568,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(stage_full));
+      }
+      if (ystore) {
+        // remaining phases: n_mine - 1 (Y of tile n_mine - 2; for n_mine = 1 phase 0, tile 0
+        // consumed) and n_mine (Y of the last tile).  The last tile has no next tile to stage,
+        // so the area being free again is signalled on stage_full explicitly.
+        for (int64_t ph = (n_mine >= 2 ? n_mine - 1 : 0); ph <= n_mine; ++ph) {
+          mbar_wait(smem_u32(stage_empty), (uint32_t)ph & 1);
+          if (ph >= 1) store_y(blockIdx.x + (ph - 1) * gridDim.x);
+          if (ph == n_mine - 1 && n_mine >= 2 && lane == 0) mbar_arrive(smem_u32(stage_full));
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
     }
   } else {
@@ -689,8 +732,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           produce_chunk(c, v);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(stage_empty));
+      // y_mode 3: after the first tile the area is released by the head epilogue instead
+      if (A.y_mode != 3 || sit == 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(stage_empty));
+      }
       ++sit;
     };
     if constexpr (GM == GM_STAGED) {
@@ -768,7 +814,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
         if (warp == 0 && lane == 0) TC_TRACE(6144 + j);
         tc_fence_after();
-        if (A.y_mode == 0) {
+        if (A.y_mode == 3) {
+          // the whole tile into the staging area (its nodes were consumed above: wait for all
+          // compute warps), then one bulk store from the gather warp (stage_empty)
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (tile + gridDim.x >= n_tiles && tile >= (int64_t)gridDim.x) {
+            // last tile of several: wait until the previous tile's Y has left the area
+            mbar_wait(smem_u32(stage_full), sit & 1);
+            ++sit;
+          }
+          float* ys = reinterpret_cast<float*>(st_base);
+          for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
+            float v[16];
+            tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int col = sl * 16 + e;
+              if (col < A.n_out) ys[row_in_tile * A.n_out + col] = v[e] * y_unscale;
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(stage_empty));
+        } else if (A.y_mode == 0) {
           for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
             float v[16];
             tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
@@ -1028,7 +1096,10 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   size_t smem = base + (gm == GM_DIRECT ? (size_t)kTcM * g->npp * 4
                         : gm == GM_STAGED ? staged_bytes(g->npp, g->n_geo, g->tile_cap) : 0);
   const size_t ybytes = (size_t)(kTcM / 2) * m->n_out * 4;  // staged in two 64-row halves
-  if (smem + ybytes <= kSmemMax && !getenv("DNNMG_Y_DIRECT")) {
+  if (gm == GM_STAGED && (size_t)kTcM * m->n_out * 4 <= staged_bytes(g->npp, g->n_geo, g->tile_cap) &&
+      !getenv("DNNMG_Y_HALVES")) {
+    A.y_mode = 3;
+  } else if (smem + ybytes <= kSmemMax && !getenv("DNNMG_Y_DIRECT")) {
     A.y_mode = 2;
     smem += ybytes;
   } else {

@@ -44,14 +44,19 @@ class CorrectionStep:
         # K2 reads J^-1 and w from the per-mesh geometry cache (the mesh is fixed in time)
         self.lv = self.level.struct(self.mask_bits, geometry=True)
         self.patchset = patchset if patchset is not None else meshmod.build_patches(hierarchy, L, J)
-        check_model(model, self.patchset)
         self.ps = dv.DevicePatchSet.get(self.patchset)
         self.precision = precision
-        self.model = dv.DeviceModel(model, precision)
-        a = model.arch
-        # K3 fused into K4 when the tensor-core MLP can stage the rows itself
-        self.fused_gather = (precision != "fp32" and a.n_hidden == 256 and a.n_in <= 256
-                             and a.n_out <= 256 and self.patchset.n_geo % 4 == 0)
+        # model=None: embedding and next-step RHS only (a hybrid loop before its first
+        # correction, driver.py:261); run() then raises
+        self.model = None
+        self.fused_gather = False
+        if model is not None:
+            check_model(model, self.patchset)
+            self.model = dv.DeviceModel(model, precision)
+            a = model.arch
+            # K3 fused into K4 when the tensor-core MLP can stage the rows itself
+            self.fused_gather = (precision != "fp32" and a.n_hidden == 256 and a.n_in <= 256
+                                 and a.n_out <= 256 and self.patchset.n_geo % 4 == 0)
         self.phys = _lib.Phys(float(nu), float(k), float(alpha0), float(delta0), 1)
         dev = dv.device()
         nf = self.space.n_nodes
@@ -61,8 +66,11 @@ class CorrectionStep:
         self.d = torch.empty(4 * nf, dtype=f, device=dev)
         self.x_corr = torch.empty(4 * nf, dtype=f, device=dev)
         self.elem = self.level.scratch()
-        self.X = torch.empty((self.ps.n_patches, input_width(self.patchset)), dtype=f, device=dev)
-        self.Y = torch.empty((self.ps.n_patches, output_width(self.patchset)), dtype=f, device=dev)
+        # X is only materialised when the gather is not fused into the MLP
+        n_x = 0 if (self.fused_gather or model is None) else self.ps.n_patches
+        self.X = torch.empty((n_x, input_width(self.patchset)), dtype=f, device=dev)
+        self.Y = torch.empty((self.ps.n_patches if model is not None else 0,
+                              output_width(self.patchset)), dtype=f, device=dev)
         self.x_mid = (torch.empty(4 * self.prolongs[0].n_fine, dtype=f, device=dev)
                       if J == 2 else None)
         self.buf = _lib.StepBuffers(dv.ptr(self.x_tilde), dv.ptr(self.r), dv.ptr(self.elem),
@@ -116,6 +124,8 @@ class CorrectionStep:
     def run(self, x_coarse, b_prev, x_corr=None):
         """Issue one correction step; all arguments are fp32 CUDA tensors."""
         out = self.x_corr if x_corr is None else x_corr
+        if self.model is None:
+            raise ValueError("correction step without a model: use embed_into() / rhs_next()")
         if x_coarse.numel() != self.coarse_ndof or b_prev.numel() != self.x_tilde.numel():
             raise ValueError("vector length does not match the coarse / fine level")
         _lib.call("dnnmg_correction_step", self.P, self.J, ctypes.byref(self.bc.struct),

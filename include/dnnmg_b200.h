@@ -229,6 +229,28 @@ int32_t dnnmg_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const u
                              const float* x_tilde, float scale, float* d, float* x_corr,
                              dnnmg_stream_t stream);
 
+/* ---- training data -------------------------------------------------
+ * rows[p] = [x~ rows | r rows | geometry | targets] as float64, the dataset-shard row of
+ * driver.export_training_data (driver.py:317-383, io.write_dataset io.py:219-287):
+ * features as assemble_network_input (patch_ops.py:49-53), targets as patch_targets
+ * (patch_ops.py:79-82), i.e. (v_ref - x~) at the velocity slots.  r NULL: zero residual
+ * block; v_ref NULL: zero targets; x_ref (float64, nullable) replaces x~ in the target
+ * difference.  rows: [n_patches][8*npp + n_geo + 3*npp]. */
+int32_t dnnmg_dataset_rows(const dnnmg_patchset_t* ps, const float* x_tilde, const float* r,
+                           const double* v_ref, const double* x_ref, double* rows,
+                           dnnmg_stream_t stream);
+/* Per-column statistics of a float64 row block [n][w] for the dataset sidecar: stats =
+ * [sum | centred sum of squares M2 | min | max], each [w]; deterministic (fixed-order
+ * two-pass partials combined pairwise).
+ * scratch: dnnmg_column_stats_scratch(w) doubles (device). */
+int32_t dnnmg_column_stats_scratch(int32_t w);
+/* Ideal correction of oracle_loop_features (driver.py:418-424): x_corr = x~ + d with
+ * d = v_ref - x~ at free velocity dofs; pressure and constrained dofs (dof_mask bits) keep
+ * x~.  Per node float4 x~ / x_corr, float64 v_ref [4*n_nodes]. */
+int32_t dnnmg_ideal_update(int32_t n_nodes, const float* x_tilde, const double* v_ref,
+                           const uint8_t* dof_mask, float* x_corr, dnnmg_stream_t stream);
+int32_t dnnmg_column_stats(const double* rows, int64_t n, int32_t w, double* scratch,
+                           double* stats, dnnmg_stream_t stream);
 /* ---- whole correction step (driver.py:251-268) ------------------------------------------ */
 typedef struct {
   float* x_tilde;   /* [4*n_fine] */

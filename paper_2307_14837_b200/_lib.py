@@ -90,6 +90,10 @@ EXPORTS = {
     "dnnmg_mlp_gather_mode": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet)]),
     "dnnmg_scatter_update": (c_i32, [ctypes.POINTER(PatchSet), c_vp, c_vp, c_vp, c_f32, c_vp, c_vp,
                                      c_vp]),
+    "dnnmg_dataset_rows": (c_i32, [ctypes.POINTER(PatchSet), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dnnmg_column_stats_scratch": (c_i32, [c_i32]),
+    "dnnmg_ideal_update": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dnnmg_column_stats": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "dnnmg_correction_step": (c_i32, [ctypes.POINTER(Prolong), c_i32, ctypes.POINTER(Dirichlet),
                                       ctypes.POINTER(Level), ctypes.POINTER(Phys),
                                       ctypes.POINTER(PatchSet), ctypes.POINTER(Mlp), c_vp, c_vp,

@@ -176,3 +176,204 @@ def _coarse_dirichlet(space, x, t, bcs):
         v[idx, 1:] = fn(t, space.nodes[idx])
     x.time = t
     return x
+
+
+# -- training data on the GPU (driver.py:286-431) -------------------
+
+def steps_in_interval(interval, k, n_max):
+    """Step indices n in 1..n_max with lo < n k <= hi (driver.py:286-291)."""
+    lo, hi = interval
+    eps = 1e-9 * k
+    return [n for n in range(1, n_max + 1) if lo + eps < n * k <= hi + eps]
+
+
+class _FineMachinery:
+    """Device workspace of the replayed hybrid machinery on level L+J: embedding with
+    Dirichlet data at t (K1), next RHS (K2 RHS form), residual (K2), dataset rows, column
+    statistics, ideal correction.  Vectors are fp32 CUDA tensors, trajectory values
+    float64 on the device."""
+
+    def __init__(self, problem, L, J, patchset):
+        if getattr(problem, "f", None) is not None:
+            raise NotImplementedError("volume forces on the fine level are not supported")
+        if not getattr(problem, "reimpose_fine_dirichlet", True):
+            raise NotImplementedError("reimpose_fine_dirichlet=False is not supported")
+        self.pr, self.L, self.J = problem, L, J
+        fl = L + J
+        self.step = CorrectionStep(problem.hierarchy, L, J, None, problem.nu, problem.k,
+                                   bcs=problem.bcs, alpha0=problem.alpha0,
+                                   delta0=problem.delta0, patchset=patchset,
+                                   mask=np.asarray(problem.mask(fl)))
+        self.ps = self.step.ps
+        self.w = 11 * self.ps.npp + self.ps.n_geo
+        self.nf = 8 * self.ps.npp + self.ps.n_geo
+        dev = self.step.x_tilde.device
+        self.rows = torch.empty((self.ps.n_patches, self.w), dtype=torch.float64, device=dev)
+        lib = _lib()
+        self.scratch = torch.empty(int(lib.dnnmg_column_stats_scratch(self.w)),
+                                   dtype=torch.float64, device=dev)
+        self.stats = torch.empty((4, self.w), dtype=torch.float64, device=dev)
+
+    def embed(self, values, t, out=None):
+        self.step.set_time(t)
+        out = torch.empty_like(self.step.x_tilde) if out is None else out
+        return self.step.embed_into(dv.f32(values), out)
+
+    def rhs(self, x):
+        return self.step.rhs_next(x)
+
+    def residual(self, xt, b):
+        return self.step.residual_into(xt, b, torch.empty_like(xt))
+
+    def make_rows(self, xt, r, v_ref=None, x_ref=None):
+        """Feature + target rows [n_patches][w] (float64) and their column statistics."""
+        import ctypes
+        s = dv.stream_handle()
+        vr = None if v_ref is None else _f64(v_ref)
+        xr = None if x_ref is None else _f64(x_ref)
+        lib_call("dnnmg_dataset_rows", ctypes.byref(self.ps.struct), dv.ptr(xt), dv.ptr(r),
+                 dv.ptr(vr), dv.ptr(xr), dv.ptr(self.rows), s)
+        lib_call("dnnmg_column_stats", dv.ptr(self.rows), ctypes.c_int64(self.ps.n_patches),
+                 self.w, dv.ptr(self.scratch), dv.ptr(self.stats), s)
+        return self.rows.cpu().numpy(), self.stats.cpu().numpy()
+
+    def ideal_update(self, xt, v_ref):
+        import ctypes
+        out = torch.empty_like(xt)
+        lib_call("dnnmg_ideal_update", ctypes.c_int32(xt.numel() // 4), dv.ptr(xt),
+                 dv.ptr(_f64(v_ref)), dv.ptr(self.step.mask_bits), dv.ptr(out),
+                 dv.stream_handle())
+        return out
+
+    def restrict(self, bf):
+        return spmod.restrict_rhs(self.pr.hierarchy, bf, self.L + self.J, self.J)
+
+
+def _lib():
+    from . import _lib as lib
+    return lib.load()
+
+
+def lib_call(name, *args):
+    from . import _lib as lib
+    lib.call(name, *args)
+
+
+def _f64(v):
+    if isinstance(v, torch.Tensor):
+        return v.to(device=dv.device(), dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.array(v, dtype=np.float64)).to(dv.device())
+
+
+def embed_state(problem, L, J, values, t):
+    """Prolongate coarse values to L+J and re-impose the boundary data at t (driver.py:611-619),
+    on the GPU; numpy in -> float64 numpy out."""
+    m = _FineMachinery(problem, L, J, meshmod.build_patches(problem.hierarchy, L, J))
+    return dv.like_input(m.embed(values, t), values)
+
+
+def replay_features(problem, L, J, coarse_values, b_fine, t):
+    """One step of the hybrid machinery without a model: (x~, r) (driver.py:294-314)."""
+    m = _FineMachinery(problem, L, J, meshmod.build_patches(problem.hierarchy, L, J))
+    xt = m.embed(coarse_values, t)
+    r = m.residual(xt, dv.f32(b_fine))
+    return dv.like_input(xt, coarse_values), dv.like_input(r, coarse_values)
+
+
+def _loop_rows(m, coarse_traj, fine_traj, n_start, interval, emit):
+    """oracle_loop_features (driver.py:386-431) on the device: the hybrid loop under the
+    ideal correction from the coarse state at n_start; emit(n, rows, stats) per step."""
+    pr, L, J = m.pr, m.L, m.J
+    x = spmod.StateVector(L, np.array(coarse_traj.values(n_start), dtype=float), n_start * pr.k)
+    xf = m.embed(x.values, x.time)
+    bf = m.rhs(xf)
+    b = m.restrict(bf).double().cpu().numpy()
+    solver = None
+    n = n_start
+    eps = 1e-9 * pr.k
+    while (n + 1) * pr.k <= interval[1] + eps and n + 1 <= fine_traj.n_steps:
+        n += 1
+        t = n * pr.k
+        x, _, solver = pr.solve_step(L, x, b, t, solver=solver)
+        xt = m.embed(x.values, t)
+        r = m.residual(xt, bf)
+        v = fine_traj.values(n)
+        rows, stats = m.make_rows(xt, r, v_ref=v)
+        emit(n, rows, stats)
+        x_corr = m.ideal_update(xt, v)
+        bf = m.rhs(x_corr)
+        b = m.restrict(bf).double().cpu().numpy()
+
+
+def oracle_loop_features(problem, L, J, coarse_traj, fine_traj, n_start, interval, patchset):
+    """(n, features, targets) per step of the ideal-correction loop (driver.py:386-431)."""
+    m = _FineMachinery(problem, L, J, patchset)
+    out = []
+    _loop_rows(m, coarse_traj, fine_traj, n_start, interval,
+               lambda n, rows, st: out.append((n, rows[:, :m.nf].copy(), rows[:, m.nf:].copy())))
+    return out
+
+
+def export_training_data(problem, L, J, coarse_traj, fine_traj, t_train, t_val, out_dir,
+                         shard_bytes=256 * 2 ** 20, loop_pass=False):
+    """The (features, targets) dataset of a coarse and a fine run (driver.py:317-383), built
+    on the GPU and streamed into the reference's shard format (io.write_dataset).
+
+    Per step n in the half-open windows: x~ = embed(coarse^n), b = rhs(embed(coarse^{n-1})),
+    r = b - A_h(x~) (K1, K2); the row block [x~ | r | geometry | fine^n - x~] is formed by
+    ``dnnmg_dataset_rows`` and its column statistics by ``dnnmg_column_stats``.  With
+    loop_pass the ideal-correction loop's rows are appended (the coarse solves are the
+    problem's own, as in the reference)."""
+    from . import io as iomod
+    pr = problem
+    if abs(coarse_traj.k - fine_traj.k) > 1e-14:
+        raise ValueError("runs do not share the time step size")
+    fl = L + J
+    if fine_traj.level != fl:
+        raise ValueError(f"fine run level {fine_traj.level} incompatible with L={L}, J={J}")
+    same_level = coarse_traj.level == fl
+    if not same_level and coarse_traj.level != L:
+        raise ValueError(f"coarse run level {coarse_traj.level} != L={L}")
+    patchset = meshmod.build_patches(pr.hierarchy, L, J)
+    n_max = min(coarse_traj.n_steps, fine_traj.n_steps)
+    windows = (("train", t_train), ("val", t_val))
+    steps = {name: steps_in_interval(iv, pr.k, n_max) for name, iv in windows}
+    loop_steps = []
+    n_lo = None
+    if loop_pass and not same_level:
+        lo, hi = min(t_train[0], t_val[0]), max(t_train[1], t_val[1])
+        n_lo = steps_in_interval((lo, hi), pr.k, n_max)[0]
+        eps = 1e-9 * pr.k
+        n = n_lo - 1
+        while (n + 1) * pr.k <= hi + eps and n + 1 <= fine_traj.n_steps:
+            n += 1
+            loop_steps.append(n)
+    m = _FineMachinery(pr, L, J, patchset)
+    n_p = m.ps.n_patches
+    writer = iomod.DatasetWriter(out_dir, patchset)
+    loop_in = {name: [n for n in loop_steps if n in set(steps_in_interval(iv, pr.k, n_max))]
+               for name, iv in windows}
+    for name, _ in windows:
+        writer.begin_set(name, n_p * (len(steps[name]) + len(loop_in[name])), m.nf,
+                         3 * m.ps.npp, shard_bytes)
+    for name, _ in windows:
+        for n in steps[name]:
+            xc = coarse_traj.values(n)
+            v = fine_traj.values(n)
+            if same_level:
+                xt = dv.f32(xc)
+                rows, stats = m.make_rows(xt, None, v_ref=v, x_ref=xc)
+            else:
+                xp = m.embed(coarse_traj.values(n - 1), (n - 1) * pr.k)
+                b_prev = m.rhs(xp)
+                xt = m.embed(xc, n * pr.k)
+                r = m.residual(xt, b_prev)
+                rows, stats = m.make_rows(xt, r, v_ref=v)
+            writer.add_rows(name, rows, stats)
+    if loop_steps:
+        def emit(n, rows, stats):
+            for name, _ in windows:
+                if n in loop_in[name]:
+                    writer.add_rows(name, rows, stats)
+        _loop_rows(m, coarse_traj, fine_traj, n_lo - 1, (None, max(t_train[1], t_val[1])), emit)
+    return writer.finish()

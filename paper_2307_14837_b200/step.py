@@ -197,6 +197,13 @@ class CorrectionStep:
         self.graph = g
         return g
 
+    def residual_into(self, x_tilde, b_prev, r):
+        """r = b_prev - A_h(x~) with stab at x~ and the mask (assembly.py:261-267), K2."""
+        _lib.call("dnnmg_residual", ctypes.byref(self.lv), dv.ptr(x_tilde), dv.ptr(b_prev), None,
+                  None, ctypes.byref(self.phys), dv.ptr(self.elem), dv.ptr(r), 1,
+                  dv.stream_handle())
+        return r
+
     def rhs_next(self, x, out=None):
         """Next-step fine RHS from a (corrected) fine state (assembly.py:242-259)."""
         out = torch.empty_like(self.x_tilde) if out is None else out

@@ -251,6 +251,35 @@ int32_t dnnmg_ideal_update(int32_t n_nodes, const float* x_tilde, const double* 
                            const uint8_t* dof_mask, float* x_corr, dnnmg_stream_t stream);
 int32_t dnnmg_column_stats(const double* rows, int64_t n, int32_t w, double* scratch,
                            double* stats, dnnmg_stream_t stream);
+/* ---- coarse-level Vanka smoother (msolve.py:51-89) -----------------
+ * A level Jacobian in CSR (float64, the reference's assemble_jacobian output) and the
+ * prefactored cell blocks of VankaData. */
+typedef struct {
+  int32_t n_rows;
+  const int32_t* indptr;   /* [n_rows+1] */
+  const int32_t* indices;  /* [nnz] */
+  const double* data;      /* [nnz] */
+} dnnmg_csr_t;
+typedef struct {
+  int32_t n_cells, ndl, n_dofs;  /* ndl = (d+1) 3^d = 108 */
+  const int32_t* cell_dofs;      /* [n_cells][ndl] (Assembler.cell_dofs) */
+  const int32_t* dof_cell_ptr;   /* [n_dofs+1] CSR dof -> (cell*ndl + i), ascending: the */
+  const int32_t* dof_cell_idx;   /*   order of np.bincount over cell_dofs */
+  const double* weight;          /* [n_dofs] 1 / multiplicity */
+  const double* inv;             /* [n_cells][ndl][ndl] inverted blocks (dnnmg_vanka_setup) */
+} dnnmg_vanka_t;
+/* inv[c] = (J.data[flat_pos[c*ndl*ndl ...]] as an ndl x ndl block)^-1 in float64
+ * (Gauss-Jordan, partial pivoting); a singular block is retried with a 1e-12 diagonal
+ * shift: flags[c] = 0 regular, 1 shifted (the reference's `flagged`), 2 singular. */
+int32_t dnnmg_vanka_setup(int32_t n_cells, int32_t ndl, const double* csr_data,
+                          const int64_t* flat_pos, double* inv, int32_t* flags,
+                          dnnmg_stream_t stream);
+/* `sweeps` Jacobi-coupled Vanka sweeps on x in place (msolve.vanka_smooth):
+ * r = b - J x; dl = inv r[dofs]; x += damping * weight * bincount(dofs, dl).
+ * Scratch: r [n_dofs], dl [n_cells*ndl] (float64, device). */
+int32_t dnnmg_vanka_smooth(const dnnmg_vanka_t* V, const dnnmg_csr_t* J, const double* b,
+                           double* x, int32_t sweeps, double damping, double* r, double* dl,
+                           dnnmg_stream_t stream);
 /* ---- whole correction step (driver.py:251-268) ------------------------------------------ */
 typedef struct {
   float* x_tilde;   /* [4*n_fine] */

@@ -60,6 +60,15 @@ class Restrict(ctypes.Structure):
                 ("w", c_vp)]
 
 
+class Csr(ctypes.Structure):
+    _fields_ = [("n_rows", c_i32), ("indptr", c_vp), ("indices", c_vp), ("data", c_vp)]
+
+
+class Vanka(ctypes.Structure):
+    _fields_ = [("n_cells", c_i32), ("ndl", c_i32), ("n_dofs", c_i32), ("cell_dofs", c_vp),
+                ("dof_cell_ptr", c_vp), ("dof_cell_idx", c_vp), ("weight", c_vp), ("inv", c_vp)]
+
+
 class StepBuffers(ctypes.Structure):
     _fields_ = [("x_tilde", c_vp), ("r", c_vp), ("elem", c_vp), ("X", c_vp), ("Y", c_vp),
                 ("d", c_vp), ("x_mid", c_vp)]
@@ -94,6 +103,9 @@ EXPORTS = {
     "dnnmg_column_stats_scratch": (c_i32, [c_i32]),
     "dnnmg_ideal_update": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dnnmg_column_stats": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "dnnmg_vanka_setup": (c_i32, [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dnnmg_vanka_smooth": (c_i32, [ctypes.POINTER(Vanka), ctypes.POINTER(Csr), c_vp, c_vp, c_i32,
+                                   ctypes.c_double, c_vp, c_vp, c_vp]),
     "dnnmg_correction_step": (c_i32, [ctypes.POINTER(Prolong), c_i32, ctypes.POINTER(Dirichlet),
                                       ctypes.POINTER(Level), ctypes.POINTER(Phys),
                                       ctypes.POINTER(PatchSet), ctypes.POINTER(Mlp), c_vp, c_vp,

@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--cpu-sample", default="16x8x8", help="coarse box of the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-aux", action="store_true", help="skip the next-row aux timings")
     return ap.parse_args()
 
 
@@ -377,6 +378,113 @@ def run_slabs(args, rank, world, local):
     tdist.destroy_process_group()
 
 
+def dataset_aux(step, steps, barrier):
+    """Next row #3: training-data rows of the step's x~ and r (dnnmg_dataset_rows, float64
+    [x~ | r | geometry | targets] per patch) and their column statistics, config 3."""
+    import ctypes
+    import torch
+    from paper_2307_14837_b200 import _lib, device as dvm
+    ps = step.ps
+    w = 11 * ps.npp + ps.n_geo
+    rows = torch.empty((ps.n_patches, w), dtype=torch.float64, device="cuda")
+    v_ref = torch.randn(step.x_tilde.numel(), dtype=torch.float64, device="cuda")
+    lib = _lib.load()
+    scratch = torch.empty(int(lib.dnnmg_column_stats_scratch(w)), dtype=torch.float64, device="cuda")
+    stats = torch.empty((4, w), dtype=torch.float64, device="cuda")
+    s = dvm.stream_handle()
+
+    def rows_call():
+        _lib.call("dnnmg_dataset_rows", ctypes.byref(ps.struct), dvm.ptr(step.x_tilde),
+                  dvm.ptr(step.r), dvm.ptr(v_ref), None, dvm.ptr(rows), s)
+
+    def stats_call():
+        _lib.call("dnnmg_column_stats", dvm.ptr(rows), ctypes.c_int64(ps.n_patches), w,
+                  dvm.ptr(scratch), dvm.ptr(stats), s)
+    rows_call()
+    stats_call()
+    barrier()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    for _ in range(steps):
+        rows_call()
+    e[1].record()
+    for _ in range(steps):
+        stats_call()
+    e[2].record()
+    barrier()
+    t_rows = e[0].elapsed_time(e[1]) / steps
+    t_stats = e[1].elapsed_time(e[2]) / steps
+    npp = ps.npp
+    # algorithmic bytes per patch: node indices, x~ and r float4 rows, geometry, the three
+    # float64 velocity comps of v_ref per node, and the float64 row written
+    per_patch = 4 * npp + 2 * 16 * npp + 4 * ps.n_geo + 24 * npp + 8 * w
+    byts = per_patch * ps.n_patches
+    return {"rows_ms": t_rows, "rows_GB/s": byts / (t_rows / 1e3) / 1e9,
+            "stats_ms": t_stats, "stats_GB/s": 8 * w * ps.n_patches / (t_stats / 1e3) / 1e9,
+            "rows": ps.n_patches, "row_bytes": 8 * w,
+            "note": "driver.export_training_data per step: row block + sidecar statistics"}
+
+
+def vanka_aux(step, steps, barrier, n_cells=(16, 8, 8)):
+    """Next row #4: cell-Vanka smoothing on a config-1-sized level (1,024 cells, 38,148 dofs,
+    Q2/Q2 block pattern of Assembler._init_sparsity, synthetic diagonally dominant values):
+    block inversion once, then sweeps (msolve.vanka_smooth)."""
+    import scipy.sparse as spm
+    import torch
+    from paper_2307_14837_b200 import mesh as meshmod, msolve
+    h = meshmod.build_template_mesh("box", extent_lo=(0, 0, 0), extent_hi=(1, 1, 1),
+                                    n_cells=n_cells)
+    cn = h.scalar_nodes(0)[1]
+    nc, ndof = cn.shape[0], 4 * h.scalar_nodes(0)[0].shape[0]
+    dofs = (4 * cn[:, :, None] + np.arange(4)).reshape(nc, -1).astype(np.int64)
+    ndl = dofs.shape[1]
+    rows = np.repeat(dofs, ndl, axis=1).reshape(-1)
+    cols = np.tile(dofs, (1, ndl)).reshape(-1)
+    pat = spm.coo_matrix((np.ones(rows.size), (rows, cols)), shape=(ndof, ndof)).tocsr()
+    pat.sort_indices()
+    keys = np.repeat(np.arange(ndof, dtype=np.int64), np.diff(pat.indptr)) * ndof + pat.indices
+    flat_pos = np.searchsorted(keys, rows * ndof + cols)
+    rng = np.random.default_rng(5)
+    data = rng.standard_normal(pat.nnz)
+    data[np.searchsorted(keys, np.arange(ndof, dtype=np.int64) * (ndof + 1))] += 2.0 * ndl
+    J = spm.csr_matrix((data, pat.indices, pat.indptr), shape=(ndof, ndof))
+
+    class Asm:
+        pass
+    asm = Asm()
+    asm.n_cells, asm.ndl, asm.cell_dofs, asm.flat_pos = nc, ndl, dofs, flat_pos
+
+    class Space:
+        pass
+    asm.space = Space()
+    asm.space.ndof = ndof
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    V = msolve.VankaData(asm, J)
+    t1.record()
+    torch.cuda.synchronize()
+    x = torch.zeros(ndof, dtype=torch.float64, device="cuda")
+    b = torch.tensor(rng.standard_normal(ndof), dtype=torch.float64, device="cuda")
+    msolve.vanka_smooth(J, V, x, b, 2, 0.7)
+    sweeps = 12 * max(1, steps // 4)
+    barrier()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record()
+    msolve.vanka_smooth(J, V, x, b, sweeps, 0.7)
+    s1.record()
+    barrier()
+    t_sweep = s0.elapsed_time(s1) / sweeps
+    # per sweep: the inverse blocks (float64), the CSR matrix (value + column), the iterate
+    # gathers and the per-dof accumulation
+    byts = nc * ndl * ndl * 8 + J.nnz * 12 + ndof * 8 * 6 + nc * ndl * 16
+    return {"cells": nc, "dofs": ndof, "nnz": int(J.nnz), "setup_ms": t0.elapsed_time(t1),
+            "sweep_ms": t_sweep, "sweep_GB/s": byts / (t_sweep / 1e3) / 1e9,
+            "note": "msolve.VankaData + vanka_smooth on a synthetic config-1-level Jacobian"}
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as tdist
@@ -445,6 +553,12 @@ def run_ours(args, rank, world, local):
                "note": "Alg. 1 lines 8-9 (next-step RHS, P^T restriction); outside the timed step"}
     except Exception as exc:  # pragma: no cover - auxiliary numbers only
         aux = {"error": str(exc)[:200]}
+    if not args.no_aux:
+        for key, fn in (("dataset_rows", dataset_aux), ("vanka", vanka_aux)):
+            try:
+                aux[key] = fn(step, args.steps, barrier)
+            except Exception as exc:  # pragma: no cover - auxiliary numbers only
+                aux[key] = {"error": str(exc)[:200]}
     # the same step replayed from CUDA graphs (one per input pair): removes launch gaps,
     # which dominate for the small configs
     graphs = []
@@ -548,10 +662,12 @@ def run_ours(args, rank, world, local):
                 "peak_source": f"{peak_kind} hbm copy"}
     # K2 is FP32-issue-bound, not HBM-bound: its compute roofline against the measured
     # 3-register FFMA throughput of this GPU (tools/ubench/ffma2.cu: 49.3 TFLOP/s).  FLOPs per
-    # cell of this kernel's formulation from its executed SASS mix (FFMA 769, FMUL 347,
-    # FADD 90 warp-instructions per cell x 32 lanes; profiles/r1_kernels_cfg3_ncu.txt)
+    # cell of this kernel's formulation from its executed SASS mix (predicated-on thread
+    # instructions per cell / 32: FFMA 659.7, FMUL 271.8, FADD 85.4; ncu
+    # smsp__sass_thread_inst_executed_op_{ffma,fmul,fadd}_pred_on of the element kernel in
+    # profiles/r1_kernels_cfg3_ncu.txt)
     if "K2_residual" in per_kernel:
-        k2_flop = 32 * (2 * 769 + 347 + 90) * step.level.n_cells
+        k2_flop = 32 * (2 * 659.7 + 271.8 + 85.4) * step.level.n_cells
         ach2 = k2_flop / (per_kernel["K2_residual"]["ms"] / 1e3) / 1e12
         per_kernel["K2_residual"]["fp32_roofline"] = {
             "bound": "fp32 issue", "achieved": ach2, "peak": 49.3, "unit": "TFLOP/s",

@@ -11,9 +11,10 @@
 // contiguous, coalesced stream (the row block is the D2H / disk payload).
 //
 // Column statistics (sum, centred sum of squares M2, min, max per column) for the dataset
-// sidecar are reduced in a fixed order — per-block two-pass partials over fixed row
-// ranges, then an in-order pairwise (Chan) combination over the blocks — so they are
-// deterministic and free of the E[x^2] - mean^2 cancellation.
+// sidecar are reduced in a fixed order — per-block partials over fixed row ranges (one
+// pass, sums shifted by the block's first row, M2 = q - s^2/n), then an in-order pairwise
+// (Chan) combination over the blocks — so they are deterministic and free of the
+// E[x^2] - mean^2 cancellation.
 #include <cfloat>
 #include "common.cuh"
 
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(256) dataset_rows_kernel(
   }
 }
 
-constexpr int kStatBlocks = 256;  // fixed row partition of the column statistics
+constexpr int kStatBlocks = 2048;  // fixed row partition of the column statistics
 
 // partial[b][4][w]: block b reduces rows [b*chunk, (b+1)*chunk) column by column
 __global__ void __launch_bounds__(256) column_stats_partial_kernel(const double* __restrict__ rows,
@@ -66,16 +67,19 @@ __global__ void __launch_bounds__(256) column_stats_partial_kernel(const double*
   double* pb = partial + (int64_t)blockIdx.x * 4 * w;
   for (int c = threadIdx.x; c < w; c += blockDim.x) {
     double s = 0.0, q = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+    const double shift = r1 > r0 ? __ldg(rows + r0 * w + c) : 0.0;
     for (int64_t i = r0; i < r1; ++i) {
       const double v = __ldg(rows + i * w + c);
-      s += v;
+      const double d = v - shift;
+      s += d;
+      q = fma(d, d, q);
       mn = fmin(mn, v);
       mx = fmax(mx, v);
     }
-    const double mean = r1 > r0 ? s / (double)(r1 - r0) : 0.0;
-    for (int64_t i = r0; i < r1; ++i) {
-      const double d = __ldg(rows + i * w + c) - mean;
-      q = fma(d, d, q);
+    const int64_t n_b = r1 - r0;
+    if (n_b > 0) {
+      q = fmax(q - s * s / (double)n_b, 0.0);   // centred M2 of the block
+      s += shift * (double)n_b;
     }
     pb[c] = s;
     pb[w + c] = q;
@@ -84,35 +88,51 @@ __global__ void __launch_bounds__(256) column_stats_partial_kernel(const double*
   }
 }
 
+// (n, sum, M2) pairwise combination (Chan et al.)
+struct ColAcc {
+  double n, s, q, mn, mx;
+};
+__device__ __forceinline__ ColAcc col_merge(const ColAcc& a, const ColAcc& b) {
+  if (a.n == 0.0) return b;
+  if (b.n == 0.0) return a;
+  const double n = a.n + b.n;
+  const double delta = b.s / b.n - a.s / a.n;
+  return {n, a.s + b.s, a.q + b.q + delta * delta * (a.n * b.n / n), fmin(a.mn, b.mn),
+          fmax(a.mx, b.mx)};
+}
+
+// one warp per column: lane l merges the partials of a fixed contiguous block range in
+// order, then a fixed butterfly merges the lanes (a fixed tree: deterministic)
 __global__ void __launch_bounds__(256) column_stats_final_kernel(const double* __restrict__ partial,
                                                                   int64_t n, int nb, int w,
                                                                   double* __restrict__ stats) {
   const int64_t chunk = (n + nb - 1) / nb;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < w; c += gridDim.x * blockDim.x) {
-    double s = 0.0, q = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
-    int64_t na = 0;
-    for (int b = 0; b < nb; ++b) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int per = (nb + 31) / 32;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < w; c += warps) {
+    ColAcc acc{0.0, 0.0, 0.0, DBL_MAX, -DBL_MAX};
+    for (int b = lane * per; b < nb && b < (lane + 1) * per; ++b) {
       const int64_t r0 = b * chunk, r1 = r0 + chunk < n ? r0 + chunk : n;
-      const int64_t nbr = r1 > r0 ? r1 - r0 : 0;
-      if (nbr == 0) continue;
+      if (r1 <= r0) continue;
       const double* pb = partial + (int64_t)b * 4 * w;
-      // Chan et al.: M2 = M2_a + M2_b + delta^2 n_a n_b / (n_a + n_b)
-      const double sb = pb[c];
-      if (na > 0) {
-        const double delta = sb / (double)nbr - s / (double)na;
-        q += pb[w + c] + delta * delta * ((double)na * (double)nbr / (double)(na + nbr));
-      } else {
-        q = pb[w + c];
-      }
-      s += sb;
-      na += nbr;
-      mn = fmin(mn, pb[2 * w + c]);
-      mx = fmax(mx, pb[3 * w + c]);
+      acc = col_merge(acc, ColAcc{(double)(r1 - r0), pb[c], pb[w + c], pb[2 * w + c], pb[3 * w + c]});
     }
-    stats[c] = s;
-    stats[w + c] = q;
-    stats[2 * w + c] = mn;
-    stats[3 * w + c] = mx;
+    for (int o = 1; o < 32; o <<= 1) {   // partner lane ^ o; the lower lane is "a"
+      ColAcc other;
+      other.n = __shfl_xor_sync(0xffffffffu, acc.n, o);
+      other.s = __shfl_xor_sync(0xffffffffu, acc.s, o);
+      other.q = __shfl_xor_sync(0xffffffffu, acc.q, o);
+      other.mn = __shfl_xor_sync(0xffffffffu, acc.mn, o);
+      other.mx = __shfl_xor_sync(0xffffffffu, acc.mx, o);
+      acc = (lane & o) ? col_merge(other, acc) : col_merge(acc, other);
+    }
+    if (lane == 0) {
+      stats[c] = acc.s;
+      stats[w + c] = acc.q;
+      stats[2 * w + c] = acc.mn;
+      stats[3 * w + c] = acc.mx;
+    }
   }
 }
 
@@ -144,8 +164,8 @@ extern "C" int32_t dnnmg_column_stats(const double* rows, int64_t n, int32_t w, 
                 "column_stats: null argument or bad shape");
   column_stats_partial_kernel<<<kStatBlocks, 256, 0, as_stream(s)>>>(rows, n, w, scratch);
   DNNMG_CHECK_LAUNCH("column_stats_partial_kernel");
-  column_stats_final_kernel<<<(w + 255) / 256, 256, 0, as_stream(s)>>>(scratch, n, kStatBlocks,
-                                                                      w, stats);
+  column_stats_final_kernel<<<(w + 7) / 8, 256, 0, as_stream(s)>>>(scratch, n, kStatBlocks, w,
+                                                                  stats);
   DNNMG_CHECK_LAUNCH("column_stats_final_kernel");
   return DNNMG_OK;
 }

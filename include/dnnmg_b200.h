@@ -266,9 +266,10 @@ typedef struct {
   const int32_t* dof_cell_ptr;   /* [n_dofs+1] CSR dof -> (cell*ndl + i), ascending: the */
   const int32_t* dof_cell_idx;   /*   order of np.bincount over cell_dofs */
   const double* weight;          /* [n_dofs] 1 / multiplicity */
-  const double* inv;             /* [n_cells][ndl][ndl] inverted blocks (dnnmg_vanka_setup) */
+  const double* inv;             /* [n_cells][ndl][ndl] inverted blocks, TRANSPOSED (column j of
+                                    the inverse contiguous), as written by dnnmg_vanka_setup */
 } dnnmg_vanka_t;
-/* inv[c] = (J.data[flat_pos[c*ndl*ndl ...]] as an ndl x ndl block)^-1 in float64
+/* inv[c] = transpose of (J.data[flat_pos[c*ndl*ndl ...]] as an ndl x ndl block)^-1, float64
  * (Gauss-Jordan, partial pivoting); a singular block is retried with a 1e-12 diagonal
  * shift: flags[c] = 0 regular, 1 shifted (the reference's `flagged`), 2 singular. */
 int32_t dnnmg_vanka_setup(int32_t n_cells, int32_t ndl, const double* csr_data,

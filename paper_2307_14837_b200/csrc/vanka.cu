@@ -115,8 +115,13 @@ __global__ void __launch_bounds__(kVankaThreads) vanka_invert_kernel(
         }
       __syncthreads();
     }
+    // stored transposed (column j of the inverse is contiguous): the apply kernel's
+    // thread-per-row loads are then coalesced
     double* out = inv + (int64_t)c * nn;
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) out[e] = A[e];
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const int j = e / ndl, i = e - j * ndl;
+      out[e] = A[i * ndl + j];
+    }
     __syncthreads();
   }
 }
@@ -139,22 +144,26 @@ __global__ void __launch_bounds__(256) csr_residual_kernel(int n, const int32_t*
   }
 }
 
-// dl[c] = inv[c] * r[dofs[c]]; one CTA per cell, one warp per output row group
-__global__ void __launch_bounds__(kVankaThreads) vanka_apply_kernel(
-    int n_cells, int ndl, const int32_t* __restrict__ dofs, const double* __restrict__ inv,
+// dl[c] = inv[c] * r[dofs[c]]; one CTA of kApplyThreads per cell, thread i = output row i,
+// reading the transposed inverse column by column (coalesced), r[dofs] staged in SMEM
+constexpr int kApplyThreads = 128;
+__global__ void __launch_bounds__(kApplyThreads) vanka_apply_kernel(
+    int n_cells, int ndl, const int32_t* __restrict__ dofs, const double* __restrict__ invT,
     const double* __restrict__ r, double* __restrict__ dl) {
   extern __shared__ double rl[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
   for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
     for (int i = threadIdx.x; i < ndl; i += blockDim.x) rl[i] = r[dofs[(int64_t)c * ndl + i]];
     __syncthreads();
-    const double* M = inv + (int64_t)c * ndl * ndl;
-    for (int i = warp; i < ndl; i += nw) {
-      double s = 0.0;
-      for (int j = lane; j < ndl; j += 32) s = fma(M[(int64_t)i * ndl + j], rl[j], s);
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) dl[(int64_t)c * ndl + i] = s;
+    const double* M = invT + (int64_t)c * ndl * ndl;
+    for (int i = threadIdx.x; i < ndl; i += blockDim.x) {
+      double s0 = 0.0, s1 = 0.0;
+      int j = 0;
+      for (; j + 1 < ndl; j += 2) {
+        s0 = fma(__ldg(M + (int64_t)j * ndl + i), rl[j], s0);
+        s1 = fma(__ldg(M + (int64_t)(j + 1) * ndl + i), rl[j + 1], s1);
+      }
+      if (j < ndl) s0 = fma(__ldg(M + (int64_t)j * ndl + i), rl[j], s0);
+      dl[(int64_t)c * ndl + i] = s0 + s1;
     }
     __syncthreads();
   }
@@ -214,8 +223,8 @@ extern "C" int32_t dnnmg_vanka_smooth(const dnnmg_vanka_t* V, const dnnmg_csr_t*
         J->n_rows, J->indptr, J->indices, J->data, x, b, r);
     DNNMG_CHECK_LAUNCH("csr_residual_kernel");
     if (V->n_cells > 0) {
-      const int grid = V->n_cells < 8 * kSMs ? V->n_cells : 8 * kSMs;
-      vanka_apply_kernel<<<grid, kVankaThreads, sizeof(double) * V->ndl, st>>>(
+      const int grid = V->n_cells < 16 * kSMs ? V->n_cells : 16 * kSMs;
+      vanka_apply_kernel<<<grid, kApplyThreads, sizeof(double) * V->ndl, st>>>(
           V->n_cells, V->ndl, V->cell_dofs, V->inv, r, dl);
       DNNMG_CHECK_LAUNCH("vanka_apply_kernel");
     }

@@ -71,10 +71,13 @@ class VankaData:
         self.n_cells, self.ndl = nc, ndl
         self.csr = DeviceCsr.get(J)
         flat = torch.from_numpy(np.ascontiguousarray(asm.flat_pos, dtype=np.int64)).to(dv.device())
-        self.inv = torch.empty((nc, ndl, ndl), dtype=torch.float64, device=dv.device())
+        # the device keeps the inverses transposed (coalesced block solves); .inv is the
+        # reference's [n_cells, ndl, ndl] view
+        self._invT = torch.empty((nc, ndl, ndl), dtype=torch.float64, device=dv.device())
+        self.inv = self._invT.transpose(1, 2)
         flags = torch.zeros(max(nc, 1), dtype=torch.int32, device=dv.device())
         _lib.call("dnnmg_vanka_setup", nc, ndl, dv.ptr(self.csr.data), dv.ptr(flat),
-                  dv.ptr(self.inv), dv.ptr(flags), dv.stream_handle())
+                  dv.ptr(self._invT), dv.ptr(flags), dv.stream_handle())
         f = flags[:nc].cpu().numpy()
         if np.any(f == 2):
             raise np.linalg.LinAlgError("Singular matrix")
@@ -88,7 +91,7 @@ class VankaData:
         self._idx = _i32(order)
         self._w = _f64(self.weight)
         self.struct = _lib.Vanka(nc, ndl, self.ndof, dv.ptr(self._dofs_d), dv.ptr(self._ptr),
-                                 dv.ptr(self._idx), dv.ptr(self._w), dv.ptr(self.inv))
+                                 dv.ptr(self._idx), dv.ptr(self._w), dv.ptr(self._invT))
         self._r = torch.empty(self.ndof, dtype=torch.float64, device=dv.device())
         self._dl = torch.empty(max(nc * ndl, 1), dtype=torch.float64, device=dv.device())
 

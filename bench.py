@@ -70,7 +70,7 @@ def default_precision(cfg_name):
     Widths the tensor-core kernel does not cover (config 2: 1024 -> 512) use the
     fp32 FFMA MLP."""
     from paper_2307_14837_b200 import synthetic
-    return "f16x3" if synthetic.CONFIGS[cfg_name]["hidden"] == 256 else "fp32"
+    return "f16x3"
 
 
 # ---------------------------------------------------------------------------

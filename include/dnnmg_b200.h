@@ -212,6 +212,14 @@ int32_t dnnmg_mlp_packed_bytes(const dnnmg_mlp_t* m, int64_t* bytes);
 int32_t dnnmg_mlp_pack(const dnnmg_mlp_t* m, void* packed, dnnmg_stream_t stream);
 int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
                           dnnmg_stream_t stream);
+/* Widths the fused per-tile kernel does not hold on chip (tensor-core modes with
+ * n_hidden != 256, n_in > 256 or n_out > 256; n_hidden % 32 == 0) run layer by layer
+ * (one tcgen05 GEMM per layer with the BN/activation/skip epilogue fused, activations in
+ * HBM in the split canonical operand layout), which needs a caller-owned device workspace
+ * of dnnmg_mlp_workspace_bytes(m, n_rows) bytes (0: none needed). */
+int32_t dnnmg_mlp_workspace_bytes(const dnnmg_mlp_t* m, int64_t n_rows, int64_t* bytes);
+int32_t dnnmg_mlp_forward_ws(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
+                             void* workspace, dnnmg_stream_t stream);
 
 /* K3 fused into K4 (tensor-core modes, 8*npp + n_geo <= 256): the network input rows
  * [x~ | r | geometry] are gathered straight into the layer-0 operand; X is never stored. */
@@ -290,6 +298,7 @@ typedef struct {
   float* Y;         /* [n_patches][n_out] */
   float* d;         /* [4*n_fine] */
   float* x_mid;     /* [4*n_mid] intermediate level for J = 2, else NULL */
+  void* mlp_ws;     /* dnnmg_mlp_workspace_bytes(m, n_patches) bytes, or NULL when 0 */
 } dnnmg_step_buffers_t;
 
 /* prolongations: J entries (levels L..L+J-1); bc: Dirichlet data of the fine level. */

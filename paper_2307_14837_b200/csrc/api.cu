@@ -37,6 +37,11 @@ int32_t launch_mlp_tc(const dnnmg_mlp_t*, const float*, int64_t, float*, cudaStr
 int32_t launch_mlp_tc_gather(const dnnmg_mlp_t*, const dnnmg_patchset_t*, const float*,
                              const float*, float*, cudaStream_t);
 int32_t mlp_tc_gather_mode(const dnnmg_mlp_t*, const dnnmg_patchset_t*);
+int32_t mlp_layered_supported(const dnnmg_mlp_t*);
+int32_t mlp_layered_packed_bytes(const dnnmg_mlp_t*, int64_t*);
+int32_t mlp_layered_workspace_bytes(const dnnmg_mlp_t*, int64_t, int64_t*);
+int32_t launch_mlp_layered_pack(const dnnmg_mlp_t*, void*, cudaStream_t);
+int32_t launch_mlp_layered(const dnnmg_mlp_t*, const float*, int64_t, float*, void*, cudaStream_t);
 
 static int32_t check_mlp(const dnnmg_mlp_t* m) {
   DNNMG_REQUIRE(m, DNNMG_ERR_ARG, "mlp: null model");
@@ -134,7 +139,10 @@ int32_t dnnmg_mlp_packed_bytes(const dnnmg_mlp_t* m, int64_t* bytes) {
     *bytes = 0;
     return DNNMG_OK;
   }
-  return mlp_tc_packed_bytes(m, bytes);
+  if (mlp_tc_supported(m)) return mlp_tc_packed_bytes(m, bytes);
+  DNNMG_REQUIRE(mlp_layered_supported(m), DNNMG_ERR_UNSUPPORTED,
+                "mlp: tensor-core modes need n_hidden %% 32 == 0");
+  return mlp_layered_packed_bytes(m, bytes);
 }
 
 int32_t dnnmg_mlp_pack(const dnnmg_mlp_t* m, void* packed, dnnmg_stream_t s) {
@@ -142,7 +150,32 @@ int32_t dnnmg_mlp_pack(const dnnmg_mlp_t* m, void* packed, dnnmg_stream_t s) {
   if (st) return st;
   if (m->precision == DNNMG_PREC_FP32) return DNNMG_OK;
   DNNMG_REQUIRE(packed, DNNMG_ERR_ARG, "mlp_pack: null buffer");
-  return launch_mlp_tc_pack(m, packed, as_stream(s));
+  if (mlp_tc_supported(m)) return launch_mlp_tc_pack(m, packed, as_stream(s));
+  return launch_mlp_layered_pack(m, packed, as_stream(s));
+}
+
+int32_t dnnmg_mlp_workspace_bytes(const dnnmg_mlp_t* m, int64_t n_rows, int64_t* bytes) {
+  int32_t st = check_mlp(m);
+  if (st) return st;
+  DNNMG_REQUIRE(bytes && n_rows >= 0, DNNMG_ERR_ARG, "mlp_workspace_bytes: bad argument");
+  *bytes = 0;
+  if (m->precision == DNNMG_PREC_FP32 || mlp_tc_supported(m)) return DNNMG_OK;
+  DNNMG_REQUIRE(mlp_layered_supported(m), DNNMG_ERR_UNSUPPORTED,
+                "mlp: tensor-core modes need n_hidden %% 32 == 0");
+  return mlp_layered_workspace_bytes(m, n_rows, bytes);
+}
+
+int32_t dnnmg_mlp_forward_ws(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
+                             void* workspace, dnnmg_stream_t s) {
+  int32_t st = check_mlp(m);
+  if (st) return st;
+  DNNMG_REQUIRE(X && Y, DNNMG_ERR_ARG, "mlp_forward: null argument");
+  DNNMG_REQUIRE(n_rows >= 0, DNNMG_ERR_ARG, "mlp_forward: negative row count");
+  if (n_rows == 0) return DNNMG_OK;
+  if (m->precision == DNNMG_PREC_FP32) return launch_mlp_simt(m, X, n_rows, Y, as_stream(s));
+  DNNMG_REQUIRE(m->packed, DNNMG_ERR_ARG, "mlp_forward: tensor-core mode needs packed weights");
+  if (mlp_tc_supported(m)) return launch_mlp_tc(m, X, n_rows, Y, as_stream(s));
+  return launch_mlp_layered(m, X, n_rows, Y, workspace, as_stream(s));
 }
 
 int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
@@ -155,7 +188,8 @@ int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, 
   if (m->precision == DNNMG_PREC_FP32) return launch_mlp_simt(m, X, n_rows, Y, as_stream(s));
   DNNMG_REQUIRE(m->packed, DNNMG_ERR_ARG, "mlp_forward: tensor-core mode needs packed weights");
   DNNMG_REQUIRE(mlp_tc_supported(m), DNNMG_ERR_UNSUPPORTED,
-                "mlp_forward: tensor-core mode supports n_in <= 256, n_hidden == 256, n_out <= 256");
+                "mlp_forward: this width runs on the layered tensor-core kernel, which needs a "
+                "workspace: use dnnmg_mlp_forward_ws");
   return launch_mlp_tc(m, X, n_rows, Y, as_stream(s));
 }
 
@@ -226,7 +260,7 @@ int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_d
     rc = launch_mlp_tc_gather(m, ps, buf->x_tilde, buf->r, buf->Y, st);
   } else {
     rc = launch_gather(ps, buf->x_tilde, buf->r, buf->X, st);
-    if (!rc) rc = dnnmg_mlp_forward(m, buf->X, ps->n_patches, buf->Y, s);
+    if (!rc) rc = dnnmg_mlp_forward_ws(m, buf->X, ps->n_patches, buf->Y, buf->mlp_ws, s);
   }
   if (rc) return rc;
   return launch_scatter_update(ps, buf->Y, fine->dof_mask, buf->x_tilde, scale, buf->d, x_corr, st);

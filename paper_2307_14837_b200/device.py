@@ -305,9 +305,23 @@ class DeviceModel:
             self.struct.packed = ptr(self.packed)
             _lib.call("dnnmg_mlp_pack", ctypes.byref(self.struct), ptr(self.packed), stream_handle())
 
+        self._ws = None
+
+    def workspace(self, n_rows):
+        """Device workspace of the layered tensor-core kernel (None when not needed),
+        grown on demand and kept for later calls."""
+        nbytes = ctypes.c_int64(0)
+        _lib.call("dnnmg_mlp_workspace_bytes", ctypes.byref(self.struct), int(n_rows),
+                  ctypes.byref(nbytes))
+        if nbytes.value == 0:
+            return None
+        if self._ws is None or self._ws.numel() < nbytes.value:
+            self._ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=device())
+        return self._ws
+
     def forward(self, X, n_rows, Y):
-        _lib.call("dnnmg_mlp_forward", ctypes.byref(self.struct), ptr(X), int(n_rows), ptr(Y),
-                  stream_handle())
+        _lib.call("dnnmg_mlp_forward_ws", ctypes.byref(self.struct), ptr(X), int(n_rows), ptr(Y),
+                  ptr(self.workspace(n_rows)), stream_handle())
 
 
 def dirichlet_codes(space, t, bcs):

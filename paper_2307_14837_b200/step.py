@@ -73,9 +73,11 @@ class CorrectionStep:
                               output_width(self.patchset)), dtype=f, device=dev)
         self.x_mid = (torch.empty(4 * self.prolongs[0].n_fine, dtype=f, device=dev)
                       if J == 2 else None)
+        self.mlp_ws = (self.model.workspace(self.ps.n_patches)
+                       if self.model is not None and not self.fused_gather else None)
         self.buf = _lib.StepBuffers(dv.ptr(self.x_tilde), dv.ptr(self.r), dv.ptr(self.elem),
                                     dv.ptr(self.X), dv.ptr(self.Y), dv.ptr(self.d),
-                                    dv.ptr(self.x_mid))
+                                    dv.ptr(self.x_mid), dv.ptr(self.mlp_ws))
         self._t = None
         self.set_time(t)
         self.graph = None
@@ -112,8 +114,9 @@ class CorrectionStep:
         t.X = torch.empty(0 if self.fused_gather else self.X.numel(), dtype=f, device=dev)
         t.Y = torch.empty_like(self.Y)
         t.x_mid = None if self.x_mid is None else torch.empty_like(self.x_mid)
+        t.mlp_ws = None if self.mlp_ws is None else torch.empty_like(self.mlp_ws)
         t.buf = _lib.StepBuffers(dv.ptr(t.x_tilde), dv.ptr(t.r), dv.ptr(t.elem), dv.ptr(t.X),
-                                 dv.ptr(t.Y), dv.ptr(t.d), dv.ptr(t.x_mid))
+                                 dv.ptr(t.Y), dv.ptr(t.d), dv.ptr(t.x_mid), dv.ptr(t.mlp_ws))
         t.graph = None
         return t
 
@@ -176,8 +179,8 @@ class CorrectionStep:
             return
         _lib.call("dnnmg_gather", ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde),
                   dv.ptr(self.r), dv.ptr(self.X), s)
-        _lib.call("dnnmg_mlp_forward", ctypes.byref(self.model.struct), dv.ptr(self.X),
-                  self.ps.n_patches, dv.ptr(self.Y), s)
+        _lib.call("dnnmg_mlp_forward_ws", ctypes.byref(self.model.struct), dv.ptr(self.X),
+                  self.ps.n_patches, dv.ptr(self.Y), dv.ptr(self.mlp_ws), s)
 
     def stage_names(self):
         """Labels of the stages run_staged() brackets with events."""

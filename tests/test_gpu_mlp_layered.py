@@ -1,0 +1,77 @@
+"""Layer-major tcgen05 MLP (csrc/mlp_layer.cu) for the widths the fused per-tile kernel
+does not hold on chip — BASELINE config 2 (1024 -> 512x3 -> 375) and the config-4 sweep
+(174 -> {128, 512, 1024}x3 -> 81) — against the float64 oracle MLP (net.py:124-159), with
+ragged row counts, BN statistics and input normalisation, tanh and relu.  Tolerances as
+for the fused kernel: fp32-level (1e-5) in f16x3 / tf32x3, 2e-2 in bf16."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2307_14837_b200 import device as dv, net  # noqa: E402
+
+TOL = {"f16x3": 1e-5, "tf32x3": 1e-5, "bf16": 2e-2}
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a, float) - b) / np.linalg.norm(b)
+
+
+def make_model(n_in, H, depth, n_out, act, bn, seed):
+    rng = np.random.default_rng(seed)
+    m = net.MlpModel(net.Architecture(n_in, H, depth, n_out), activation=act, seed=seed)
+    dims = [n_in] + [H] * depth + [n_out]
+    m.W = [(rng.uniform(-1, 1, (a, b)) * np.sqrt(6.0 / (a + b))).astype(np.float32).astype(float)
+           for a, b in zip(dims[:-1], dims[1:])]
+    if bn:
+        m.gamma = [rng.uniform(0.5, 1.5, H) for _ in range(depth)]
+        m.beta = [rng.normal(0, 0.1, H) for _ in range(depth)]
+        m.running_mean = [rng.normal(0, 0.2, H) for _ in range(depth)]
+        m.running_var = [rng.uniform(0.5, 2.0, H) for _ in range(depth)]
+        m.set_input_norm(rng.normal(0, 0.3, n_in), rng.uniform(0.5, 2.0, n_in))
+    m.eval()
+    return m
+
+
+@pytest.mark.parametrize("precision", ["f16x3", "tf32x3", "bf16"])
+@pytest.mark.parametrize("shape", [(1024, 512, 3, 375, "tanh", 777, True),
+                                   (174, 128, 3, 81, "tanh", 300, False),
+                                   (174, 512, 3, 81, "relu", 1000, True),
+                                   (174, 1024, 3, 81, "tanh", 257, False),
+                                   (240, 256, 2, 300, "tanh", 129, True)])
+def test_layered_mlp_matches_oracle(precision, shape):
+    from oracle import dnnmg_oracle as orc
+    n_in, H, depth, n_out, act, rows, bn = shape
+    if precision == "f16x3" and act == "relu":
+        pytest.skip("f16x3 assumes bounded activations (tanh); relu models use tf32x3")
+    m = make_model(n_in, H, depth, n_out, act, bn, rows + H)
+    rng = np.random.default_rng(rows)
+    X = rng.standard_normal((rows, n_in)).astype(np.float32).astype(float)
+    ref = orc.mlp_forward(orc.Mlp(m.W, act, m.gamma, m.beta, m.running_mean, m.running_var,
+                                  m.input_mean, m.input_std), X)
+    Y = net.forward(m, X, precision=precision)
+    tol = TOL[precision]
+    if precision == "tf32x3" and H >= 1024:
+        # the tensor core's fp32 accumulation of the tf32 products rounds per K step, so the
+        # 3-pass error grows with K: 1.2e-5 measured at K = 1024 (3.0e-6 at K = 256)
+        tol = 2e-5
+    assert rel(Y, ref) < tol, rel(Y, ref)
+
+
+def test_layered_row_chunks_are_independent():
+    """More rows than one pass (2^19): the chunked run equals separate runs bitwise."""
+    m = make_model(174, 128, 3, 81, "tanh", False, 5)
+    dm = dv.DeviceModel(m, "f16x3")
+    n = (1 << 19) + 1000
+    X = torch.randn((n, 174), device="cuda")
+    Y = torch.empty((n, 81), device="cuda")
+    dm.forward(X, n, Y)
+    Y2 = torch.empty((1000, 81), device="cuda")
+    dm.forward(X[-1000:].contiguous(), 1000, Y2)
+    torch.cuda.synchronize()
+    assert torch.equal(Y[-1000:], Y2)
+    assert torch.isfinite(Y).all()

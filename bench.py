@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-aux", action="store_true", help="skip the next-row aux timings")
+    ap.add_argument("--mlp-sweep", action="store_true",
+                    help="BASELINE config 4: isolated patch-MLP sweep (one JSON line)")
+    ap.add_argument("--sweep-batches", default="1024,16384,262144,4194304")
     return ap.parse_args()
 
 
@@ -717,9 +720,68 @@ def run_ours(args, rank, world, local):
         tdist.destroy_process_group()
 
 
+def run_mlp_sweep(args):
+    """BASELINE config 4: isolated patch-MLP throughput, 174 -> H x3 -> 81 tanh, Xavier
+    weights, N(0,1) inputs resident in HBM, for H in {128, 256, 512, 1024}, batches
+    2^10 .. 2^22 rows and the tensor-core modes (fp32-accurate f16x3 / tf32x3, bf16).
+    H = 256 runs the fused per-tile kernel, the other widths the layer-major kernel.
+    One JSON line: rows/s, TFLOP/s of the reference FLOPs and the fraction of the mode's
+    tensor peak per point (CUDA events, median-free mean of K launches after W warm-ups)."""
+    import torch
+    from paper_2307_14837_b200 import device as dvm, synthetic
+    from paper_2307_14837_b200.net import Architecture, MlpModel
+    peaks, peak_kind = load_peaks()
+    modes = (args.precision,) if args.precision else ("f16x3", "tf32x3", "bf16")
+    hs = (128, 256, 512, 1024)
+    batches = tuple(int(b) for b in args.sweep_batches.split(","))
+    out = []
+    for H in hs:
+        dims = [174, H, H, H, 81]
+        model = MlpModel(Architecture(174, H, 3, 81), activation="tanh")
+        model.W = synthetic.xavier_weights(dims, 4 + H)
+        model.eval()
+        flop = 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
+        for mode in modes:
+            dm = dvm.DeviceModel(model, mode)
+            for B in batches:
+                X = torch.randn((B, 174), device="cuda")
+                Y = torch.empty((B, 81), device="cuda")
+                dm.workspace(B)
+                for _ in range(max(args.warmup, 3)):
+                    dm.forward(X, B, Y)
+                reps = max(3, min(args.steps, int(2 ** 22 // B) + 3))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(reps):
+                    dm.forward(X, B, Y)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                tf = flop * B / (ms / 1e3) / 1e12
+                peak = {"bf16": peaks["bf16_tflops_sustained"],
+                        "f16x3": peaks["bf16_tflops_sustained"] / 3.0,
+                        "tf32x3": peaks["bf16_tflops_sustained"] / 6.0}[mode]
+                out.append({"H": H, "mode": mode, "batch": B, "ms": ms, "rows/s": B / (ms / 1e3),
+                            "TFLOP/s": tf, "frac": tf / peak,
+                            "kernel": "fused" if H == 256 else "layered"})
+                del X, Y
+            del dm
+    line = {"metric": "patch-MLP rows/s and TFLOP/s (BASELINE config 4)", "n_gpus": 1,
+            "data": "synthetic", "dtype": "fp32 accumulate",
+            "config": {"workload": "cfg4", "mlp": "174 -> H x3 -> 81 tanh", "H": list(hs),
+                       "batches": list(batches), "modes": list(modes)},
+            "peak_source": f"{peak_kind} bf16 sustained; f16x3 = /3, tf32x3 = /6",
+            "points": out}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.mlp_sweep:
+        run_mlp_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

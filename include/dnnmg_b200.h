@@ -225,6 +225,12 @@ int32_t dnnmg_mlp_forward_ws(const dnnmg_mlp_t* m, const float* X, int64_t n_row
  * [x~ | r | geometry] are gathered straight into the layer-0 operand; X is never stored. */
 int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
                                   const float* r, float* Y, dnnmg_stream_t stream);
+/* The same for every tensor-core width: the fused kernel when it applies, else the layered
+ * kernel with the layer-0 operand gathered from x~, r and the geometry (workspace as for
+ * dnnmg_mlp_forward_ws). */
+int32_t dnnmg_mlp_forward_patches_ws(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps,
+                                     const float* x, const float* r, float* Y, void* workspace,
+                                     dnnmg_stream_t stream);
 
 /* Which layer-0 source dnnmg_mlp_forward_patches uses for (m, ps): 1 = direct gather of
  * every (patch, slot) at the tile boundary, 2 = staged gather of each tile's distinct nodes

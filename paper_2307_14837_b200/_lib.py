@@ -96,6 +96,8 @@ EXPORTS = {
     "dnnmg_mlp_forward": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_i64, c_vp, c_vp]),
     "dnnmg_mlp_workspace_bytes": (c_i32, [ctypes.POINTER(Mlp), c_i64, ctypes.POINTER(c_i64)]),
     "dnnmg_mlp_forward_ws": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "dnnmg_mlp_forward_patches_ws": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet), c_vp,
+                                             c_vp, c_vp, c_vp, c_vp]),
     "dnnmg_mlp_forward_patches": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet), c_vp, c_vp,
                                           c_vp, c_vp]),
     "dnnmg_mlp_gather_mode": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet)]),

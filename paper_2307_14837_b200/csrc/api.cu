@@ -42,6 +42,8 @@ int32_t mlp_layered_packed_bytes(const dnnmg_mlp_t*, int64_t*);
 int32_t mlp_layered_workspace_bytes(const dnnmg_mlp_t*, int64_t, int64_t*);
 int32_t launch_mlp_layered_pack(const dnnmg_mlp_t*, void*, cudaStream_t);
 int32_t launch_mlp_layered(const dnnmg_mlp_t*, const float*, int64_t, float*, void*, cudaStream_t);
+int32_t launch_mlp_layered_patches(const dnnmg_mlp_t*, const dnnmg_patchset_t*, const float*,
+                                   const float*, float*, void*, cudaStream_t);
 
 static int32_t check_mlp(const dnnmg_mlp_t* m) {
   DNNMG_REQUIRE(m, DNNMG_ERR_ARG, "mlp: null model");
@@ -193,6 +195,26 @@ int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, 
   return launch_mlp_tc(m, X, n_rows, Y, as_stream(s));
 }
 
+static bool fused_gather(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps);
+static bool layered_gather(const dnnmg_mlp_t* m);
+
+int32_t dnnmg_mlp_forward_patches_ws(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps,
+                                     const float* x, const float* r, float* Y, void* workspace,
+                                     dnnmg_stream_t s) {
+  int32_t st = check_mlp(m);
+  if (st) return st;
+  DNNMG_REQUIRE(ps && ps->node_table && ps->geom && x && r && Y, DNNMG_ERR_ARG,
+                "mlp_forward_patches: null argument");
+  if (fused_gather(m, ps)) return dnnmg_mlp_forward_patches(m, ps, x, r, Y, s);
+  DNNMG_REQUIRE(layered_gather(m), DNNMG_ERR_UNSUPPORTED,
+                "mlp_forward_patches: needs a packed tensor-core model");
+  DNNMG_REQUIRE(m->n_out == 3 * ps->nodes_per_patch, DNNMG_ERR_ARCH,
+                "model architecture (%d outputs) does not match the patch layout (%d)", m->n_out,
+                3 * ps->nodes_per_patch);
+  if (ps->n_patches == 0) return DNNMG_OK;
+  return launch_mlp_layered_patches(m, ps, x, r, Y, workspace, as_stream(s));
+}
+
 int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
                                   const float* r, float* Y, dnnmg_stream_t s) {
   int32_t st = check_mlp(m);
@@ -223,9 +245,18 @@ static bool fused_gather(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps) {
          (ps == nullptr || (ps->n_geo % 4 == 0 && 8 * ps->nodes_per_patch + ps->n_geo <= 256));
 }
 
+static bool layered_gather(const dnnmg_mlp_t* m) {
+  return m->precision != DNNMG_PREC_FP32 && !mlp_tc_supported(m) && mlp_layered_supported(m) &&
+         m->packed;
+}
+
 int32_t dnnmg_correction_step_launches(int32_t J, const dnnmg_mlp_t* m) {
-  // J prolongations + element + node-sum + [gather] + mlp + scatter
-  return J + (fused_gather(m, nullptr) ? 4 : 5);
+  // J prolongations + element + node-sum + MLP stage + scatter; the MLP stage is one fused
+  // kernel, or (layered) epilogue affine + gathered layer-0 operand + one GEMM per layer,
+  // or (fp32 SIMT) gather + MLP
+  if (fused_gather(m, nullptr)) return J + 4;
+  if (layered_gather(m)) return J + 3 + 2 + m->depth + 1;
+  return J + 5;
 }
 
 int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_dirichlet_t* bc,
@@ -258,6 +289,8 @@ int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_d
   // (4) patch features, network, averaging scatter, update (driver.py:263-268)
   if (fused_gather(m, ps)) {
     rc = launch_mlp_tc_gather(m, ps, buf->x_tilde, buf->r, buf->Y, st);
+  } else if (layered_gather(m)) {
+    rc = launch_mlp_layered_patches(m, ps, buf->x_tilde, buf->r, buf->Y, buf->mlp_ws, st);
   } else {
     rc = launch_gather(ps, buf->x_tilde, buf->r, buf->X, st);
     if (!rc) rc = dnnmg_mlp_forward_ws(m, buf->X, ps->n_patches, buf->Y, buf->mlp_ws, s);

@@ -238,10 +238,31 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
 
 // layer-0 operand: (X - mean) / std of rows [r0, r0 + n) split into the canonical chunks;
 // one thread per (row, HC-column group); rows and columns past the data are zero
-template <int MODE>
-__global__ void __launch_bounds__(256) layer_input_kernel(const float* __restrict__ X, int64_t r0,
-                                                          int64_t n, int64_t n_rows_pad, int n_in,
-                                                          int n_kc, const float* __restrict__ mean,
+// patch source of the layer-0 rows (K3 fused into the layered MLP): row p =
+// [x~ of node_table[p][s] | r of node_table[p][s] | geom[p]] (patch_ops.py:49-53)
+struct PatchRows {
+  const int32_t* table;
+  const float* x;
+  const float* r;
+  const float* geom;
+  int npp, n_geo;
+};
+
+__device__ __forceinline__ float patch_value(const PatchRows& P, int64_t p, int col) {
+  const int nb = 4 * P.npp;
+  if (col < nb) return __ldg(P.x + 4 * (int64_t)__ldg(P.table + p * P.npp + (col >> 2)) + (col & 3));
+  if (col < 2 * nb) {
+    const int c = col - nb;
+    return __ldg(P.r + 4 * (int64_t)__ldg(P.table + p * P.npp + (c >> 2)) + (c & 3));
+  }
+  return __ldg(P.geom + p * P.n_geo + (col - 2 * nb));
+}
+
+template <int MODE, bool PATCH>
+__global__ void __launch_bounds__(256) layer_input_kernel(const float* __restrict__ X, PatchRows P,
+                                                          int64_t r0, int64_t n, int64_t n_rows_pad,
+                                                          int n_in, int n_kc,
+                                                          const float* __restrict__ mean,
                                                           const float* __restrict__ std_,
                                                           uint8_t* __restrict__ out) {
   using C = TcCfg<MODE>;
@@ -258,9 +279,12 @@ __global__ void __launch_bounds__(256) layer_input_kernel(const float* __restric
 #pragma unroll
     for (int e = 0; e < HC; ++e) {
       const int col = col0 + e;
-      v[e] = (r < n && col < n_in) ? (__ldg(X + (r0 + r) * n_in + col) - __ldg(mean + col)) /
-                                         __ldg(std_ + col)
-                                   : 0.f;
+      float x = 0.f;
+      if (r < n && col < n_in) {
+        if constexpr (PATCH) x = patch_value(P, r0 + r, col);
+        else x = __ldg(X + (r0 + r) * n_in + col);
+      }
+      v[e] = (r < n && col < n_in) ? (x - __ldg(mean + col)) / __ldg(std_ + col) : 0.f;
     }
     const int64_t t = r / kTcM;
     uint8_t* chunk = out + (t * n_kc + col0 / KC) * AST;
@@ -396,8 +420,8 @@ int32_t launch_mlp_layered_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t
 }
 
 template <int MODE>
-static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
-                            void* ws, cudaStream_t s) {
+static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, const PatchRows* P,
+                            int64_t n_rows, float* Y, void* ws, cudaStream_t s) {
   using C = TcCfg<MODE>;
   constexpr int NS = LCfg<MODE>::NS;
   constexpr size_t STG = (size_t)kTcM * C::KC * C::ESZ * C::PARTS +
@@ -424,8 +448,13 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows
     const int64_t n = n_rows - r0 < L.chunk_rows ? n_rows - r0 : L.chunk_rows;
     const int tiles = (int)((n + kTcM - 1) / kTcM);
     const int kc0 = L.K[0] / C::KC;
-    layer_input_kernel<MODE><<<grid_for((int64_t)tiles * kTcM * kc0 * 2, 256), 256, 0, s>>>(
-        X, r0, n, (int64_t)tiles * kTcM, m->n_in, kc0, m->in_mean, m->in_std, abuf[0]);
+    const int in_grid = grid_for((int64_t)tiles * kTcM * kc0 * 2, 256);
+    if (P)
+      layer_input_kernel<MODE, true><<<in_grid, 256, 0, s>>>(
+          nullptr, *P, r0, n, (int64_t)tiles * kTcM, m->n_in, kc0, m->in_mean, m->in_std, abuf[0]);
+    else
+      layer_input_kernel<MODE, false><<<in_grid, 256, 0, s>>>(
+          X, PatchRows{}, r0, n, (int64_t)tiles * kTcM, m->n_in, kc0, m->in_mean, m->in_std, abuf[0]);
     DNNMG_CHECK_LAUNCH("layer_input_kernel");
     for (int g = 0; g <= m->depth; ++g) {
       LayerArgs A{};
@@ -460,16 +489,32 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows
   return DNNMG_OK;
 }
 
-int32_t launch_mlp_layered(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y, void* ws,
-                           cudaStream_t s) {
+int32_t launch_mlp_layered_rows(const dnnmg_mlp_t* m, const float* X, const PatchRows* P,
+                                int64_t n_rows, float* Y, void* ws, cudaStream_t s) {
   DNNMG_REQUIRE(mlp_layered_supported(m) && m->packed, DNNMG_ERR_UNSUPPORTED,
                 "mlp: layered tensor-core mode needs packed weights and n_hidden %% 32 == 0");
   DNNMG_REQUIRE(ws, DNNMG_ERR_ARG, "mlp: the layered tensor-core MLP needs a workspace "
                 "(dnnmg_mlp_workspace_bytes)");
   if (n_rows == 0) return DNNMG_OK;
-  if (m->precision == DNNMG_PREC_BF16) return layered_mode<DNNMG_PREC_BF16>(m, X, n_rows, Y, ws, s);
-  if (m->precision == DNNMG_PREC_F16X3) return layered_mode<DNNMG_PREC_F16X3>(m, X, n_rows, Y, ws, s);
-  return layered_mode<DNNMG_PREC_TF32X3>(m, X, n_rows, Y, ws, s);
+  if (m->precision == DNNMG_PREC_BF16) return layered_mode<DNNMG_PREC_BF16>(m, X, P, n_rows, Y, ws, s);
+  if (m->precision == DNNMG_PREC_F16X3) return layered_mode<DNNMG_PREC_F16X3>(m, X, P, n_rows, Y, ws, s);
+  return layered_mode<DNNMG_PREC_TF32X3>(m, X, P, n_rows, Y, ws, s);
+}
+
+int32_t launch_mlp_layered(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y, void* ws,
+                           cudaStream_t s) {
+  return launch_mlp_layered_rows(m, X, nullptr, n_rows, Y, ws, s);
+}
+
+// K3 fused into the layered MLP: the layer-0 operand is gathered straight from x~, r and the
+// patch geometry (no X in HBM)
+int32_t launch_mlp_layered_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
+                                   const float* r, float* Y, void* ws, cudaStream_t s) {
+  DNNMG_REQUIRE(8 * ps->nodes_per_patch + ps->n_geo == m->n_in, DNNMG_ERR_ARCH,
+                "model architecture (%d inputs) does not match the patch layout (%d)", m->n_in,
+                8 * ps->nodes_per_patch + ps->n_geo);
+  PatchRows P{ps->node_table, x, r, ps->geom, ps->nodes_per_patch, ps->n_geo};
+  return launch_mlp_layered_rows(m, nullptr, &P, ps->n_patches, Y, ws, s);
 }
 
 }  // namespace dnnmg

@@ -66,15 +66,16 @@ class CorrectionStep:
         self.d = torch.empty(4 * nf, dtype=f, device=dev)
         self.x_corr = torch.empty(4 * nf, dtype=f, device=dev)
         self.elem = self.level.scratch()
+        # layered tensor-core MLP (other widths): the gather is fused into its layer-0 operand
+        self.layered = model is not None and precision != "fp32" and not self.fused_gather
         # X is only materialised when the gather is not fused into the MLP
-        n_x = 0 if (self.fused_gather or model is None) else self.ps.n_patches
+        n_x = 0 if (self.fused_gather or self.layered or model is None) else self.ps.n_patches
         self.X = torch.empty((n_x, input_width(self.patchset)), dtype=f, device=dev)
         self.Y = torch.empty((self.ps.n_patches if model is not None else 0,
                               output_width(self.patchset)), dtype=f, device=dev)
         self.x_mid = (torch.empty(4 * self.prolongs[0].n_fine, dtype=f, device=dev)
                       if J == 2 else None)
-        self.mlp_ws = (self.model.workspace(self.ps.n_patches)
-                       if self.model is not None and not self.fused_gather else None)
+        self.mlp_ws = self.model.workspace(self.ps.n_patches) if self.layered else None
         self.buf = _lib.StepBuffers(dv.ptr(self.x_tilde), dv.ptr(self.r), dv.ptr(self.elem),
                                     dv.ptr(self.X), dv.ptr(self.Y), dv.ptr(self.d),
                                     dv.ptr(self.x_mid), dv.ptr(self.mlp_ws))
@@ -111,7 +112,7 @@ class CorrectionStep:
         t.d = torch.empty_like(self.d)
         t.x_corr = torch.empty_like(self.x_corr)
         t.elem = torch.empty_like(self.elem)
-        t.X = torch.empty(0 if self.fused_gather else self.X.numel(), dtype=f, device=dev)
+        t.X = torch.empty_like(self.X)
         t.Y = torch.empty_like(self.Y)
         t.x_mid = None if self.x_mid is None else torch.empty_like(self.x_mid)
         t.mlp_ws = None if self.mlp_ws is None else torch.empty_like(self.mlp_ws)
@@ -172,10 +173,10 @@ class CorrectionStep:
 
     def predict_rows(self, s):
         """Y = network(patch rows of x~, r): fused gather+MLP or gather then MLP."""
-        if self.fused_gather:
-            _lib.call("dnnmg_mlp_forward_patches", ctypes.byref(self.model.struct),
+        if self.fused_gather or self.layered:
+            _lib.call("dnnmg_mlp_forward_patches_ws", ctypes.byref(self.model.struct),
                       ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde), dv.ptr(self.r),
-                      dv.ptr(self.Y), s)
+                      dv.ptr(self.Y), dv.ptr(self.mlp_ws), s)
             return
         _lib.call("dnnmg_gather", ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde),
                   dv.ptr(self.r), dv.ptr(self.X), s)
@@ -184,7 +185,7 @@ class CorrectionStep:
 
     def stage_names(self):
         """Labels of the stages run_staged() brackets with events."""
-        mid = ["K3K4_gather_mlp"] if self.fused_gather else ["K3_gather+K4_mlp"]
+        mid = ["K3K4_gather_mlp"] if (self.fused_gather or self.layered) else ["K3_gather+K4_mlp"]
         return ["K1_prolong"] * self.J + ["K2_residual"] + mid + ["K5_scatter"]
 
     def capture(self, x_coarse, b_prev):

@@ -4,10 +4,13 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
                     [--precision fp32|bf16|tf32x3|f16x3] [--impl ours|reference]
+                    [--no-e2e] [--no-cpu-baseline] [--no-aux]
+    python bench.py --mlp-sweep        # BASELINE config 4: isolated patch-MLP sweep
 
 Workload (default): BASELINE config 3 under the SURVEY §0.1 mapping — unit box,
 level L = 64x32x32 cells, J = 1: 524,288 patches, 4,276,737 fine Q2 nodes,
-MLP 240 -> 256x3 -> 81 tanh, seeded synthetic Fourier inputs, fp32.
+MLP 240 -> 256x3 -> 81 tanh, seeded synthetic Fourier inputs, fp32 arithmetic
+(the MLP in the fp32-accurate f16x3 tensor-core mode).
 
 A timed step is one full correction (driver.py:251-268): prolongate (K1) ->
 Dirichlet -> stab + residual (K2) -> patch gather (K3) -> patch MLP (K4) ->
@@ -19,10 +22,14 @@ buffers: x_L and b_prev copied H2D and x_corr copied D2H inside every step,
 pipelined by step.HostPipeline (copies of neighbouring steps overlap the
 kernels of the current one).
 
+`aux` times the rows around the step (next-step RHS, restriction, training-data
+rows + statistics, Vanka sweeps); they are not part of `value`.
+
 --impl reference times the CPU oracle port of the reference (oracle/,
 float64 numpy, all host threads) on a bounded sample of the same workload.
-Multi-GPU (torchrun): replicas of the single-GPU workload, one per rank
-("weak"), timed on the device, max over ranks.
+Multi-GPU (torchrun): the x-slab decomposition (slab.py), one config-sized slab
+per rank ("weak"), NCCL P2P halo exchange twice per step, timed on the device,
+max over ranks.
 """
 
 import argparse
@@ -70,9 +77,8 @@ def default_precision(cfg_name):
     """fp32-accuracy mode: every kernel in fp32, the MLP on tcgen05 with the
     3-pass fp16 split of scaled weights (f16x3: d within 1e-5 of the float64
     reference, tests/test_gpu_parity.py; tanh keeps activations in fp16 range).
-    Widths the tensor-core kernel does not cover (config 2: 1024 -> 512) use the
-    fp32 FFMA MLP."""
-    from paper_2307_14837_b200 import synthetic
+    Width 256 (configs 0, 1, 3) runs the fused per-tile kernel, config 2
+    (1024 -> 512x3 -> 375) the layer-major kernel."""
     return "f16x3"
 
 
@@ -704,7 +710,7 @@ def run_ours(args, rank, world, local):
                    "coarse_cells": int(np.prod(cfg["n_cells"])), "J": cfg["J"],
                    "mlp": f"{8 * step.ps.npp + 24}->{cfg['hidden']}x{cfg['depth']}->{3 * step.ps.npp} tanh",
                    "precision": precision, "l2": "inputs > L2 (4 cycled input pairs, 308 MB)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": "single GPU"},
         "e2e": e2e,
         "gpu_launches": int(step.launches * args.steps),
         "roofline": roof,

@@ -730,7 +730,7 @@ def run_mlp_sweep(args):
     """BASELINE config 4: isolated patch-MLP throughput, 174 -> H x3 -> 81 tanh, Xavier
     weights, N(0,1) inputs resident in HBM, for H in {128, 256, 512, 1024}, batches
     2^10 .. 2^22 rows and the tensor-core modes (fp32-accurate f16x3 / tf32x3, bf16).
-    H = 256 runs the fused per-tile kernel, the other widths the layer-major kernel.
+    H = 128 and 256 run the fused per-tile kernel, 512 and 1024 the layer-major kernel.
     One JSON line: rows/s, TFLOP/s of the reference FLOPs and the fraction of the mode's
     tensor peak per point (CUDA events, median-free mean of K launches after W warm-ups)."""
     import torch
@@ -770,7 +770,7 @@ def run_mlp_sweep(args):
                         "tf32x3": peaks["bf16_tflops_sustained"] / 6.0}[mode]
                 out.append({"H": H, "mode": mode, "batch": B, "ms": ms, "rows/s": B / (ms / 1e3),
                             "TFLOP/s": tf, "frac": tf / peak,
-                            "kernel": "fused" if H == 256 else "layered"})
+                            "kernel": "fused" if dvm.tc_fused_supported(model.arch) else "layered"})
                 del X, Y
             del dm
     line = {"metric": "patch-MLP rows/s and TFLOP/s (BASELINE config 4)", "n_gpus": 1,

@@ -241,7 +241,7 @@ int32_t dnnmg_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const u
 }
 
 static bool fused_gather(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps) {
-  return m->precision != DNNMG_PREC_FP32 && mlp_tc_supported(m) && m->packed &&
+  return m->precision != DNNMG_PREC_FP32 && mlp_tc_supported(m) && m->n_hidden == 256 && m->packed &&
          (ps == nullptr || (ps->n_geo % 4 == 0 && 8 * ps->nodes_per_patch + ps->n_geo <= 256));
 }
 

@@ -37,7 +37,8 @@
 
 namespace dnnmg {
 
-constexpr int kTcH = 256;
+constexpr int kTcH = 256;   // hidden width of the largest instantiation
+constexpr int kTcIn = 256;  // network inputs the fused kernel stages (n_in <= kTcIn)
 constexpr int kTcThreads = 352;
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
@@ -89,14 +90,15 @@ __host__ __device__ inline uint32_t staged_bytes(int npp, int n_geo, int cap) {
   return staged_slot_bytes(npp) + kTcM * n_geo * 4 + 2u * 16u * cap;
 }
 
-template <int MODE, int GM>
+template <int MODE, int GM, int H>
 __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   constexpr bool GATHER = GM != GM_X;
   using C = TcCfg<MODE>;
   constexpr int KC = C::KC;
   constexpr int HC = KC / 2;                       // K columns per thread per chunk
-  constexpr int NCH = kTcH / KC;                   // chunks of a hidden layer
-  constexpr int WST = kTcH * KC * C::ESZ * C::PARTS;  // bytes per weight stage
+  constexpr int NCH = H / KC;                      // chunks of a hidden layer
+  constexpr int NCH0 = kTcIn / KC;                 // chunks of the (at most kTcIn) inputs
+  constexpr int WST = H * KC * C::ESZ * C::PARTS;  // bytes per weight stage
   constexpr int AST = kTcM * KC * C::ESZ * C::PARTS;  // bytes per A stage
   constexpr uint32_t SBO = KC * C::ESZ * 8;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -117,22 +119,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stage_empty + 1);
   // BN scale/shift per hidden layer and the input normalisation, staged once per CTA
   float* p_scale = reinterpret_cast<float*>(tmem_slot + 4);
-  float* p_shift = p_scale + A.depth * kTcH;
-  float* p_mean = p_shift + A.depth * kTcH;
-  float* p_rstd = p_mean + kTcH;
+  float* p_shift = p_scale + A.depth * H;
+  float* p_mean = p_shift + A.depth * H;
+  float* p_rstd = p_mean + kTcIn;
   const PackHdr* hdr = reinterpret_cast<const PackHdr*>(A.packed);
   // fp32-accuracy tanh takes 2^(2 log2(e) z): fold 2 log2(e) into the BN scale and shift so
   // that the epilogue needs one FFMA before ex2 (the activation never needs z itself)
   const bool fold = MODE != DNNMG_PREC_BF16 && A.act == DNNMG_ACT_TANH;
   const float k2 = fold ? 2.8853900817779268f : 1.0f;
-  for (int i = threadIdx.x; i < A.depth * kTcH; i += blockDim.x) {
-    p_scale[i] = A.scale[i] * hdr->unscale[i / kTcH] * k2;  // 2^-s: exact
+  for (int i = threadIdx.x; i < A.depth * H; i += blockDim.x) {
+    p_scale[i] = A.scale[i] * hdr->unscale[i / H] * k2;  // 2^-s: exact
     p_shift[i] = A.shift[i] * k2;
   }
   const float y_unscale = hdr->unscale[A.depth];
-  int32_t* idx_s = reinterpret_cast<int32_t*>(p_rstd + kTcH);  // [kTcM][npp] (GM_DIRECT only)
+  int32_t* idx_s = reinterpret_cast<int32_t*>(p_rstd + kTcIn);  // [kTcM][npp] (GM_DIRECT only)
   // GM_STAGED: slot block [kTcM][npp] u16 | geometry rows [kTcM][n_geo] | x~ [cap] | r [cap]
-  uint8_t* st_base = reinterpret_cast<uint8_t*>(p_rstd + kTcH);
+  uint8_t* st_base = reinterpret_cast<uint8_t*>(p_rstd + kTcIn);
   const uint16_t* slot_s = reinterpret_cast<const uint16_t*>(st_base);
   float4* geo_s = reinterpret_cast<float4*>(st_base + staged_slot_bytes(A.npp));
   float4* stx = geo_s + kTcM * A.n_geo / 4;
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   float* y_stage = reinterpret_cast<float*>(
       st_base + (GM == GM_DIRECT ? kTcM * A.npp * 4
                                  : GM == GM_STAGED ? staged_bytes(A.npp, A.n_geo, A.tile_cap) : 0));
-  for (int i = threadIdx.x; i < kTcH; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kTcIn; i += blockDim.x) {
     p_mean[i] = i < A.n_in ? A.in_mean[i] : 0.f;
     p_rstd[i] = i < A.n_in ? 1.0f / A.in_std[i] : 0.f;
   }
@@ -200,8 +202,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         stage_idx(tile + gridDim.x);
         for (int g = 0; g < G; ++g) {
-          const int N = g < A.depth ? kTcH : A.Nhead;
-          const int nk = (g == 0 ? A.K0p : kTcH) / KC;
+          const int N = g < A.depth ? H : A.Nhead;
+          const int nk = (g == 0 ? A.K0p : H) / KC;
           const uint32_t bytes = (uint32_t)N * KC * C::ESZ * C::PARTS;
           for (int c = 0; c < nk; ++c, ++item) {
             const int s = item % C::NW;
@@ -220,13 +222,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       uint32_t witem = 0, aitem = 0, j = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int g = 0; g < G; ++g, ++j) {
-          const int N = g < A.depth ? kTcH : A.Nhead;
-          const int nk = (g == 0 ? A.K0p : kTcH) / KC;
+          const int N = g < A.depth ? H : A.Nhead;
+          const int nk = (g == 0 ? A.K0p : H) / KC;
           const uint32_t idesc = idesc_for<MODE>(N);
           const int buf = j & 1;
           mbar_wait(smem_u32(&acc_empty[buf]), ((j >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t d = tmem + buf * kTcH;
+          const uint32_t d = tmem + buf * H;
           for (int c = 0; c < nk; ++c, ++witem, ++aitem) {
             const int sw = witem % C::NW, sa = aitem % C::NA;
             mbar_wait(smem_u32(&w_full[sw]), (witem / C::NW) & 1);
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
 
     const int nck0 = A.K0p / KC;
     const bool vec_x = (A.n_in & 3) == 0;
-    float xin[NCH][HC];                 // raw input row slice of the next tile (prefetched)
+    float xin[NCH0][HC];                 // raw input row slice of the next tile (prefetched)
     uint32_t iload = 0;                 // staged index blocks consumed
     const bool idx_staged = GATHER && ((kTcM * A.npp * 4) & 15) == 0;
     auto load_x = [&](int64_t tile) {
@@ -369,9 +371,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         // r of node s - npp, or geometry; indices first, then all value loads in flight
         const int32_t* nt = A.node_table + row * A.npp;
         const int geo4 = A.n_geo / 4;
-        int nidx[NCH][HC / 4];
+        int nidx[NCH0][HC / 4];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
+        for (int c = 0; c < NCH0; ++c)
 #pragma unroll
           for (int j = 0; j < HC / 4; ++j) {
             const int f4 = (KC / 4) * c + (HC / 4) * hh + j;
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           ++iload;
         }
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
+        for (int c = 0; c < NCH0; ++c)
 #pragma unroll
           for (int j = 0; j < HC / 4; ++j) {
             const int f4 = (KC / 4) * c + (HC / 4) * hh + j;
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       } else {
       const float* xr = A.X + row * A.n_in;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = 0; c < NCH0; ++c) {
 #pragma unroll
         for (int j = 0; j < HC / 4; ++j) {
           const int col = c * KC + HC * hh + 4 * j;
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
     // layer-0 operand: normalised input rows (net.py:131), from the prefetched registers
     auto produce_layer0 = [&]() {
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = 0; c < NCH0; ++c) {
         if (c < nck0) {
           float v[HC];
 #pragma unroll
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       const float4* gr = geo_s + row_in_tile * (A.n_geo / 4);
       const int geo4 = A.n_geo / 4;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = 0; c < NCH0; ++c) {
         if (c < nck0) {
           float v[HC];
 #pragma unroll
@@ -511,12 +513,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
         if (warp == 0 && lane == 0) TC_TRACE(6144 + j);
         tc_fence_after();
-        const float* sc = p_scale + g * kTcH;
-        const float* sh = p_shift + g * kTcH;
+        const float* sc = p_scale + g * H;
+        const float* sh = p_shift + g * H;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           float v[HC];
-          tmem_ld<HC>(tmem + lane_addr + buf * kTcH + c * KC + HC * hh, v);
+          tmem_ld<HC>(tmem + lane_addr + buf * H + c * KC + HC * hh, v);
 #pragma unroll
           for (int e = 0; e < HC; e += 4) {
             const int col = c * KC + HC * hh + e;
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           float* ys = reinterpret_cast<float*>(st_base);
           for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
             float v[16];
-            tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
+            tmem_ld16(tmem + lane_addr + buf * H + sl * 16, v);
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int col = sl * 16 + e;
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         } else if (A.y_mode == 0) {
           for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
             float v[16];
-            tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
+            tmem_ld16(tmem + lane_addr + buf * H + sl * 16, v);
             if (live) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           if ((quad >> 1) == half) {
             for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
               float v[16];
-              tmem_ld16(tmem + lane_addr + buf * kTcH + sl * 16, v);
+              tmem_ld16(tmem + lane_addr + buf * H + sl * 16, v);
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const int col = sl * 16 + e;
@@ -720,7 +722,8 @@ static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 int32_t mlp_tc_supported(const dnnmg_mlp_t* m) {
   return (m->precision == DNNMG_PREC_BF16 || m->precision == DNNMG_PREC_TF32X3 ||
           m->precision == DNNMG_PREC_F16X3) &&
-         m->n_hidden == kTcH && m->n_in <= kTcH && m->n_out <= kTcH && m->depth >= 1 &&
+         (m->n_hidden == 256 || m->n_hidden == 128) && m->n_in <= kTcIn &&
+         m->n_out <= m->n_hidden && m->depth >= 1 &&
          m->depth < DNNMG_MAX_LAYERS;
 }
 
@@ -729,8 +732,8 @@ static void layout(const dnnmg_mlp_t* m, int64_t* goff, int64_t* total) {
   const int parts = m->precision == DNNMG_PREC_BF16 ? 1 : 2;
   int64_t off = kPackHdr;
   for (int g = 0; g <= m->depth; ++g) {
-    const int K = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : kTcH;
-    const int N = g < m->depth ? kTcH : round_up(m->n_out, 16);
+    const int K = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : m->n_hidden;
+    const int N = g < m->depth ? m->n_hidden : round_up(m->n_out, 16);
     goff[g] = off;
     off += (int64_t)K * N * esz * parts;
   }
@@ -739,7 +742,8 @@ static void layout(const dnnmg_mlp_t* m, int64_t* goff, int64_t* total) {
 
 int32_t mlp_tc_packed_bytes(const dnnmg_mlp_t* m, int64_t* bytes) {
   DNNMG_REQUIRE(mlp_tc_supported(m), DNNMG_ERR_UNSUPPORTED,
-                "mlp: tensor-core mode needs n_hidden == 256, n_in <= 256, n_out <= 256");
+                "mlp: fused tensor-core mode needs n_hidden 128 or 256, n_in <= 256, "
+                "n_out <= n_hidden");
   int64_t goff[DNNMG_MAX_LAYERS];
   layout(m, goff, bytes);
   return DNNMG_OK;
@@ -747,7 +751,8 @@ int32_t mlp_tc_packed_bytes(const dnnmg_mlp_t* m, int64_t* bytes) {
 
 int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
   DNNMG_REQUIRE(mlp_tc_supported(m), DNNMG_ERR_UNSUPPORTED,
-                "mlp: tensor-core mode needs n_hidden == 256, n_in <= 256, n_out <= 256");
+                "mlp: fused tensor-core mode needs n_hidden 128 or 256, n_in <= 256, "
+                "n_out <= n_hidden");
   int64_t goff[DNNMG_MAX_LAYERS], total;
   layout(m, goff, &total);
   PackHdr* hdr = static_cast<PackHdr*>(packed);
@@ -755,10 +760,11 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
   int32_t rc = launch_pack_scales(m, hdr, s);
   if (rc) return rc;
   for (int g = 0; g <= m->depth; ++g) {
-    const int K = g == 0 ? m->n_in : kTcH;
-    const int N = g < m->depth ? kTcH : m->n_out;
-    const int Kp = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : kTcH;
-    const int Np = g < m->depth ? kTcH : round_up(m->n_out, 16);
+    const int H = m->n_hidden;
+    const int K = g == 0 ? m->n_in : H;
+    const int N = g < m->depth ? H : m->n_out;
+    const int Kp = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : H;
+    const int Np = g < m->depth ? H : round_up(m->n_out, 16);
     uint8_t* out = static_cast<uint8_t*>(packed) + goff[g];
     const int64_t n = (int64_t)Kp * Np;
     if (m->precision == DNNMG_PREC_BF16)
@@ -788,10 +794,10 @@ constexpr size_t kSmemMax = 227 * 1024;
 template <int MODE>
 static size_t smem_base(const dnnmg_mlp_t* m) {
   using C = TcCfg<MODE>;
-  constexpr int WST = kTcH * C::KC * C::ESZ * C::PARTS;
+  const size_t WST = (size_t)m->n_hidden * C::KC * C::ESZ * C::PARTS;
   constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
   return (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 8) + 16 +
-         sizeof(float) * (2 * (size_t)m->depth * kTcH + 2 * kTcH);
+         sizeof(float) * (2 * (size_t)m->depth * m->n_hidden + 2 * kTcIn);
 }
 static size_t smem_base_of(const dnnmg_mlp_t* m) {
   return m->precision == DNNMG_PREC_BF16 ? smem_base<DNNMG_PREC_BF16>(m)
@@ -846,8 +852,6 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   A.shift = m->bn_shift;
   A.in_mean = m->in_mean;
   A.in_std = m->in_std;
-  constexpr int WST = kTcH * C::KC * C::ESZ * C::PARTS;
-  constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
   const size_t base = smem_base<MODE>(m);
   const int gm = choose_gm(m, g);
   size_t smem = base + (gm == GM_DIRECT ? (size_t)kTcM * g->npp * 4
@@ -865,18 +869,24 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: TMEM (512 columns) is per SM
   const int64_t tiles = (n_rows + kTcM - 1) / kTcM;
   const int grid = (int)(tiles < kSMs ? tiles : kSMs);
-  if (gm == GM_STAGED) {
-    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (m->n_hidden == 128) {   // width 128: stored-X rows only (the patch paths use 256)
+    DNNMG_REQUIRE(gm == GM_X, DNNMG_ERR_UNSUPPORTED,
+                  "mlp: the fused patch gather needs n_hidden == 256");
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_X, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    mlp_tc_kernel<MODE, GM_STAGED><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_X, 128><<<grid, kTcThreads, smem, s>>>(A);
+  } else if (gm == GM_STAGED) {
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_STAGED, kTcH>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    mlp_tc_kernel<MODE, GM_STAGED, kTcH><<<grid, kTcThreads, smem, s>>>(A);
   } else if (gm == GM_DIRECT) {
-    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    mlp_tc_kernel<MODE, GM_DIRECT><<<grid, kTcThreads, smem, s>>>(A);
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_DIRECT, kTcH>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    mlp_tc_kernel<MODE, GM_DIRECT, kTcH><<<grid, kTcThreads, smem, s>>>(A);
   } else {
-    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_X>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_X, kTcH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    mlp_tc_kernel<MODE, GM_X><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_X, kTcH><<<grid, kTcThreads, smem, s>>>(A);
   }
   DNNMG_CHECK_LAUNCH("mlp_tc_kernel");
   if (A.trace) {  // debug only: synchronous copy-out of CTA 0's timeline

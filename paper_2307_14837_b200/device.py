@@ -273,6 +273,12 @@ class DevicePatchSet:
         return store[key]
 
 
+def tc_fused_supported(arch):
+    """Widths of the fused per-tile tensor-core kernel (csrc/mlp_tc.cu, mlp_tc_supported);
+    other widths run on the layer-major kernel (csrc/mlp_layer.cu)."""
+    return arch.n_hidden in (128, 256) and arch.n_in <= 256 and arch.n_out <= arch.n_hidden
+
+
 class DeviceModel:
     """Eval-mode MlpModel on the device (net.py:54-159), BN folded to scale/shift."""
 

@@ -66,8 +66,10 @@ class CorrectionStep:
         self.d = torch.empty(4 * nf, dtype=f, device=dev)
         self.x_corr = torch.empty(4 * nf, dtype=f, device=dev)
         self.elem = self.level.scratch()
-        # layered tensor-core MLP (other widths): the gather is fused into its layer-0 operand
-        self.layered = model is not None and precision != "fp32" and not self.fused_gather
+        # layered tensor-core MLP (widths the fused kernel does not hold): the gather is fused
+        # into its layer-0 operand; width 128 runs the fused kernel on stored X rows
+        self.layered = (model is not None and precision != "fp32"
+                        and not dv.tc_fused_supported(model.arch))
         # X is only materialised when the gather is not fused into the MLP
         n_x = 0 if (self.fused_gather or self.layered or model is None) else self.ps.n_patches
         self.X = torch.empty((n_x, input_width(self.patchset)), dtype=f, device=dev)

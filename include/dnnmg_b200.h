@@ -92,6 +92,19 @@ typedef struct {
   const int32_t* ptr;   /* [n_coarse_nodes+1] */
   const int32_t* fine;  /* [nnz] */
   const float* w;       /* [nnz] */
+  /* optional owner-computes form (all set, or all NULL): per coarse cell, the transpose of
+   * K1's separable stencil applied to the fine nodes whose first-appearance parent it is
+   * (owner lists as in dnnmg_prolong_t) gives 27 partial sums into cell_scratch, which are
+   * then summed per coarse node over its incident (cell, local node) entries in ascending
+   * cell order.  Deterministic; streams b_fine once instead of gathering it per P entry. */
+  int32_t n_coarse_cells;
+  const int32_t* coarse_cell_nodes; /* [n_coarse_cells][27] (unused by the kernels; layout ref) */
+  const int32_t* owner_ptr;         /* [n_coarse_cells+1] */
+  const int32_t* owner_node;        /* [n_fine_nodes] */
+  const uint8_t* owner_code;        /* [n_fine_nodes]: o*27 + a */
+  const int32_t* node_cell_ptr;     /* [n_coarse_nodes+1] CSR coarse node -> cell*27 + a */
+  const int32_t* node_cell_idx;
+  float* cell_scratch;              /* [n_coarse_cells][27][4] device scratch */
 } dnnmg_restrict_t;
 
 /* Dirichlet data of one level (space.py:245-255): bc_code[n] = 0 untouched,

@@ -57,7 +57,9 @@ class Mlp(ctypes.Structure):
 
 class Restrict(ctypes.Structure):
     _fields_ = [("n_coarse_nodes", c_i32), ("n_fine_nodes", c_i32), ("ptr", c_vp), ("fine", c_vp),
-                ("w", c_vp)]
+                ("w", c_vp), ("n_coarse_cells", c_i32), ("coarse_cell_nodes", c_vp),
+                ("owner_ptr", c_vp), ("owner_node", c_vp), ("owner_code", c_vp),
+                ("node_cell_ptr", c_vp), ("node_cell_idx", c_vp), ("cell_scratch", c_vp)]
 
 
 class Csr(ctypes.Structure):

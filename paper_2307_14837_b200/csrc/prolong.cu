@@ -278,12 +278,97 @@ __global__ void __launch_bounds__(256) restrict_kernel(int n_coarse, const int32
   }
 }
 
+// K6 owner-computes form: one warp per coarse (parent) cell scatters the b values of its
+// owned fine nodes onto the 5 x 5 x 5 lattice of the refined cell and applies the transpose
+// of the separable prolongation stencil (z: 125 -> 75, y: 75 -> 45, x: 45 -> 27), giving the
+// cell's 27 partial sums of P^T b; a node sum over the coarse node -> (cell, a) CSR
+// (ascending cell) completes them.
+__device__ __forceinline__ float4 tlerp(const float4& a0, const float4& a1, const float4& a2,
+                                        const float4& a3, const float4& a4, int i) {
+  // sum_p phi_i(p/4) a_p: p even copies the node, p odd the quarter-point weights
+  float4 r;
+  if (i == 0) {
+    r.x = fmaf(-0.125f, a3.x, fmaf(0.375f, a1.x, a0.x));
+    r.y = fmaf(-0.125f, a3.y, fmaf(0.375f, a1.y, a0.y));
+    r.z = fmaf(-0.125f, a3.z, fmaf(0.375f, a1.z, a0.z));
+    r.w = fmaf(-0.125f, a3.w, fmaf(0.375f, a1.w, a0.w));
+  } else if (i == 1) {
+    r.x = fmaf(0.75f, a3.x, fmaf(0.75f, a1.x, a2.x));
+    r.y = fmaf(0.75f, a3.y, fmaf(0.75f, a1.y, a2.y));
+    r.z = fmaf(0.75f, a3.z, fmaf(0.75f, a1.z, a2.z));
+    r.w = fmaf(0.75f, a3.w, fmaf(0.75f, a1.w, a2.w));
+  } else {
+    r.x = fmaf(0.375f, a3.x, fmaf(-0.125f, a1.x, a4.x));
+    r.y = fmaf(0.375f, a3.y, fmaf(-0.125f, a1.y, a4.y));
+    r.z = fmaf(0.375f, a3.z, fmaf(-0.125f, a1.z, a4.z));
+    r.w = fmaf(0.375f, a3.w, fmaf(-0.125f, a1.w, a4.w));
+  }
+  return r;
+}
+
+__global__ void __launch_bounds__(32 * kProlongWarps) restrict_owner_kernel(
+    int n_cells, const int32_t* __restrict__ owner_ptr, const int32_t* __restrict__ owner_node,
+    const uint8_t* __restrict__ owner_code, const float4* __restrict__ bf,
+    float4* __restrict__ scratch) {
+  __shared__ float4 sm[kProlongWarps][125 + 75 + 45];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* X3 = sm[w];        // [pz][py][px]
+  float4* X2 = X3 + 125;     // [iz][py][px]
+  float4* X1 = X2 + 75;      // [iz][iy][px]
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int C = blockIdx.x * kProlongWarps + w; C < n_cells; C += gridDim.x * kProlongWarps) {
+    for (int l = lane; l < 125; l += 32) X3[l] = zero;
+    __syncwarp();
+    const int s = __ldg(owner_ptr + C), e = __ldg(owner_ptr + C + 1);
+    for (int i = s + lane; i < e; i += 32) {
+      const int oa = __ldg(owner_code + i);
+      const int o = oa / 27, a = oa - 27 * o;
+      const int px = 2 * (o & 1) + a % 3;
+      const int py = 2 * ((o >> 1) & 1) + (a / 3) % 3;
+      const int pz = 2 * (o >> 2) + a / 9;
+      X3[25 * pz + 5 * py + px] = __ldg(bf + __ldg(owner_node + i));
+    }
+    __syncwarp();
+    for (int l = lane; l < 75; l += 32) {          // z: [iz][py][px]
+      const int iz = l / 25, yx = l % 25;
+      const float4* c = X3 + yx;
+      X2[l] = tlerp(c[0], c[25], c[50], c[75], c[100], iz);
+    }
+    __syncwarp();
+    for (int l = lane; l < 45; l += 32) {          // y: [iz][iy][px]
+      const int iz = l / 15, iy = (l / 5) % 3, px = l % 5;
+      const float4* c = X2 + 25 * iz + px;
+      X1[l] = tlerp(c[0], c[5], c[10], c[15], c[20], iy);
+    }
+    __syncwarp();
+    if (lane < 27) {                               // x: [iz][iy][ix]
+      const int line = lane / 3, ix = lane % 3;
+      const float4* c = X1 + 5 * line;
+      scratch[(int64_t)C * 27 + lane] = tlerp(c[0], c[1], c[2], c[3], c[4], ix);
+    }
+    __syncwarp();
+  }
+}
+
+int32_t launch_node_sum(int n_nodes, const int32_t* ptr, const int32_t* idx, const float* elem,
+                        float* out, cudaStream_t s);
+
 int32_t launch_restrict(const dnnmg_restrict_t* R, const float* bf, float* bc, cudaStream_t s) {
-  DNNMG_REQUIRE(R && R->ptr && R->fine && R->w && bf && bc, DNNMG_ERR_ARG,
-                "restrict: null argument");
+  DNNMG_REQUIRE(R && bf && bc, DNNMG_ERR_ARG, "restrict: null argument");
   DNNMG_REQUIRE(((uintptr_t)bf & 15) == 0 && ((uintptr_t)bc & 15) == 0, DNNMG_ERR_ARG,
                 "restrict: vectors must be 16-byte aligned");
   if (R->n_coarse_nodes == 0) return DNNMG_OK;
+  if (R->owner_ptr && R->owner_node && R->owner_code && R->node_cell_ptr && R->node_cell_idx &&
+      R->cell_scratch && R->n_coarse_cells > 0) {
+    const int blocks = grid_for((R->n_coarse_cells + kProlongWarps - 1) / kProlongWarps, 1, 4);
+    restrict_owner_kernel<<<blocks, 32 * kProlongWarps, 0, s>>>(
+        R->n_coarse_cells, R->owner_ptr, R->owner_node, R->owner_code,
+        reinterpret_cast<const float4*>(bf), reinterpret_cast<float4*>(R->cell_scratch));
+    DNNMG_CHECK_LAUNCH("restrict_owner_kernel");
+    return launch_node_sum(R->n_coarse_nodes, R->node_cell_ptr, R->node_cell_idx, R->cell_scratch,
+                           bc, s);
+  }
+  DNNMG_REQUIRE(R->ptr && R->fine && R->w, DNNMG_ERR_ARG, "restrict: null table");
   restrict_kernel<<<grid_for(R->n_coarse_nodes, 256), 256, 0, s>>>(
       R->n_coarse_nodes, R->ptr, R->fine, R->w, reinterpret_cast<const float4*>(bf),
       reinterpret_cast<float4*>(bc));

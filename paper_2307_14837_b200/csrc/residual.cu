@@ -767,6 +767,16 @@ int32_t launch_level_geometry(const dnnmg_level_t* lv, float* geo, cudaStream_t 
   return DNNMG_OK;
 }
 
+int32_t launch_node_sum(int n_nodes, const int32_t* ptr, const int32_t* idx, const float* elem,
+                        float* out, cudaStream_t s) {
+  if (n_nodes == 0) return DNNMG_OK;
+  node_sum_kernel<<<grid_for(n_nodes, 256), 256, 0, s>>>(
+      n_nodes, ptr, idx, reinterpret_cast<const float4*>(elem), nullptr, 1.0f, nullptr,
+      reinterpret_cast<float4*>(out));
+  DNNMG_CHECK_LAUNCH("node_sum_kernel");
+  return DNNMG_OK;
+}
+
 int32_t launch_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph, float* aT,
                     float* dT, cudaStream_t s) {
   int32_t st = check_level(lv, "stab");

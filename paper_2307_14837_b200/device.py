@@ -10,6 +10,7 @@ and cached on that object, so repeated API calls only move the vectors.
 """
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -165,8 +166,21 @@ class DeviceRestrict:
         self.ptr = upload(PT.indptr, np.int32)
         self.fine = upload(PT.indices, np.int32)
         self.w = upload(PT.data, np.float32)   # dyadic weights: exact in fp32
+        # owner-computes form: K1's owner lists plus the coarse node -> (cell, a) CSR
+        # (env DNNMG_RESTRICT_CSR=1 keeps the P^T CSR form)
+        P = DeviceProlong.get(hierarchy, level)
+        ctab = hierarchy.scalar_nodes(level)[1]
+        cp, ci = node_csr(ctab)
+        self.cell_ptr = upload(cp, np.int32)
+        self.cell_idx = upload(ci, np.int32)
+        self.n_cells = int(ctab.shape[0])
+        self.scratch = torch.empty(self.n_cells * 27 * 4, dtype=torch.float32, device=device())
+        own = not os.environ.get("DNNMG_RESTRICT_CSR")
         self.struct = _lib.Restrict(self.n_coarse, self.n_fine, ptr(self.ptr), ptr(self.fine),
-                                    ptr(self.w))
+                                    ptr(self.w), self.n_cells if own else 0, ptr(P.ctab),
+                                    ptr(P.owner_ptr) if own else None, ptr(P.owner_node),
+                                    ptr(P.owner_code), ptr(self.cell_ptr), ptr(self.cell_idx),
+                                    ptr(self.scratch))
 
     @staticmethod
     def get(hierarchy, level):

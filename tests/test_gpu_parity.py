@@ -403,3 +403,28 @@ def test_geometry_cache_matches_recomputed(name):
     # the cached geometry is formed in fp64: at least as close to the reference
     assert rel(out[1], g["r"]) < 2e-5, rel(out[1], g["r"])
     assert rel(out[1], g["r"]) <= 1.2 * rel(out[0], g["r"]) + 1e-9
+
+
+@pytest.mark.parametrize("name", ["cfg0", "jit", "j2", "lvl1", "chan"])
+def test_restrict_owner_form_matches_csr_form(name):
+    """K6 owner-computes form (transpose of K1's per-cell stencil + ordered node sum) against
+    the P^T CSR form on the same vector: equal to fp32 rounding."""
+    import ctypes
+    from paper_2307_14837_b200 import _lib, device as dv
+    g = load_golden(name)
+    h = product_hierarchy(g)
+    L, J = int(g["L"]), int(g["J"])
+    R = dv.DeviceRestrict.get(h, L + J - 1)
+    b = torch.tensor(np.random.default_rng(7).standard_normal(4 * R.n_fine), dtype=torch.float32,
+                     device="cuda")
+    outs = []
+    for owner in (True, False):
+        st = _lib.Restrict()
+        ctypes.memmove(ctypes.addressof(st), ctypes.addressof(R.struct), ctypes.sizeof(st))
+        if not owner:
+            st.owner_ptr = None
+        out = torch.empty(4 * R.n_coarse, dtype=torch.float32, device="cuda")
+        _lib.call("dnnmg_restrict", ctypes.byref(st), dv.ptr(b), dv.ptr(out), dv.stream_handle())
+        outs.append(out.double().cpu().numpy())
+    assert R.struct.owner_ptr is not None
+    assert rel(outs[0], outs[1]) < 1e-6, rel(outs[0], outs[1])

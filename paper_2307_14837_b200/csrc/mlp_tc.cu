@@ -4,16 +4,20 @@
 //   h0 = (X - mean)/std; layer i: z = h W_i, a = act(z*scale_i + shift_i) (BN folded),
 //   h_{i+1} = a (+ h_i for i >= 1); head Y = h_depth W_depth.
 //
-// One persistent CTA per SM processes 128-row tiles.  Warp roles (320 threads):
-//   warps 0..7  compute: stage the layer-0 A operand from X (input normalisation),
+// One persistent CTA per SM processes 128-row tiles of a network with hidden width
+// H = 128 or 256 (template).  Warp roles (352 threads):
+//   warps 0..7  compute: stage the layer-0 A operand (input normalisation) from X, from
+//               a direct per-(patch, slot) gather or from the staged tile nodes,
 //               run every epilogue (TMEM -> registers -> BN/activation/skip) and
 //               write the next GEMM's A operand into the SMEM ring chunk by chunk;
-//               the fp32 skip state h lives in their registers (128 values/thread)
+//               the fp32 skip state h lives in their registers (H/2 values/thread)
 //   warp 8      weight producer: cp.async.bulk (TMA) of pre-packed weight chunks
 //               (already in the UMMA canonical layout) into the SMEM ring
 //   warp 9      MMA issuer: one thread issues tcgen05.mma into TMEM, commits to
 //               mbarriers that release SMEM stages and signal the epilogue
-// TMEM holds two 128 x 256 fp32 accumulators, so the epilogue of GEMM j overlaps
+//   warp 10     staged gather (GM_STAGED): cp.async of the next tile's distinct nodes,
+//               bulk copies of its slot block and geometry; bulk store of Y (y_mode 3)
+// TMEM holds two 128 x H fp32 accumulators, so the epilogue of GEMM j overlaps
 // the MMAs of GEMM j+1 (which consume the A chunks the epilogue produces).
 //
 // Precision modes:

@@ -156,13 +156,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return r;
 }
 // x = hi + lo for a pair of values: hi = fp16(x), lo = fp16(x - hi) (x - hi is exact)
-// hi = x with its fp32 mantissa rounded (to nearest, integer add + mask) to the 10 bits fp16
-// keeps (exact in fp16 for |x| >= 2^-14), lo = x - hi (exact, symmetric about zero, so the
-// dropped lo*lo term of the 3-pass product carries no bias) rounded to fp16:
-// |x - hi - lo| <= 2^-22 |x|
+// hi = x with its fp32 mantissa truncated to the 10 bits fp16 keeps (exact in fp16 for
+// |x| >= 2^-14), lo = x - hi (exact) rounded to fp16: |x - hi - lo| <= 2^-21 |x|.
+// (Rounding hi to nearest instead, which makes lo symmetric, measured no accuracy change
+// — tests/prec_cmp.py — and costs one more integer op per value.)
 __device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const float ha = __uint_as_float((__float_as_uint(a) + 0x1000u) & 0xFFFFE000u);
-  const float hb = __uint_as_float((__float_as_uint(b) + 0x1000u) & 0xFFFFE000u);
+  const float ha = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+  const float hb = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(hb), "f"(ha));
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - hb), "f"(a - ha));
 }
@@ -249,11 +249,10 @@ __device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const 
       uint32_t* l = &lo.x;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        // exact split x = hi + lo: hi = x rounded to tf32 (10 mantissa bits, integer add +
-        // mask), lo = x - hi (exact, symmetric about zero), lo rounded to nearest tf32
-        // (|err| <= 2^-11 |lo| <= 2^-22 |x|)
+        // exact split x = hi + lo: hi = x truncated to tf32 (10 mantissa bits), lo = x - hi
+        // (exact), lo rounded to nearest tf32 (|err| <= 2^-11 |lo| <= 2^-21 |x|)
         const uint32_t xb = __float_as_uint(v[4 * j + e]);
-        const uint32_t t = (xb + 0x1000u) & 0xFFFFE000u;
+        const uint32_t t = xb & 0xFFFFE000u;
         const uint32_t lb = __float_as_uint(v[4 * j + e] - __uint_as_float(t));
         h[e] = t;
         l[e] = (lb + 0x1000u) & 0xFFFFE000u;

@@ -737,7 +737,7 @@ def run_mlp_sweep(args):
     from paper_2307_14837_b200 import device as dvm, synthetic
     from paper_2307_14837_b200.net import Architecture, MlpModel
     peaks, peak_kind = load_peaks()
-    modes = (args.precision,) if args.precision else ("f16x3", "tf32x3", "bf16")
+    modes = (args.precision,) if args.precision else ("f16x3", "tf32x3", "bf16", "fp8")
     hs = (128, 256, 512, 1024)
     batches = tuple(int(b) for b in args.sweep_batches.split(","))
     out = []
@@ -767,17 +767,19 @@ def run_mlp_sweep(args):
                 tf = flop * B / (ms / 1e3) / 1e12
                 peak = {"bf16": peaks["bf16_tflops_sustained"],
                         "f16x3": peaks["bf16_tflops_sustained"] / 3.0,
-                        "tf32x3": peaks["bf16_tflops_sustained"] / 6.0}[mode]
+                        "tf32x3": peaks["bf16_tflops_sustained"] / 6.0,
+                        "fp8": 2.0 * peaks["bf16_tflops_sustained"]}[mode]
                 out.append({"H": H, "mode": mode, "batch": B, "ms": ms, "rows/s": B / (ms / 1e3),
                             "TFLOP/s": tf, "frac": tf / peak,
-                            "kernel": "fused" if dvm.tc_fused_supported(model.arch) else "layered"})
+                            "kernel": ("fused" if dvm.tc_fused_supported(model.arch) and mode != "fp8"
+                                       else "layered")})
                 del X, Y
             del dm
     line = {"metric": "patch-MLP rows/s and TFLOP/s (BASELINE config 4)", "n_gpus": 1,
             "data": "synthetic", "dtype": "fp32 accumulate",
             "config": {"workload": "cfg4", "mlp": "174 -> H x3 -> 81 tanh", "H": list(hs),
                        "batches": list(batches), "modes": list(modes)},
-            "peak_source": f"{peak_kind} bf16 sustained; f16x3 = /3, tf32x3 = /6",
+            "peak_source": f"{peak_kind} bf16 sustained; f16x3 = /3, tf32x3 = /6, fp8 = x2",
             "points": out}
     print(json.dumps(line), flush=True)
 

@@ -61,8 +61,10 @@ enum {
   DNNMG_PREC_FP32 = 0,   /* SIMT fp32 FFMA (any width) */
   DNNMG_PREC_BF16 = 1,   /* tcgen05 kind::f16, bf16 operands, fp32 accumulate in TMEM */
   DNNMG_PREC_TF32X3 = 2, /* tcgen05 kind::tf32, 3-pass split (hi*hi + hi*lo + lo*hi), fp32 accuracy */
-  DNNMG_PREC_F16X3 = 3   /* tcgen05 kind::f16, fp16 3-pass split of power-of-two scaled weights,
+  DNNMG_PREC_F16X3 = 3,  /* tcgen05 kind::f16, fp16 3-pass split of power-of-two scaled weights,
                             fp32 accuracy at twice the tf32 rate (|activations| < 65504) */
+  DNNMG_PREC_FP8 = 4     /* tcgen05 kind::f8f6f4, e4m3 operands (weights scaled by a power of
+                            two per layer), fp32 accumulate; report-only accuracy (~1e-1) */
 };
 
 /* Q2 embedding level l -> l+1 (space.py:117-165).  Each fine node n takes the

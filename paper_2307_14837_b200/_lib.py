@@ -13,8 +13,9 @@ LIB_PATH = os.path.join(_HERE, "libdnnmg_b200.so")
 
 DNNMG_OK, DNNMG_ERR_ARG, DNNMG_ERR_CUDA, DNNMG_ERR_UNSUPPORTED, DNNMG_ERR_ARCH = range(5)
 ACT_RELU, ACT_TANH = 0, 1
-PREC_FP32, PREC_BF16, PREC_TF32X3, PREC_F16X3 = 0, 1, 2, 3
-PRECISIONS = {"fp32": PREC_FP32, "bf16": PREC_BF16, "tf32x3": PREC_TF32X3, "f16x3": PREC_F16X3}
+PREC_FP32, PREC_BF16, PREC_TF32X3, PREC_F16X3, PREC_FP8 = 0, 1, 2, 3, 4
+PRECISIONS = {"fp32": PREC_FP32, "bf16": PREC_BF16, "tf32x3": PREC_TF32X3, "f16x3": PREC_F16X3,
+              "fp8": PREC_FP8}
 MAX_LAYERS = 16
 
 c_i32, c_i64, c_f32, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p

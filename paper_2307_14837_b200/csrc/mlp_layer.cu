@@ -27,6 +27,7 @@ constexpr int64_t kLChunkRows = 1 << 19;   // rows per pass (bounds the workspac
 
 template <int MODE> struct LCfg { static constexpr int NS = 4; };
 template <> struct LCfg<DNNMG_PREC_BF16> { static constexpr int NS = 6; };
+template <> struct LCfg<DNNMG_PREC_FP8> { static constexpr int NS = 6; };
 
 struct LayerArgs {
   const uint8_t* A;        // operand [tiles][n_kc][PARTS][kTcM*KC*ESZ]
@@ -148,7 +149,8 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
     const int quad = warp & 3, half = warp >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    constexpr bool accurate = MODE != DNNMG_PREC_BF16;
+    constexpr bool accurate = MODE == DNNMG_PREC_F16X3 || MODE == DNNMG_PREC_TF32X3;
+    constexpr int GS = HC > 16 ? HC : 16;   // columns per epilogue step (FP8: one 64-K half chunk)
     const int g16 = A.N / 16;   // 16-column groups of the layer output
     const float yu = A.head ? __ldg(A.y_unscale) : 1.f;
     uint32_t j = 0;
@@ -161,35 +163,39 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
       mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
       tc_fence_after();
       const int c0 = half * (nbw / 2);
-      for (int cc = c0; cc < c0 + nbw / 2; cc += 16) {
-        float v[16];
-        tmem_ld16(tmem + lane_addr + buf * kLN + cc, v);
+      for (int cc = c0; cc < c0 + nbw / 2; cc += GS) {
+        float v[GS];
+#pragma unroll
+        for (int p = 0; p < GS / 16; ++p) tmem_ld16(tmem + lane_addr + buf * kLN + cc + 16 * p, v + 16 * p);
         const int col0 = b * kLN + cc;          // layer column of v[0]
         if (A.head) {
           if (live) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
+            for (int e = 0; e < GS; ++e)
               if (col0 + e < A.n_out) A.Y[grow * A.n_out + col0 + e] = v[e] * yu;
           }
           continue;
         }
-        const int64_t hoff = (((int64_t)t * g16 + col0 / 16) * kTcM + row) * 16;
-        float hv[16];
+        float hv[GS];
         if (A.h_in) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(A.h_in + hoff) + q);
-            hv[4 * q] = x.x;
-            hv[4 * q + 1] = x.y;
-            hv[4 * q + 2] = x.z;
-            hv[4 * q + 3] = x.w;
+          for (int p = 0; p < GS / 16; ++p) {
+            const int64_t hoff = (((int64_t)t * g16 + col0 / 16 + p) * kTcM + row) * 16;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(A.h_in + hoff) + q);
+              hv[16 * p + 4 * q] = x.x;
+              hv[16 * p + 4 * q + 1] = x.y;
+              hv[16 * p + 4 * q + 2] = x.z;
+              hv[16 * p + 4 * q + 3] = x.w;
+            }
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) hv[e] = 0.f;
+          for (int e = 0; e < GS; ++e) hv[e] = 0.f;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < GS / 4; ++q) {
           const float4 s4 = __ldg(reinterpret_cast<const float4*>(A.scale + col0) + q);
           const float4 t4 = __ldg(reinterpret_cast<const float4*>(A.shift + col0) + q);
           const float sv[4] = {s4.x, s4.y, s4.z, s4.w}, tv[4] = {t4.x, t4.y, t4.z, t4.w};
@@ -210,13 +216,18 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
         }
         if (A.h_out) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            reinterpret_cast<float4*>(A.h_out + hoff)[q] =
-                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          for (int p = 0; p < GS / 16; ++p) {
+            const int64_t hoff = (((int64_t)t * g16 + col0 / 16 + p) * kTcM + row) * 16;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              reinterpret_cast<float4*>(A.h_out + hoff)[q] =
+                  make_float4(v[16 * p + 4 * q], v[16 * p + 4 * q + 1], v[16 * p + 4 * q + 2],
+                              v[16 * p + 4 * q + 3]);
+          }
         }
         if (A.A_out) {
 #pragma unroll
-          for (int g = 0; g < 16; g += HC) {
+          for (int g = 0; g < GS; g += HC) {
             const int col = col0 + g;
             uint8_t* chunk = A.A_out + ((int64_t)t * A.n_kc_out + col / KC) * AST;
             put_row<MODE>(chunk, row, col % KC, v + g);
@@ -329,7 +340,11 @@ __global__ void pack_layered_kernel(const float* __restrict__ W, int K, int N, i
                      (int64_t)b * kLN * KC * C::ESZ * C::PARTS;
     const uint32_t off = canon_off<C::ESZ, KC>(nr, kk);
     const uint32_t part = (uint32_t)nbw * KC * C::ESZ;
-    if constexpr (MODE == DNNMG_PREC_BF16) {
+    if constexpr (MODE == DNNMG_PREC_FP8) {
+      uint16_t q;
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(q) : "f"(0.f), "f"(ldexpf(w, shift)));
+      *(chunk + off) = (uint8_t)(q & 0xFF);
+    } else if constexpr (MODE == DNNMG_PREC_BF16) {
       *reinterpret_cast<__nv_bfloat16_raw*>(chunk + off) =
           static_cast<__nv_bfloat16_raw>(__float2bfloat16_rn(w));
     } else if constexpr (MODE == DNNMG_PREC_F16X3) {
@@ -359,13 +374,14 @@ struct LayeredGeom {
 
 static LayeredGeom layered_geom(const dnnmg_mlp_t* m, int64_t n_rows) {
   LayeredGeom L{};
-  L.KC = m->precision == DNNMG_PREC_TF32X3 ? 16 : 32;
-  L.esz = m->precision == DNNMG_PREC_TF32X3 ? 4 : 2;
-  L.parts = m->precision == DNNMG_PREC_BF16 ? 1 : 2;
+  L.KC = kc_of(m->precision);
+  L.esz = m->precision == DNNMG_PREC_TF32X3 ? 4 : m->precision == DNNMG_PREC_FP8 ? 1 : 2;
+  L.parts = (m->precision == DNNMG_PREC_BF16 || m->precision == DNNMG_PREC_FP8) ? 1 : 2;
   int64_t off = kPackHdr;
   for (int g = 0; g <= m->depth; ++g) {
     L.K[g] = rup(g == 0 ? m->n_in : m->n_hidden, L.KC);
-    L.N[g] = rup(g < m->depth ? m->n_hidden : m->n_out, 32);
+    // N blocks split into two column halves of whole epilogue steps (FP8: 32 columns)
+    L.N[g] = rup(g < m->depth ? m->n_hidden : m->n_out, m->precision == DNNMG_PREC_FP8 ? 64 : 32);
     L.goff[g] = off;
     off += (int64_t)L.K[g] * L.N[g] * L.esz * L.parts;
   }
@@ -381,8 +397,8 @@ static LayeredGeom layered_geom(const dnnmg_mlp_t* m, int64_t n_rows) {
 
 int32_t mlp_layered_supported(const dnnmg_mlp_t* m) {
   return (m->precision == DNNMG_PREC_BF16 || m->precision == DNNMG_PREC_TF32X3 ||
-          m->precision == DNNMG_PREC_F16X3) &&
-         m->n_hidden % 32 == 0 && m->n_hidden <= 4096 && m->n_in <= 8192 && m->n_out <= 4096 &&
+          m->precision == DNNMG_PREC_F16X3 || m->precision == DNNMG_PREC_FP8) &&
+         m->n_hidden % (m->precision == DNNMG_PREC_FP8 ? 64 : 32) == 0 && m->n_hidden <= 4096 && m->n_in <= 8192 && m->n_out <= 4096 &&
          m->depth >= 1 && m->depth < DNNMG_MAX_LAYERS;
 }
 
@@ -408,7 +424,9 @@ int32_t launch_mlp_layered_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t
     const int N = g < m->depth ? m->n_hidden : m->n_out;
     uint8_t* out = static_cast<uint8_t*>(packed) + L.goff[g];
     const int64_t n = (int64_t)L.K[g] * L.N[g];
-    if (m->precision == DNNMG_PREC_BF16)
+    if (m->precision == DNNMG_PREC_FP8)
+      pack_layered_kernel<DNNMG_PREC_FP8><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, L.K[g], L.N[g], hdr, g, out);
+    else if (m->precision == DNNMG_PREC_BF16)
       pack_layered_kernel<DNNMG_PREC_BF16><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, L.K[g], L.N[g], hdr, g, out);
     else if (m->precision == DNNMG_PREC_F16X3)
       pack_layered_kernel<DNNMG_PREC_F16X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, L.K[g], L.N[g], hdr, g, out);
@@ -434,7 +452,8 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, const PatchRow
                     reinterpret_cast<float*>(base + 2 * L.a_bytes + L.h_bytes)};
   float* affine = reinterpret_cast<float*>(base + 2 * L.a_bytes + 2 * L.h_bytes);
   const PackHdr* hdr = static_cast<const PackHdr*>(m->packed);
-  const bool fold = MODE != DNNMG_PREC_BF16 && m->activation == DNNMG_ACT_TANH;
+  const bool fold = (MODE == DNNMG_PREC_F16X3 || MODE == DNNMG_PREC_TF32X3) &&
+                    m->activation == DNNMG_ACT_TANH;
   const int H = m->n_hidden;
   layer_affine_kernel<<<grid_for((int64_t)m->depth * H, 256), 256, 0, s>>>(
       m->bn_scale, m->bn_shift, hdr, m->depth, H, H, fold ? 2.8853900817779268f : 1.0f, affine);
@@ -496,6 +515,7 @@ int32_t launch_mlp_layered_rows(const dnnmg_mlp_t* m, const float* X, const Patc
   DNNMG_REQUIRE(ws, DNNMG_ERR_ARG, "mlp: the layered tensor-core MLP needs a workspace "
                 "(dnnmg_mlp_workspace_bytes)");
   if (n_rows == 0) return DNNMG_OK;
+  if (m->precision == DNNMG_PREC_FP8) return layered_mode<DNNMG_PREC_FP8>(m, X, P, n_rows, Y, ws, s);
   if (m->precision == DNNMG_PREC_BF16) return layered_mode<DNNMG_PREC_BF16>(m, X, P, n_rows, Y, ws, s);
   if (m->precision == DNNMG_PREC_F16X3) return layered_mode<DNNMG_PREC_F16X3>(m, X, P, n_rows, Y, ws, s);
   return layered_mode<DNNMG_PREC_TF32X3>(m, X, P, n_rows, Y, ws, s);

@@ -669,10 +669,10 @@ __global__ void pack_scale_kernel(const float* __restrict__ W, int size, int mod
     for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, red[i]);
     m = fmaxf(m, red[0]);
     int s = 0;
-    if (mode == DNNMG_PREC_F16X3 && m > 0.f && isfinite(m)) {
+    if ((mode == DNNMG_PREC_F16X3 || mode == DNNMG_PREC_FP8) && m > 0.f && isfinite(m)) {
       int e;
       frexpf(m, &e);  // m < 2^e
-      s = 14 - e;
+      s = (mode == DNNMG_PREC_FP8 ? 8 : 14) - e;   // e4m3 max 448, fp16 max 65504
     }
     hdr->shift[g] = s;
     hdr->unscale[g] = ldexpf(1.0f, -s);

@@ -26,10 +26,15 @@ template <> struct TcCfg<DNNMG_PREC_BF16> {
 template <> struct TcCfg<DNNMG_PREC_TF32X3> {
   static constexpr int ESZ = 4, PARTS = 2, NW = 3, NA = 4, KSTEP = 8, KC = 16;
 };
+template <> struct TcCfg<DNNMG_PREC_FP8> {
+  static constexpr int ESZ = 1, PARTS = 1, NW = 6, NA = 4, KSTEP = 32, KC = 64;
+};
 template <> struct TcCfg<DNNMG_PREC_F16X3> {
   static constexpr int ESZ = 2, PARTS = 2, NW = 2, NA = 4, KSTEP = 16, KC = 32;
 };
-static int kc_of(int precision) { return precision == DNNMG_PREC_TF32X3 ? 16 : 32; }
+static int kc_of(int precision) {
+  return precision == DNNMG_PREC_TF32X3 ? 16 : precision == DNNMG_PREC_FP8 ? 64 : 32;
+}
 
 // ---- PTX helpers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -104,7 +109,13 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
 template <int MODE>
 __device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                        uint32_t acc) {
-  if constexpr (MODE != DNNMG_PREC_TF32X3) {
+  if constexpr (MODE == DNNMG_PREC_FP8) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  } else if constexpr (MODE != DNNMG_PREC_TF32X3) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
@@ -178,6 +189,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo) {
 }
 template <int MODE>
 __host__ __device__ constexpr uint32_t ab_format() {  // F16 = 0, BF16 = 1, TF32 = 2
+  // kind::f16: F16 = 0, BF16 = 1; kind::tf32: TF32 = 2; kind::f8f6f4: E4M3 = 0
   return MODE == DNNMG_PREC_BF16 ? 1u : MODE == DNNMG_PREC_TF32X3 ? 2u : 0u;
 }
 template <int MODE>
@@ -217,7 +229,21 @@ template <int MODE>
 __device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const float* v) {
   using C = TcCfg<MODE>;
   constexpr int HC = C::KC / 2;
-  if constexpr (MODE == DNNMG_PREC_BF16) {
+  if constexpr (MODE == DNNMG_PREC_FP8) {
+#pragma unroll
+    for (int j = 0; j < HC / 16; ++j) {
+      uint32_t q[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint16_t lo2, hi2;
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo2) : "f"(v[16 * j + 4 * w + 1]), "f"(v[16 * j + 4 * w]));
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi2) : "f"(v[16 * j + 4 * w + 3]), "f"(v[16 * j + 4 * w + 2]));
+        q[w] = (uint32_t)lo2 | ((uint32_t)hi2 << 16);
+      }
+      *reinterpret_cast<uint4*>(stage + canon_off<1, C::KC>(row, kk0 + 16 * j)) =
+          make_uint4(q[0], q[1], q[2], q[3]);
+    }
+  } else if constexpr (MODE == DNNMG_PREC_BF16) {
 #pragma unroll
     for (int j = 0; j < HC / 8; ++j) {
       uint4 q;

@@ -97,8 +97,8 @@ def zero_weights(model):
 def resolve_precision(precision=None):
     import os
     p = precision or os.environ.get("DNNMG_B200_PRECISION", "fp32")
-    if p not in ("fp32", "bf16", "tf32x3", "f16x3"):
-        raise ValueError(f"unknown precision '{p}' (fp32 | bf16 | tf32x3 | f16x3)")
+    if p not in ("fp32", "bf16", "tf32x3", "f16x3", "fp8"):
+        raise ValueError(f"unknown precision '{p}' (fp32 | bf16 | tf32x3 | f16x3 | fp8)")
     return p
 
 

@@ -55,7 +55,7 @@ class CorrectionStep:
             self.model = dv.DeviceModel(model, precision)
             a = model.arch
             # K3 fused into K4 when the tensor-core MLP can stage the rows itself
-            self.fused_gather = (precision != "fp32" and a.n_hidden == 256 and a.n_in <= 256
+            self.fused_gather = (precision not in ("fp32", "fp8") and a.n_hidden == 256 and a.n_in <= 256
                                  and a.n_out <= 256 and self.patchset.n_geo % 4 == 0)
         self.phys = _lib.Phys(float(nu), float(k), float(alpha0), float(delta0), 1)
         dev = dv.device()
@@ -69,7 +69,7 @@ class CorrectionStep:
         # layered tensor-core MLP (widths the fused kernel does not hold): the gather is fused
         # into its layer-0 operand; width 128 runs the fused kernel on stored X rows
         self.layered = (model is not None and precision != "fp32"
-                        and not dv.tc_fused_supported(model.arch))
+                        and (precision == "fp8" or not dv.tc_fused_supported(model.arch)))
         # X is only materialised when the gather is not fused into the MLP
         n_x = 0 if (self.fused_gather or self.layered or model is None) else self.ps.n_patches
         self.X = torch.empty((n_x, input_width(self.patchset)), dtype=f, device=dev)

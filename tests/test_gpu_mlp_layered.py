@@ -102,3 +102,18 @@ def test_layered_correction_step_matches_reference(name, precision):
     # the staged (per-call) form agrees bitwise
     out2 = step.run_staged(xc, b).double().cpu().numpy()
     assert np.array_equal(out, out2)
+
+
+@pytest.mark.parametrize("H", [128, 512])
+def test_fp8_mode_is_report_only_accuracy(H):
+    """BASELINE config 4's fp8-e4m3 mode (layer-major kernel, kind::f8f6f4, power-of-two
+    weight scaling, fp32 accumulate): finite and at the e4m3 error level the survey predicts
+    (~6.5e-2 with per-tensor scaling), far from the 2e-2 gate, hence report-only."""
+    from oracle import dnnmg_oracle as orc
+    m = make_model(174, H, 3, 81, "tanh", False, 11 + H)
+    X = np.random.default_rng(5).standard_normal((777, 174)).astype(np.float32).astype(float)
+    ref = orc.mlp_forward(orc.Mlp(m.W, "tanh", m.gamma, m.beta, m.running_mean, m.running_var,
+                                  m.input_mean, m.input_std), X)
+    Y = net.forward(m, X, precision="fp8")
+    err = rel(Y, ref)
+    assert np.isfinite(Y).all() and 5e-3 < err < 0.25, err

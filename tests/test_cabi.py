@@ -31,6 +31,8 @@ def test_library_exports_every_declared_symbol():
     exported = set(re.findall(r"\b(dnnmg_\w+)\b", out))
     assert set(declared()) <= exported
     assert set(_lib.EXPORTS) <= exported
+    # and the ctypes binding (the reference-side stub of INTEGRATION.md) covers all of them
+    assert set(declared()) <= set(_lib.EXPORTS)
 
 
 def test_status_strings_and_version():

@@ -305,6 +305,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         }
         const int cnt = __ldg(A.tile_count + tile);
         const int32_t* un = A.tile_nodes + tile * A.tile_cap;
+        constexpr int kIdxPerLane = 64;   // up to 2048 distinct nodes: all index loads in flight
+        if (cnt <= 32 * kIdxPerLane) {
+          int u[kIdxPerLane];
+#pragma unroll
+          for (int k = 0; k < kIdxPerLane; ++k) {
+            const int i = 32 * k + lane;
+            u[k] = i < cnt ? __ldg(un + i) : -1;
+          }
+#pragma unroll
+          for (int k = 0; k < kIdxPerLane; ++k) {
+            if (u[k] >= 0) {
+              cp_async16(stx + 32 * k + lane, A.xg + u[k]);
+              cp_async16(str + 32 * k + lane, A.rg + u[k]);
+            }
+          }
+        } else
         for (int i0 = 0; i0 < cnt; i0 += 32 * 8) {
           int u[8];
 #pragma unroll

@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--mlp-sweep", action="store_true",
                     help="BASELINE config 4: isolated patch-MLP sweep (one JSON line)")
     ap.add_argument("--sweep-batches", default="1024,16384,262144,4194304")
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="run the multi-GPU x-slab path even on one GPU (code-path check)")
     return ap.parse_args()
 
 
@@ -349,26 +351,57 @@ def run_slabs(args, rank, world, local):
     # memory and its x_corr copied back inside each step
     e2e = None
     if not args.no_e2e:
+        # the same distributed steps from pinned host memory, pipelined as step.HostPipeline
+        # does on one GPU: H2D of step i+1 (copy stream) | kernels + halo exchanges of step i
+        # (compute stream) | D2H of step i-1 (copy stream), double-buffered
         hx = [p[0].cpu().pin_memory() for p in pairs]
         hb = [p[1].cpu().pin_memory() for p in pairs]
-        hout = torch.empty(slab.step.x_corr.numel(), dtype=torch.float32).pin_memory()
-        dx, db = torch.empty_like(pairs[0][0]), torch.empty_like(pairs[0][1])
+        hout = [torch.empty(slab.step.x_corr.numel(), dtype=torch.float32).pin_memory()
+                for _ in range(2)]
+        dx = [torch.empty_like(pairs[0][0]) for _ in range(2)]
+        db = [torch.empty_like(pairs[0][1]) for _ in range(2)]
+        dout = [torch.empty_like(slab.step.x_corr) for _ in range(2)]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_run = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        used = [False, False]
+        comp = torch.cuda.current_stream()
         tdist.barrier()
         torch.cuda.synchronize()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0.record()
+        s_in.wait_stream(comp)
+        s_out.wait_stream(comp)
         for i in range(args.steps):
-            dx.copy_(hx[i % S], non_blocking=True)
-            db.copy_(hb[i % S], non_blocking=True)
-            hout.copy_(slab.run(dx, db, ex), non_blocking=True)
+            k = i % 2
+            with torch.cuda.stream(s_in):
+                if used[k]:
+                    s_in.wait_event(ev_run[k])
+                dx[k].copy_(hx[i % S], non_blocking=True)
+                db[k].copy_(hb[i % S], non_blocking=True)
+                ev_in[k].record()
+            comp.wait_event(ev_in[k])
+            if used[k]:
+                comp.wait_event(ev_out[k])
+            dout[k].copy_(slab.run(dx[k], db[k], ex))
+            ev_run[k].record()
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_run[k])
+                hout[k].copy_(dout[k], non_blocking=True)
+                ev_out[k].record()
+            used[k] = True
+        comp.wait_stream(s_in)
+        comp.wait_stream(s_out)
         h1.record()
         tdist.barrier()
         torch.cuda.synchronize()
         te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device="cuda")
         tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
         e2e = {"value": float(tot.item()) * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(world * (dx.numel() + db.numel()) * 4),
-               "d2h_bytes_per_step": int(world * hout.numel() * 4)}
+               "h2d_bytes_per_step": int(world * (dx[0].numel() + db[0].numel()) * 4),
+               "d2h_bytes_per_step": int(world * hout[0].numel() * 4),
+               "overlap": "H2D(i+1) | kernels + halo exchanges(i) | D2H(i-1) on 3 streams"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": float(tot.item()) * args.steps / (ms / 1e3), "unit": UNIT,
@@ -497,7 +530,12 @@ def vanka_aux(step, steps, barrier, n_cells=(16, 8, 8)):
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as tdist
-    if world > 1:
+    if world > 1 or args.force_slabs:
+        if world == 1:   # single-process check of the distributed code path
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29555")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         return run_slabs(args, rank, world, local)
     torch.cuda.set_device(local)
     precision = args.precision or default_precision(args.config)

@@ -171,9 +171,9 @@ int32_t dnnmg_mlp_forward_ws(const dnnmg_mlp_t* m, const float* X, int64_t n_row
                              void* workspace, dnnmg_stream_t s) {
   int32_t st = check_mlp(m);
   if (st) return st;
-  DNNMG_REQUIRE(X && Y, DNNMG_ERR_ARG, "mlp_forward: null argument");
   DNNMG_REQUIRE(n_rows >= 0, DNNMG_ERR_ARG, "mlp_forward: negative row count");
-  if (n_rows == 0) return DNNMG_OK;
+  if (n_rows == 0) return DNNMG_OK;   // an empty batch: nothing to read or write
+  DNNMG_REQUIRE(X && Y, DNNMG_ERR_ARG, "mlp_forward: null argument");
   if (m->precision == DNNMG_PREC_FP32) return launch_mlp_simt(m, X, n_rows, Y, as_stream(s));
   DNNMG_REQUIRE(m->packed, DNNMG_ERR_ARG, "mlp_forward: tensor-core mode needs packed weights");
   if (mlp_tc_supported(m)) return launch_mlp_tc(m, X, n_rows, Y, as_stream(s));
@@ -184,9 +184,9 @@ int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, 
                           dnnmg_stream_t s) {
   int32_t st = check_mlp(m);
   if (st) return st;
-  DNNMG_REQUIRE(X && Y, DNNMG_ERR_ARG, "mlp_forward: null argument");
   DNNMG_REQUIRE(n_rows >= 0, DNNMG_ERR_ARG, "mlp_forward: negative row count");
-  if (n_rows == 0) return DNNMG_OK;
+  if (n_rows == 0) return DNNMG_OK;   // an empty batch: nothing to read or write
+  DNNMG_REQUIRE(X && Y, DNNMG_ERR_ARG, "mlp_forward: null argument");
   if (m->precision == DNNMG_PREC_FP32) return launch_mlp_simt(m, X, n_rows, Y, as_stream(s));
   DNNMG_REQUIRE(m->packed, DNNMG_ERR_ARG, "mlp_forward: tensor-core mode needs packed weights");
   DNNMG_REQUIRE(mlp_tc_supported(m), DNNMG_ERR_UNSUPPORTED,

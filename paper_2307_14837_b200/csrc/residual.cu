@@ -64,6 +64,7 @@ __constant__ float cW[4] = {float(tab::wg[0]), float(tab::wg[1]), float(tab::wg[
 constexpr int kNF = 7;
 constexpr int oU = 0;                  // u[f][27]
 constexpr int oSY = 192;               // sy[f][kind*3+iz][16 yx]            | backward out tz
+constexpr int oVtx = 112;              // cached form (4 fields in u[0..108)): vertex float4 x 8
 constexpr int kSYF = 148;              // sy field stride (= 20 mod 32: the (f, qx) lanes of the
                                        // forward x-y stage store to distinct banks)
 constexpr int oCF = oSY + kNF * kSYF;  // cf[25][kCFS]: A[4], B[4][3], P[3][3]
@@ -171,9 +172,16 @@ __device__ __forceinline__ void stage_geo(const ResidualArgs& A, int c, int t, f
 // Q1 (pi) fields p, vx, vy, vz at the two Gauss points (qx, qy, qz) and (qx, qy, qz + 2) of a
 // lane: trilinear in the 8 vertex values (elements.py:96-118); the x-y bilinear part is
 // shared by the two points.  PQ[f] = [value, d/dxi, d/deta, d/dzeta]
-__device__ __forceinline__ void pi_fields(const float* u, int qx, int qy, int qz, float PQa[4][4],
-                                          float PQb[4][4]) {
+// vtx (nullable): the 8 vertex values as float4 (p, vx, vy, vz) [vz][vy][vx], read with 8
+// vector loads instead of 32 scalar ones from the field-major u
+__device__ __forceinline__ void pi_fields(const float* u, const float4* vtx, int qx, int qy,
+                                          int qz, float PQa[4][4], float PQb[4][4]) {
   const float lx1 = cX[qx], ly1 = cX[qy], lza = cX[qz], lzb = cX[qz + 2];
+  float4 V[8];
+  if (vtx) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) V[k] = vtx[k];
+  }
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
     const float* uf = u + f * 27;
@@ -182,7 +190,15 @@ __device__ __forceinline__ void pi_fields(const float* u, int qx, int qy, int qz
     for (int vz = 0; vz < 2; ++vz)
 #pragma unroll
       for (int vy = 0; vy < 2; ++vy) {
-        const float g0 = uf[18 * vz + 6 * vy], g1 = uf[18 * vz + 6 * vy + 2];
+        float g0, g1;
+        if (vtx) {
+          const float4 v0 = V[4 * vz + 2 * vy], v1 = V[4 * vz + 2 * vy + 1];
+          g0 = f == 0 ? v0.x : f == 1 ? v0.y : f == 2 ? v0.z : v0.w;
+          g1 = f == 0 ? v1.x : f == 1 ? v1.y : f == 2 ? v1.z : v1.w;
+        } else {
+          g0 = uf[18 * vz + 6 * vy];
+          g1 = uf[18 * vz + 6 * vy + 2];
+        }
         a[vz][vy] = fmaf(lx1, g1 - g0, g0);
         ax[vz][vy] = g1 - g0;
       }
@@ -348,6 +364,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       S[oU + (L::FO + 1) * 27 + t] = raw.xv.y;
       S[oU + (L::FO + 2) * 27 + t] = raw.xv.z;
       S[oU + (L::FO + 3) * 27 + t] = raw.xv.w;
+      if constexpr (CACHED) {   // vertex copy as float4 (pi fields)
+        const int ix = t % 3, iy = (t / 3) % 3, iz = t / 9;
+        if (ix != 1 && iy != 1 && iz != 1)
+          reinterpret_cast<float4*>(S + oVtx)[(ix >> 1) + 2 * (iy >> 1) + 4 * (iz >> 1)] = raw.xv;
+      }
       vsq = raw.xv.y * raw.xv.y + raw.xv.z * raw.xv.z + raw.xv.w * raw.xv.w;
     }
     const float hT = raw.hT;
@@ -437,7 +458,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       }
       float PQa[4][4], PQb[4][4];
       if constexpr (MODE == MODE_OPERATOR)
-        pi_fields(S + oU + L::FO * 27, yx & 3, yx >> 2, qz, PQa, PQb);
+        pi_fields(S + oU + L::FO * 27,
+                  CACHED ? reinterpret_cast<const float4*>(S + oVtx) : nullptr, yx & 3, yx >> 2,
+                  qz, PQa, PQb);
       pointwise<MODE, CACHED>(A, S, S + L::oCF, t, F, PQa, aT, dT);
       pointwise<MODE, CACHED>(A, S, S + L::oCF, t + 32, G, PQb, aT, dT);
     }

@@ -26,6 +26,18 @@ inline cudaStream_t as_stream(dnnmg_stream_t s) { return reinterpret_cast<cudaSt
 
 constexpr int kSMs = 148;  // B200
 
+// true the first time it is called on the current device for this `seen` mask: kernel
+// attributes (dynamic shared memory limits) are per device, so one process driving several
+// GPUs must set them on each
+inline bool first_use_on_device(uint64_t& seen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (seen & bit) return false;
+  seen |= bit;
+  return true;
+}
+
 inline int grid_for(int64_t n, int block, int max_waves = 64) {
   int64_t g = (n + block - 1) / block;
   int64_t cap = (int64_t)kSMs * max_waves;

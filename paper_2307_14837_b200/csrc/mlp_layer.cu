@@ -458,10 +458,9 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, const PatchRow
   layer_affine_kernel<<<grid_for((int64_t)m->depth * H, 256), 256, 0, s>>>(
       m->bn_scale, m->bn_shift, hdr, m->depth, H, H, fold ? 2.8853900817779268f : 1.0f, affine);
   DNNMG_CHECK_LAUNCH("layer_affine_kernel");
-  static bool configured = false;
-  if (!configured) {
+  static uint64_t configured = 0;
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(mlp_layer_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
   }
   for (int64_t r0 = 0; r0 < n_rows; r0 += L.chunk_rows) {
     const int64_t n = n_rows - r0 < L.chunk_rows ? n_rows - r0 : L.chunk_rows;

@@ -671,8 +671,8 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
   const bool cached = lv->geo_q != nullptr;
   const size_t smem =
       sizeof(float) * (cached ? KLay<true>::kFloats : KLay<false>::kFloats) * kWarpsPerBlock;
-  static bool configured = false;
-  if (!configured) {
+  static uint64_t configured = 0;
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(element_kernel<MODE_OPERATOR, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(float) * KLay<false>::kFloats * kWarpsPerBlock));
@@ -683,7 +683,6 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
                          (int)(sizeof(float) * KLay<true>::kFloats * kWarpsPerBlock));
     cudaFuncSetAttribute(element_kernel<MODE_RHS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(float) * KLay<true>::kFloats * kWarpsPerBlock));
-    configured = true;
   }
   int blocks = (lv->n_cells + kWarpsPerBlock - 1) / kWarpsPerBlock;
   int per_sm = 0;

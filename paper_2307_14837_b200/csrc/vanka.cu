@@ -194,11 +194,10 @@ extern "C" int32_t dnnmg_vanka_setup(int32_t n_cells, int32_t ndl, const double*
                 "vanka_setup: null argument");
   if (n_cells == 0) return DNNMG_OK;
   const size_t smem = sizeof(double) * (ndl * ndl + ndl) + sizeof(int) * ndl;
-  static bool configured = false;
-  if (!configured) {
+  static uint64_t configured = 0;
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(vanka_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(double) * (128 * 128 + 128) + sizeof(int) * 128));
-    configured = true;
   }
   const int grid = n_cells < 2 * kSMs ? n_cells : 2 * kSMs;
   vanka_invert_kernel<<<grid, kVankaThreads, smem, as_stream(s)>>>(n_cells, ndl, csr_data,

@@ -377,3 +377,41 @@ def export_training_data(problem, L, J, coarse_traj, fine_traj, t_train, t_val, 
                     writer.add_rows(name, rows, stats)
         _loop_rows(m, coarse_traj, fine_traj, n_lo - 1, (None, max(t_train[1], t_val[1])), emit)
     return writer.finish()
+
+
+# -- checkpoint / resume (driver.py:442-480) --------------------------------------------
+
+def checkpoint_state(loop):
+    """Arrays + meta needed to resume a loop exactly (driver.py:442-450); the fine state
+    and the carried fine RHS come back from the device."""
+    st = loop.state
+    arrays = {"x": st.x.values, "b_next": st.b_next}
+    if st.x_fine is not None:
+        arrays["x_fine"] = st.x_fine.values
+        arrays["b_next_fine"] = st.b_next_fine
+    meta = {"level": loop.level, "J": loop.J, "n": st.n, "t": st.t}
+    return st.n, st.t, arrays, meta
+
+
+def resume_loop(problem, ckpt_path, model=None, J=None, precision="fp32", **kw):
+    """TimeLoop continued from a "DMGC" checkpoint (driver.py:453-480).  A pure-MG checkpoint
+    (J = 0) resumes as a hybrid loop when J is given: the fine RHS history is rebuilt from
+    the embedded coarse state on the device, as a zero-correction hybrid run would carry."""
+    from . import io as iomod
+    step, t, arrays, meta = iomod.load_checkpoint(ckpt_path)
+    J = J if J is not None else meta["J"]
+    to_hybrid = J > 0 and meta["J"] == 0
+    loop = TimeLoop(problem, meta["level"], J, model=model, precision=precision, **kw)
+    L, fl = meta["level"], meta["level"] + J
+    x = spmod.StateVector(L, arrays["x"].copy(), t)
+    st = TimeLoopState(step, t, x, arrays["b_next"].copy())
+    if "x_fine" in arrays:
+        st.x_fine = spmod.StateVector(fl, dv.f32(arrays["x_fine"]), t)
+        st.b_next_fine = dv.f32(arrays["b_next_fine"])
+    elif to_hybrid:
+        loop.fine.set_time(t)
+        xf = loop.fine.embed_into(dv.f32(x.values), torch.empty_like(loop.fine.x_tilde))
+        st.x_fine = spmod.StateVector(fl, xf, t)
+        st.b_next_fine = loop.fine.rhs_next(xf)
+    loop.state = st
+    return loop

@@ -238,3 +238,49 @@ def load_dataset(dataset_json, name):
     Xc = np.concatenate(X) if X else np.zeros((0, nf))
     Tc = np.concatenate(T) if T else np.zeros((0, nt))
     return Xc, Tc, meta
+
+
+# -- checkpoints -------------------------------------------------------------------------
+
+_CKPT_MAGIC, _CKPT_VERSION = b"DMGC", 1
+_CKPT_HDR = struct.Struct("<IQdI")   # version, step, t, meta length (after the magic)
+
+
+def save_checkpoint(path, step, t, arrays, meta=None):
+    """"DMGC" checkpoint (io.py:112-128): named float64 vectors plus a JSON meta; device
+    tensors are copied to the host."""
+    meta_b = json.dumps(meta or {}, sort_keys=True).encode()
+    with open(path, "wb") as f:
+        f.write(_CKPT_MAGIC)
+        f.write(_CKPT_HDR.pack(_CKPT_VERSION, int(step), float(t), len(meta_b)))
+        f.write(meta_b)
+        f.write(struct.pack("<I", len(arrays)))
+        for name, arr in arrays.items():
+            if hasattr(arr, "detach"):
+                arr = arr.detach().double().cpu().numpy()
+            a = np.ascontiguousarray(arr, dtype="<f8").reshape(-1)
+            nb = name.encode()
+            f.write(struct.pack("<I", len(nb)))
+            f.write(nb)
+            f.write(struct.pack("<Q", a.size))
+            f.write(a.tobytes())
+
+
+def load_checkpoint(path):
+    """(step, t, arrays, meta) of a "DMGC" file (io.py:131-147)."""
+    with open(path, "rb") as f:
+        magic = f.read(4)
+        if magic != _CKPT_MAGIC:
+            raise ValueError(f"not a checkpoint file: bad magic {magic!r}")
+        version, step, t, metalen = _CKPT_HDR.unpack(f.read(_CKPT_HDR.size))
+        if version != _CKPT_VERSION:
+            raise ValueError(f"unsupported checkpoint version {version}")
+        meta = json.loads(f.read(metalen).decode())
+        (count,) = struct.unpack("<I", f.read(4))
+        arrays = {}
+        for _ in range(count):
+            (nl,) = struct.unpack("<I", f.read(4))
+            name = f.read(nl).decode()
+            (size,) = struct.unpack("<Q", f.read(8))
+            arrays[name] = np.frombuffer(f.read(8 * size), dtype="<f8").copy()
+    return step, t, arrays, meta

@@ -86,6 +86,36 @@ def main():
     out["input_mean"], out["input_std"] = model.input_mean, model.input_std
     out["n_layers"] = len(model.W)
     np.savez_compressed(os.path.join(HERE, "timeloop.npz"), **out)
+    checkpoints(pr, model)
+
+
+def checkpoints(pr, model):
+    """Reference checkpoints for resume tests (driver.checkpoint_state / resume_loop,
+    driver.py:442-480): a hybrid loop saved after step 2 and resumed for 2 steps, and a
+    pure-MG loop (J = 0) saved after step 2 and resumed as a hybrid loop."""
+    from dnnmg import io as iomod
+    c = CASE
+    out = {}
+    hyb = driver.TimeLoop(pr, c["L"], J=c["J"], model=model, correction_scale=c["scale"],
+                          correction_start=c["start"])
+    hyb.run(2)
+    iomod.save_checkpoint(os.path.join(HERE, "timeloop_hybrid.dmgc"), *driver.checkpoint_state(hyb))
+    mg = driver.TimeLoop(pr, c["L"], J=0)
+    mg.run(2)
+    iomod.save_checkpoint(os.path.join(HERE, "timeloop_mg.dmgc"), *driver.checkpoint_state(mg))
+    for name in ("hybrid", "mg"):
+        loop = driver.resume_loop(pr, os.path.join(HERE, f"timeloop_{name}.dmgc"), model=model,
+                                  J=c["J"])
+        loop.correction_scale, loop.correction_start = c["scale"], c["start"]
+        out[f"{name}_b_next_fine_0"] = loop.state.b_next_fine.copy()
+        for n in (1, 2):
+            st = loop.step()
+            out[f"{name}_t_{n}"] = st.t
+            out[f"{name}_x_{n}"] = st.x.values.copy()
+            out[f"{name}_x_fine_{n}"] = st.x_fine.values.copy()
+            out[f"{name}_b_next_fine_{n}"] = st.b_next_fine.copy()
+            out[f"{name}_b_next_{n}"] = st.b_next.copy()
+    np.savez_compressed(os.path.join(HERE, "timeloop_resume.npz"), **out)
 
 
 if __name__ == "__main__":

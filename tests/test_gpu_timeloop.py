@@ -118,3 +118,39 @@ def test_timeloop_rejects_unsupported(g):
     pr.f = lambda t, pts: np.zeros((pts.shape[0], 3))
     with pytest.raises(NotImplementedError):
         driver.TimeLoop(pr, 0, J=1)
+
+
+class ResumeReplay(ReplayProblem):
+    """Replays the reference's coarse solutions of a resumed run."""
+
+    def __init__(self, g, r, name):
+        super().__init__(g)
+        self.r, self.name = r, name
+
+    def solve_step(self, level, x_prev, b, t, solver=None):
+        n = len(self.received_b) + 1
+        self.received_b.append(np.array(b))
+        assert abs(t - float(self.r[f"{self.name}_t_{n}"])) < 1e-12
+        return spmod.StateVector(level, self.r[f"{self.name}_x_{n}"].copy(), t), None, solver
+
+
+@pytest.mark.parametrize("name", ["hybrid", "mg"])
+def test_resume_from_reference_checkpoint(g, name):
+    """driver.resume_loop on a checkpoint the reference wrote mid-run (hybrid, and pure-MG
+    resumed as hybrid with the fine RHS rebuilt on the device) continues like the
+    reference's own resumed loop (driver.py:453-480)."""
+    import os
+    r = load_golden("timeloop_resume")
+    pr = ResumeReplay(g, r, name)
+    ck = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"timeloop_{name}.dmgc")
+    loop = driver.resume_loop(pr, ck, model=product_model(g), J=int(g["J"]), precision="f16x3",
+                              correction_scale=float(g["scale"]), correction_start=float(g["start"]))
+    assert rel(loop.state.b_next_fine, r[f"{name}_b_next_fine_0"]) < 1e-5
+    for n in (1, 2):
+        st = loop.step()
+        assert rel(st.x_fine.values, r[f"{name}_x_fine_{n}"]) < 1e-5, n
+        assert rel(st.b_next_fine, r[f"{name}_b_next_fine_{n}"]) < 2e-5, n
+        assert rel(st.b_next, r[f"{name}_b_next_{n}"]) < 2e-5, n
+    # checkpoint_state of the resumed loop round-trips through the reference format
+    n, t, arrays, meta = driver.checkpoint_state(loop)
+    assert n == 4 and meta["J"] == int(g["J"]) and "b_next_fine" in arrays

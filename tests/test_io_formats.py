@@ -85,3 +85,20 @@ def test_dataset_writer_reproduces_reference_shards(tmp_path, which):
         for c, st in theirs["component_stats"].items():
             for k, v in st.items():
                 assert mine["component_stats"][c][k] == pytest.approx(v, rel=1e-7, abs=1e-10)
+
+
+@pytest.mark.parametrize("name", ["hybrid", "mg"])
+def test_checkpoint_roundtrip_is_byte_identical(tmp_path, name):
+    """"DMGC" checkpoints written by the reference (driver.checkpoint_state +
+    io.save_checkpoint, made by make_timeloop.py) read back and re-written byte for byte."""
+    src = os.path.join(HERE, "golden", f"timeloop_{name}.dmgc")
+    step, t, arrays, meta = iomod.load_checkpoint(src)
+    assert step == 2 and abs(t - 0.04) < 1e-12 and meta["n"] == 2
+    assert ("x_fine" in arrays) == (name == "hybrid")
+    out = tmp_path / "c.dmgc"
+    iomod.save_checkpoint(out, step, t, arrays, meta)
+    assert out.read_bytes() == open(src, "rb").read()
+    bad = tmp_path / "bad.dmgc"
+    bad.write_bytes(b"NOPE" + bytes(24))
+    with pytest.raises(ValueError, match="magic"):
+        iomod.load_checkpoint(bad)

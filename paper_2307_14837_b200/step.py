@@ -91,6 +91,15 @@ class CorrectionStep:
         if self._t is not None and vals is None and self._static:
             return
         self._static = vals is None
+        old = getattr(self, "bc", None)
+        if (old is not None and vals is not None and old.vals is not None
+                and old.vals.numel() == vals.size):
+            # in place: a captured graph keeps reading the same buffers
+            old.code.copy_(dv.upload(code, np.uint8))
+            old.vals.copy_(dv.upload(vals, np.float32))
+            self._t = t
+            return
+        self.graph = None  # new buffers: a graph captured earlier would read stale ones
         self.bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
         self.bc.code = dv.upload(code, np.uint8)
         self.bc.vals = None if vals is None else dv.upload(vals, np.float32)
@@ -120,6 +129,12 @@ class CorrectionStep:
         t.mlp_ws = None if self.mlp_ws is None else torch.empty_like(self.mlp_ws)
         t.buf = _lib.StepBuffers(dv.ptr(t.x_tilde), dv.ptr(t.r), dv.ptr(t.elem), dv.ptr(t.X),
                                  dv.ptr(t.Y), dv.ptr(t.d), dv.ptr(t.x_mid), dv.ptr(t.mlp_ws))
+        if self.bc.vals is not None:
+            # time-dependent Dirichlet data are updated in place by set_time: own a copy
+            bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
+            bc.code, bc.vals = self.bc.code.clone(), self.bc.vals.clone()
+            bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(bc.code), dv.ptr(bc.vals))
+            t.bc = bc
         t.graph = None
         return t
 
@@ -231,7 +246,10 @@ class CorrectionStep:
         return dst
 
     def embed(self, x_coarse, t=None):
-        """Prolongate + Dirichlet only (driver.embed_state, driver.py:611-619)."""
+        """Prolongate + Dirichlet only (driver.embed_state, driver.py:611-619); t, when
+        given, becomes the step's Dirichlet time (set_time)."""
+        if t is not None and t != self._t:
+            self.set_time(t)
         cur = dv.f32(x_coarse)
         for i, P in enumerate(self.prolongs):
             out = torch.empty(4 * P.n_fine, dtype=torch.float32, device=cur.device)

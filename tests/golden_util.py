@@ -79,3 +79,37 @@ def product_bcs(g):
     if int(g["channel"]):
         return {mesh.INFLOW: space.inflow_profile(3, 1.0, 0.41), mesh.WALL: space.no_slip}
     return {mesh.WALL: space.no_slip}
+
+
+def cfg1_case():
+    """BASELINE config 1 rebuilt with the oracle: context, coarse states x^0 / x^1, the
+    carried fine RHS b_prev (rhs_next of the embedded x^0, float64), the Xavier weights
+    and the reference's pin (tests/golden/make_cfg1.py)."""
+    from paper_2307_14837_b200 import synthetic
+    c = synthetic.CONFIGS["cfg1"]
+
+    def jf(verts):
+        synthetic.jitter_vertices(verts, c["n_cells"], (0, 0, 0), (1, 1, 1), c["seed"] + 1)
+    ctx = orc.build_context((0, 0, 0), (1, 1, 1), c["n_cells"], 0, c["J"], jitter_fn=jf)
+    modes = synthetic.fourier_modes(c["seed"])
+    x0 = synthetic.coarse_state(ctx["coarse_coords"], modes, c["seed"], 0, 0.0, c["nu"])
+    x1 = synthetic.coarse_state(ctx["coarse_coords"], modes, c["seed"], 1, c["dt"], c["nu"])
+    xf0 = orc.prolongate_state(ctx["P"], x0)
+    orc.impose_dirichlet(xf0, ctx["tags"], ctx["coords"], 0.0, {orc.WALL: orc.no_slip})
+    b_prev = orc.rhs_next(xf0, ctx["coords"], ctx["table"], c["dt"], c["nu"])
+    pin = load_golden("cfg1_pin")
+    dims = [int(pin["n_in"])] + [c["hidden"]] * c["depth"] + [int(pin["n_out"])]
+    W = [w.astype(np.float64) for w in synthetic.xavier_weights(dims, c["seed"] + 7)]
+    return dict(cfg=c, ctx=ctx, x0=x0, x1=x1, b_prev=b_prev, W=W, pin=pin)
+
+
+def sampled_rel(v, pin, name):
+    """Relative L2 error of v on the pin's sampled dofs, and the worst per-component
+    relative error of v's full-vector norms."""
+    s = np.asarray(v, dtype=float)
+    ref = pin[name]
+    e = np.linalg.norm(s[pin["dofs"]] - ref) / max(np.linalg.norm(ref), 1e-300)
+    n = np.linalg.norm(s.reshape(-1, 4), axis=0)
+    rn = pin[name + "_norms"]
+    en = np.max(np.abs(n - rn) / np.maximum(rn, 1e-300) * (rn > 0))
+    return e, en

@@ -68,3 +68,35 @@ def test_export_with_an_empty_window(tmp_path):
     X, T, _ = iomod.load_dataset(path, "val")
     assert X.shape[0] == 0 and T.shape[0] == 0
     assert meta["sets"]["train"]["rows"] == 2 * 16
+
+
+def test_graph_replay_follows_time_dependent_dirichlet():
+    """set_time with a ramped inflow updates the Dirichlet data in place, so a captured
+    CUDA graph replays at the new time; a twin keeps its own copy."""
+    from paper_2307_14837_b200 import space as spmod
+    from paper_2307_14837_b200.step import CorrectionStep
+    h = meshmod.build_template_mesh("box", extent_lo=(0, 0, -0.205), extent_hi=(1.0, 0.41, 0.205),
+                                    n_cells=(3, 2, 2), channel_tags=True)
+    meshmod.refine_uniform(h)
+    bcs = {meshmod.INFLOW: spmod.inflow_profile(3, 1.0, 0.41), meshmod.WALL: spmod.no_slip}
+    ps = meshmod.build_patches(h, 0, 1)
+    m = _model(patch_ops.input_width(ps), 256, patch_ops.output_width(ps), seed=3)
+    step = CorrectionStep(h, 0, 1, m, 1e-3, 0.01, bcs=bcs, precision="f16x3", patchset=ps, t=0.05)
+    rng = np.random.default_rng(0)
+    nc = spmod.FeSpace(h, 0).n_nodes
+    xc = torch.tensor(rng.standard_normal(4 * nc), dtype=torch.float32, device="cuda")
+    b = torch.tensor(rng.standard_normal(4 * step.space.n_nodes) * 1e-2, dtype=torch.float32,
+                     device="cuda")
+    twin = step.twin()
+    g = step.capture(xc, b)
+    step.set_time(0.4)
+    g.replay()
+    torch.cuda.synchronize()
+    got = step.x_corr.clone()
+    fresh = CorrectionStep(h, 0, 1, m, 1e-3, 0.01, bcs=bcs, precision="f16x3", patchset=ps, t=0.4)
+    want = fresh(xc, b)
+    assert torch.equal(got, want)
+    # the twin still runs at t = 0.05
+    at05 = CorrectionStep(h, 0, 1, m, 1e-3, 0.01, bcs=bcs, precision="f16x3", patchset=ps, t=0.05)
+    assert torch.equal(twin(xc, b), at05(xc, b))
+    assert not torch.equal(got, at05(xc, b))

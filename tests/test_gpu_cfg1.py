@@ -86,5 +86,5 @@ def test_cfg1_carried_rhs_on_gpu(c1):
     check("b_prev", b, pin, 2e-6)
     step.set_time(c1["cfg"]["dt"])
     out = step(torch.tensor(c1["x1"], dtype=torch.float32, device="cuda"), b)
-    check("r", step.r, pin, 5e-5)
-    check("x_corr", out, pin, 2e-5)
+    check("r", step.r, pin, 2e-5)
+    check("x_corr", out, pin, 1e-5)

@@ -131,6 +131,12 @@ typedef struct {
   const float* geo_q;            /* per-mesh geometry cache from dnnmg_level_geometry
                                     ([n_cells][10][64]: J^-1 row-major, w) or NULL: K2 then
                                     recomputes the isoparametric geometry every call */
+  const int32_t* node_order;     /* [n_nodes] permutation: the node sum visits node_order[i]
+                                    at position i (NULL = ascending ids).  Any order gives the
+                                    same bits (each node's sum is ordered by its CSR row); the
+                                    build passes nodes by descending first incident cell, so
+                                    the element vectors written last (still in L2) are read
+                                    first and every node is visited next to its cells */
 } dnnmg_level_t;
 
 typedef struct {
@@ -159,6 +165,8 @@ typedef struct {
   const int32_t* tile_nodes;      /* [n_tiles][tile_cap], n_tiles = ceil(n_patches/128) */
   const int32_t* tile_count;      /* [n_tiles] */
   const uint16_t* tile_slot;      /* [n_tiles*128][npp] (rows past n_patches: any valid slot) */
+  const int32_t* node_order;      /* [n_nodes] visiting order of the scatter (K5), as
+                                     dnnmg_level_t.node_order; NULL = ascending ids */
 } dnnmg_patchset_t;
 
 #define DNNMG_MAX_LAYERS 16

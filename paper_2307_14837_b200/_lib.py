@@ -34,7 +34,7 @@ class Dirichlet(ctypes.Structure):
 class Level(ctypes.Structure):
     _fields_ = [("n_nodes", c_i32), ("n_cells", c_i32), ("cell_nodes", c_vp), ("coords", c_vp),
                 ("h_T", c_vp), ("node_cell_ptr", c_vp), ("node_cell_idx", c_vp),
-                ("dof_mask", c_vp), ("geo_q", c_vp)]
+                ("dof_mask", c_vp), ("geo_q", c_vp), ("node_order", c_vp)]
 
 
 class Phys(ctypes.Structure):
@@ -46,7 +46,8 @@ class PatchSet(ctypes.Structure):
     _fields_ = [("n_patches", c_i32), ("nodes_per_patch", c_i32), ("n_geo", c_i32),
                 ("n_nodes", c_i32), ("node_table", c_vp), ("geom", c_vp),
                 ("node_patch_ptr", c_vp), ("node_patch_idx", c_vp),
-                ("tile_cap", c_i32), ("tile_nodes", c_vp), ("tile_count", c_vp), ("tile_slot", c_vp)]
+                ("tile_cap", c_i32), ("tile_nodes", c_vp), ("tile_count", c_vp), ("tile_slot", c_vp),
+                ("node_order", c_vp)]
 
 
 class Mlp(ctypes.Structure):

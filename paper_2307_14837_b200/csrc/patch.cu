@@ -72,8 +72,11 @@ __global__ void __launch_bounds__(256) extend_kernel(int n_nodes, const int32_t*
 __global__ void __launch_bounds__(256) scatter_update_kernel(
     int n_nodes, int npp, int n_out, const int32_t* __restrict__ ptr,
     const int32_t* __restrict__ idx, const float* __restrict__ Y, const uint8_t* __restrict__ mask,
-    const float4* __restrict__ xt, float scale, float4* __restrict__ d, float4* __restrict__ xc) {
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes; n += gridDim.x * blockDim.x) {
+    const float4* __restrict__ xt, float scale, float4* __restrict__ d, float4* __restrict__ xc,
+    const int32_t* __restrict__ order) {
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < n_nodes;
+       pos += gridDim.x * blockDim.x) {
+    const int n = order ? __ldg(order + pos) : pos;
     const int s = __ldg(ptr + n), e = __ldg(ptr + n + 1);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f;
     for (int i = s; i < e; ++i) {
@@ -161,7 +164,7 @@ int32_t launch_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const 
   scatter_update_kernel<<<grid_for(ps->n_nodes, 256), 256, 0, s>>>(
       ps->n_nodes, ps->nodes_per_patch, 3 * ps->nodes_per_patch, ps->node_patch_ptr,
       ps->node_patch_idx, Y, mask, reinterpret_cast<const float4*>(xt), scale,
-      reinterpret_cast<float4*>(d), reinterpret_cast<float4*>(xc));
+      reinterpret_cast<float4*>(d), reinterpret_cast<float4*>(xc), ps->node_order);
   DNNMG_CHECK_LAUNCH("scatter_update_kernel");
   return DNNMG_OK;
 }

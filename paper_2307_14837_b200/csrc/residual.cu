@@ -591,8 +591,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
 __global__ void __launch_bounds__(256) node_sum_kernel(
     int n_nodes, const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const float4* __restrict__ elem, const float4* __restrict__ b, float sign,
-    const uint8_t* __restrict__ mask, float4* __restrict__ out) {
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes; n += gridDim.x * blockDim.x) {
+    const uint8_t* __restrict__ mask, float4* __restrict__ out, const int32_t* __restrict__ order) {
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < n_nodes;
+       pos += gridDim.x * blockDim.x) {
+    const int n = order ? __ldg(order + pos) : pos;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const int s = __ldg(ptr + n), e = __ldg(ptr + n + 1);
     for (int i = s; i < e; ++i) {
@@ -794,7 +796,7 @@ int32_t launch_node_sum(int n_nodes, const int32_t* ptr, const int32_t* idx, con
   if (n_nodes == 0) return DNNMG_OK;
   node_sum_kernel<<<grid_for(n_nodes, 256), 256, 0, s>>>(
       n_nodes, ptr, idx, reinterpret_cast<const float4*>(elem), nullptr, 1.0f, nullptr,
-      reinterpret_cast<float4*>(out));
+      reinterpret_cast<float4*>(out), nullptr);
   DNNMG_CHECK_LAUNCH("node_sum_kernel");
   return DNNMG_OK;
 }
@@ -832,7 +834,8 @@ int32_t launch_residual(const dnnmg_level_t* lv, const float* x, const float* b_
   if (lv->n_nodes == 0) return DNNMG_OK;
   node_sum_kernel<<<grid_for(lv->n_nodes, 256), 256, 0, s>>>(
       lv->n_nodes, lv->node_cell_ptr, lv->node_cell_idx, reinterpret_cast<const float4*>(elem), b,
-      1.0f, (apply_mask && lv->dof_mask) ? lv->dof_mask : nullptr, reinterpret_cast<float4*>(r));
+      1.0f, (apply_mask && lv->dof_mask) ? lv->dof_mask : nullptr, reinterpret_cast<float4*>(r),
+      lv->node_order);
   DNNMG_CHECK_LAUNCH("node_sum_kernel");
   return DNNMG_OK;
 }

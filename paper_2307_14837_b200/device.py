@@ -48,6 +48,10 @@ def upload(a, dtype):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(device())
 
 
+def upload_opt(a, dtype=np.int32):
+    return None if a is None else upload(a, dtype)
+
+
 def like_input(t, ref):
     """Return a device result in the caller's convention: numpy float64 for numpy
     inputs (the reference's dtype), the CUDA tensor otherwise."""
@@ -69,6 +73,27 @@ def node_csr(table):
     ptr_ = np.zeros(counts.size + 1, dtype=np.int64)
     np.cumsum(counts, out=ptr_[1:])
     return ptr_, order
+
+
+def visit_order(ptr_, idx):
+    """Visiting order of the owner-computes node passes (K2's node sum, K5): nodes by
+    descending first incident row (their lowest cell / patch), ties by descending id.
+    Each node then meets the element vectors / Y rows of its own cells together (the
+    vertex nodes, numbered first, no longer sweep all of them at kernel start), and the
+    rows the producing kernel wrote last, still in L2, are read first.  Any order gives
+    the same bits.  DNNMG_NODE_ORDER=ascending|forward selects ids / ascending first row
+    (diagnostic A/B)."""
+    mode = os.environ.get("DNNMG_NODE_ORDER", "")
+    if mode == "ascending":
+        return None
+    ptr_ = np.asarray(ptr_, dtype=np.int64)
+    n = ptr_.size - 1
+    idx = np.asarray(idx)
+    first = np.full(n, -1, dtype=np.int64)
+    has = ptr_[1:] > ptr_[:-1]
+    first[has] = idx[ptr_[:-1][has]]
+    order = np.lexsort((np.arange(n), first))
+    return order if mode == "forward" else order[::-1].copy()
 
 
 TILE_ROWS = 128  # patches per tensor-core MLP tile (kTcM in csrc/mlp_tc.cu)
@@ -221,12 +246,13 @@ class DeviceLevel:
         p, idx = node_csr(space.cell_nodes)
         self.csr_ptr = upload(p, np.int32)
         self.csr_idx = upload(idx, np.int32)
+        self.order = upload_opt(visit_order(p, idx))
         self.elem = None
 
     def struct(self, dof_mask=None, geometry=False):
         return _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
                           ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask),
-                          ptr(self.geometry()) if geometry else None)
+                          ptr(self.geometry()) if geometry else None, ptr(self.order))
 
     def geometry(self):
         """Per-mesh cache of J^-1 and w at every (cell, Gauss point) (2,560 B per cell),
@@ -265,6 +291,7 @@ class DevicePatchSet:
             raise RuntimeError("patch union does not cover the fine level")
         self.csr_ptr = upload(p, np.int32)
         self.csr_idx = upload(idx, np.int32)
+        self.order = upload_opt(visit_order(p, idx))
         tt = tile_tables(ps.node_table)
         self.tile_cap = 0
         self.tile_nodes = self.tile_count = self.tile_slot = None
@@ -277,7 +304,8 @@ class DevicePatchSet:
         self.struct = _lib.PatchSet(self.n_patches, self.npp, self.n_geo, self.n_nodes,
                                     ptr(self.node_table), ptr(self.geom), ptr(self.csr_ptr),
                                     ptr(self.csr_idx), self.tile_cap, ptr(self.tile_nodes),
-                                    ptr(self.tile_count), ptr(self.tile_slot))
+                                    ptr(self.tile_count), ptr(self.tile_slot),
+                                    ptr(self.order))
 
     @staticmethod
     def get(ps):

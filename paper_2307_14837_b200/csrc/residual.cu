@@ -25,6 +25,7 @@
 // so results are deterministic and independent of the launch configuration;
 // no float atomics are used.
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace dnnmg {
 
@@ -69,9 +70,13 @@ constexpr int kSYF = 148;              // sy field stride (= 20 mod 32: the (f, 
                                        // forward x-y stage store to distinct banks)
 constexpr int oCF = oSY + kNF * kSYF;  // cf[25][kCFS]: A[4], B[4][3], P[3][3]
 constexpr int kNCF = 25;
-// coefficient array stride: 64 Gauss points + 4, so that array a starts in bank 4a (mod 32)
-// and the eight (comp, part) lines of the backward stage read eight different banks
-constexpr int kCFS = 68;
+// coefficient array stride and position of Gauss point q in an array: the second half of
+// the points (qz >= 2) is shifted by 4 floats, so that the four qz lanes of one (comp, part)
+// line of the backward stage read float4s from four different bank groups, and array a starts
+// in bank 8a (mod 32), so that the two lines of a quarter-warp do not collide either (every
+// backward LDS.128 is 4 wavefronts; with qz-stride 16 and no shift it was 8)
+constexpr int kCFS = 72;
+__host__ __device__ constexpr int cfq(int q) { return q + ((q >> 5) << 2); }
 constexpr int oTZ = oSY;              // tz[4][2][27] aliases sy (dead after the pointwise phase)
 constexpr int kCellFloats = (oCF + kNCF * kCFS + 3) / 4 * 4;
 static_assert(oTZ + 4 * 2 * 27 <= oCF, "tz must fit in sy");
@@ -86,7 +91,8 @@ struct KLay {
   static constexpr int FO = NF - 4;                    // index of p among them
   static constexpr int oCF = oSY + NF * kSYF;
   static constexpr int oGQ = oCF + kNCF * kCFS;        // cached [J^-1 (9) | w][64]
-  static constexpr int kFloats = (oGQ + (CACHED ? 10 * 64 : 0) + 3) / 4 * 4;
+  static constexpr int oBar = oGQ + 10 * 64;           // cached: the staging mbarrier (8 B)
+  static constexpr int kFloats = (oGQ + (CACHED ? 10 * 64 + 4 : 0) + 3) / 4 * 4;
   static_assert(oTZ + 4 * 2 * 27 <= oCF && oCF % 4 == 0 && oGQ % 4 == 0, "layout");
 };
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
@@ -158,15 +164,15 @@ __device__ __forceinline__ void load_raw(const ResidualArgs& A, int c, int node,
 }
 
 // cp.async of cell c's cached geometry block (2560 B = 160 x 16 B, 5 per lane)
-__device__ __forceinline__ void stage_geo(const ResidualArgs& A, int c, int t, float* dst) {
-  const float4* src = reinterpret_cast<const float4*>(A.geo_q + (int64_t)c * 640);
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + 4 * (t + 32 * k)));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + t + 32 * k)
-                 : "memory");
+// the cell's contiguous 2,560-byte geometry block, one bulk (TMA) copy issued by lane 0 and
+// completed on the warp's mbarrier (per-lane cp.async cost 11 shared wavefronts per 512 B)
+__device__ __forceinline__ void stage_geo(const ResidualArgs& A, int c, int t, float* dst,
+                                          uint32_t bar) {
+  if (t == 0) {
+    fence_async_smem();  // the previous cell's generic reads of dst precede the async write
+    mbar_expect_tx(bar, 640 * 4);
+    bulk_g2s(smem_u32(dst), A.geo_q + (int64_t)c * 640, 640 * 4, bar);
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // Q1 (pi) fields p, vx, vy, vz at the two Gauss points (qx, qy, qz) and (qx, qy, qz + 2) of a
@@ -272,7 +278,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #pragma unroll
   for (int i = 0; i < 3; ++i)
     conv[i] = A.convection ? v[0] * gv[i][0] + v[1] * gv[i][1] + v[2] * gv[i][2] : 0.f;
-#define CFW(arr) CF[(arr) * kCFS + q]
+#define CFW(arr) CF[(arr) * kCFS + cfq(q)]
   const float ik = A.ik;
   if constexpr (MODE == MODE_OPERATOR) {
     const float p = F[FO][0];
@@ -344,11 +350,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
   int c = blockIdx.x * kWarpsPerBlock + wib;
   NodeRaw raw;
   int idx_next = 0;  // node index of cell c + stride (lane t < 27)
+  const uint32_t bar = smem_u32(S + L::oBar);
+  uint32_t phase = 0;
+  if constexpr (CACHED) {
+    if (t == 0) {
+      mbar_init(bar, 1);
+      fence_async_smem();
+    }
+    __syncwarp();
+  }
   if (c < A.n_cells) {
     const int node = t < 27 ? __ldg(A.cell_nodes + (int64_t)c * 27 + t) : 0;
     load_raw<CACHED>(A, c, node, t, raw);
     if (c + stride < A.n_cells && t < 27) idx_next = __ldg(A.cell_nodes + (int64_t)(c + stride) * 27 + t);
-    if constexpr (CACHED) stage_geo(A, c, t, S + L::oGQ);
+    if constexpr (CACHED) stage_geo(A, c, t, S + L::oGQ, bar);
   }
 
   for (; c < A.n_cells; c += stride) {
@@ -453,8 +468,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         }
       }
       if constexpr (CACHED) {  // this cell's geometry block (staged one cell ahead)
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
+        mbar_wait(bar, phase);
+        phase ^= 1;
       }
       float PQa[4][4], PQb[4][4];
       if constexpr (MODE == MODE_OPERATOR)
@@ -466,7 +481,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     }
     __syncwarp();
     if constexpr (CACHED) {
-      if (c + stride < A.n_cells) stage_geo(A, c + stride, t, S + L::oGQ);
+      if (c + stride < A.n_cells) stage_geo(A, c + stride, t, S + L::oGQ, bar);
     }
     // ---------------- backward x, y, z in registers: lane (cp, qz), cp = (comp, part) ----------------
     // tz[cp][iz][iy][ix] = sum_q test(q; ix, iy, iz) . coefficients(cp, q).  Each of the 32
@@ -481,10 +496,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       const int comp = cp >> 1, part = cp & 1;
       // part 0: A_c, B_c0..2; part 1: comp 0 -> B_00..02, comps 1..3 -> P_(c-1)0..2; part 1 has
       // no value test and enters with a minus sign
-      const float* c0 = S + L::oCF + (CA + comp) * kCFS + 16 * qz;
+      const float* c0 = S + L::oCF + (CA + comp) * kCFS + cfq(16 * qz);
       const float* c1 = S + L::oCF +
                         (part == 0 || comp == 0 ? CB + 3 * comp : CP + 3 * (comp - 1)) * kCFS +
-                        16 * qz;
+                        cfq(16 * qz);
       const float* c2 = c1 + kCFS;
       const float* c3 = c1 + 2 * kCFS;
       float ua[3][3], ub[3][3];  // [iy][ix]

@@ -69,21 +69,51 @@ __global__ void __launch_bounds__(256) extend_kernel(int n_nodes, const int32_t*
 
 // d = mu * sum over incident (patch, slot) of Y[patch][3*slot .. 3*slot+2]; pressure 0;
 // d[mask] = 0; x_corr = x~ + scale*d
+// Up to kBatch incident entries of a node are loaded before any is summed (all Y loads of a
+// node in flight at once); the sum stays in ascending entry order.  NPP > 0 makes the
+// (patch, slot) split a constant division.
+constexpr int kBatch = 8;
+
+template <int NPP>
 __global__ void __launch_bounds__(256) scatter_update_kernel(
-    int n_nodes, int npp, int n_out, const int32_t* __restrict__ ptr,
+    int n_nodes, int npp_rt, const int32_t* __restrict__ ptr,
     const int32_t* __restrict__ idx, const float* __restrict__ Y, const uint8_t* __restrict__ mask,
     const float4* __restrict__ xt, float scale, float4* __restrict__ d, float4* __restrict__ xc,
     const int32_t* __restrict__ order) {
+  const int npp = NPP > 0 ? NPP : npp_rt;
+  const int n_out = 3 * npp;
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < n_nodes;
        pos += gridDim.x * blockDim.x) {
     const int n = order ? __ldg(order + pos) : pos;
     const int s = __ldg(ptr + n), e = __ldg(ptr + n + 1);
+    int ent[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) ent[k] = s + k < e ? __ldg(idx + s + k) : -1;
+    float y0[kBatch], y1[kBatch], y2[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      y0[k] = y1[k] = y2[k] = 0.f;
+      if (ent[k] >= 0) {
+        const int p = ent[k] / npp;
+        const float* y = Y + (int64_t)p * n_out + 3 * (ent[k] - p * npp);
+        y0[k] = __ldg(y);
+        y1[k] = __ldg(y + 1);
+        y2[k] = __ldg(y + 2);
+      }
+    }
     float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-    for (int i = s; i < e; ++i) {
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      if (ent[k] >= 0) {
+        a0 += y0[k];
+        a1 += y1[k];
+        a2 += y2[k];
+      }
+    }
+    for (int i = s + kBatch; i < e; ++i) {
       const int ps = __ldg(idx + i);
       const int p = ps / npp;
-      const int slot = ps - p * npp;
-      const float* y = Y + (int64_t)p * n_out + 3 * slot;
+      const float* y = Y + (int64_t)p * n_out + 3 * (ps - p * npp);
       a0 += __ldg(y);
       a1 += __ldg(y + 1);
       a2 += __ldg(y + 2);
@@ -161,10 +191,13 @@ int32_t launch_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const 
   DNNMG_REQUIRE(Y && (d || xc), DNNMG_ERR_ARG, "scatter_update: null argument");
   DNNMG_REQUIRE(!xc || xt, DNNMG_ERR_ARG, "scatter_update: x_corr requested without x_tilde");
   if (ps->n_nodes == 0) return DNNMG_OK;
-  scatter_update_kernel<<<grid_for(ps->n_nodes, 256), 256, 0, s>>>(
-      ps->n_nodes, ps->nodes_per_patch, 3 * ps->nodes_per_patch, ps->node_patch_ptr,
-      ps->node_patch_idx, Y, mask, reinterpret_cast<const float4*>(xt), scale,
-      reinterpret_cast<float4*>(d), reinterpret_cast<float4*>(xc), ps->node_order);
+  auto kern = ps->nodes_per_patch == 27    ? scatter_update_kernel<27>
+              : ps->nodes_per_patch == 125 ? scatter_update_kernel<125>
+                                           : scatter_update_kernel<0>;
+  kern<<<grid_for(ps->n_nodes, 256), 256, 0, s>>>(
+      ps->n_nodes, ps->nodes_per_patch, ps->node_patch_ptr, ps->node_patch_idx, Y, mask,
+      reinterpret_cast<const float4*>(xt), scale, reinterpret_cast<float4*>(d),
+      reinterpret_cast<float4*>(xc), ps->node_order);
   DNNMG_CHECK_LAUNCH("scatter_update_kernel");
   return DNNMG_OK;
 }

@@ -612,12 +612,30 @@ __global__ void __launch_bounds__(256) node_sum_kernel(
     const int n = order ? __ldg(order + pos) : pos;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const int s = __ldg(ptr + n), e = __ldg(ptr + n + 1);
-    for (int i = s; i < e; ++i) {
-      const float4 v = __ldg(elem + __ldg(idx + i));
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
+    // the first 8 incident element vectors are loaded before any is summed (all in flight at
+    // once); the sum stays in ascending cell order
+    int ent[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ent[k] = s + k < e ? __ldg(idx + s + k) : -1;
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      v[k] = ent[k] >= 0 ? __ldg(elem + ent[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (ent[k] >= 0) {
+        acc.x += v[k].x;
+        acc.y += v[k].y;
+        acc.z += v[k].z;
+        acc.w += v[k].w;
+      }
+    }
+    for (int i = s + 8; i < e; ++i) {
+      const float4 w = __ldg(elem + __ldg(idx + i));
+      acc.x += w.x;
+      acc.y += w.y;
+      acc.z += w.z;
+      acc.w += w.w;
     }
     float4 r;
     if (b) {

@@ -86,6 +86,9 @@ __global__ void __launch_bounds__(256) scatter_update_kernel(
        pos += gridDim.x * blockDim.x) {
     const int n = order ? __ldg(order + pos) : pos;
     const int s = __ldg(ptr + n), e = __ldg(ptr + n + 1);
+    // the node's own loads first: in flight with the entry loads
+    const float4 x = xc ? __ldg(xt + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint8_t m = mask ? __ldg(mask + n) : 0;
     int ent[kBatch];
 #pragma unroll
     for (int k = 0; k < kBatch; ++k) ent[k] = s + k < e ? __ldg(idx + s + k) : -1;
@@ -120,15 +123,11 @@ __global__ void __launch_bounds__(256) scatter_update_kernel(
     }
     const float mu = e > s ? 1.0f / (float)(e - s) : 0.f;
     float4 dv = make_float4(0.f, mu * a0, mu * a1, mu * a2);
-    if (mask) {
-      const uint8_t m = mask[n];
-      if (m & 2) dv.y = 0.f;
-      if (m & 4) dv.z = 0.f;
-      if (m & 8) dv.w = 0.f;
-    }
+    if (m & 2) dv.y = 0.f;
+    if (m & 4) dv.z = 0.f;
+    if (m & 8) dv.w = 0.f;
     if (d) d[n] = dv;
     if (xc) {
-      const float4 x = __ldg(xt + n);
       xc[n] = make_float4(x.x, fmaf(scale, dv.y, x.y), fmaf(scale, dv.z, x.z), fmaf(scale, dv.w, x.w));
     }
   }

@@ -62,7 +62,9 @@ enum {
   DNNMG_PREC_BF16 = 1,   /* tcgen05 kind::f16, bf16 operands, fp32 accumulate in TMEM */
   DNNMG_PREC_TF32X3 = 2, /* tcgen05 kind::tf32, 3-pass split (hi*hi + hi*lo + lo*hi), fp32 accuracy */
   DNNMG_PREC_F16X3 = 3,  /* tcgen05 kind::f16, fp16 3-pass split of power-of-two scaled weights,
-                            fp32 accuracy at twice the tf32 rate (|activations| < 65504) */
+                            fp32 accuracy at twice the tf32 rate; needs |activations| < 65504,
+                            so only tanh models are accepted (relu: DNNMG_ERR_UNSUPPORTED,
+                            use TF32X3) */
   DNNMG_PREC_FP8 = 4     /* tcgen05 kind::f8f6f4, e4m3 operands (weights scaled by a power of
                             two per layer), fp32 accumulate; report-only accuracy (~1e-1) */
 };
@@ -242,7 +244,7 @@ int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, 
  * of dnnmg_mlp_workspace_bytes(m, n_rows) bytes (0: none needed). */
 int32_t dnnmg_mlp_workspace_bytes(const dnnmg_mlp_t* m, int64_t n_rows, int64_t* bytes);
 int32_t dnnmg_mlp_forward_ws(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
-                             void* workspace, dnnmg_stream_t stream);
+                             void* workspace, int64_t workspace_bytes, dnnmg_stream_t stream);
 
 /* K3 fused into K4 (tensor-core modes, 8*npp + n_geo <= 256): the network input rows
  * [x~ | r | geometry] are gathered straight into the layer-0 operand; X is never stored. */
@@ -253,7 +255,7 @@ int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* 
  * dnnmg_mlp_forward_ws). */
 int32_t dnnmg_mlp_forward_patches_ws(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps,
                                      const float* x, const float* r, float* Y, void* workspace,
-                                     dnnmg_stream_t stream);
+                                     int64_t workspace_bytes, dnnmg_stream_t stream);
 
 /* Which layer-0 source dnnmg_mlp_forward_patches uses for (m, ps): 1 = direct gather of
  * every (patch, slot) at the tile boundary, 2 = staged gather of each tile's distinct nodes
@@ -328,6 +330,7 @@ typedef struct {
   float* d;         /* [4*n_fine] */
   float* x_mid;     /* [4*n_mid] intermediate level for J = 2, else NULL */
   void* mlp_ws;     /* dnnmg_mlp_workspace_bytes(m, n_patches) bytes, or NULL when 0 */
+  int64_t mlp_ws_bytes; /* size of mlp_ws: a smaller buffer than the rows need is an error */
 } dnnmg_step_buffers_t;
 
 /* prolongations: J entries (levels L..L+J-1); bc: Dirichlet data of the fine level. */

@@ -75,7 +75,7 @@ class Vanka(ctypes.Structure):
 
 class StepBuffers(ctypes.Structure):
     _fields_ = [("x_tilde", c_vp), ("r", c_vp), ("elem", c_vp), ("X", c_vp), ("Y", c_vp),
-                ("d", c_vp), ("x_mid", c_vp), ("mlp_ws", c_vp)]
+                ("d", c_vp), ("x_mid", c_vp), ("mlp_ws", c_vp), ("mlp_ws_bytes", c_i64)]
 
 
 EXPORTS = {
@@ -99,9 +99,9 @@ EXPORTS = {
     "dnnmg_mlp_pack": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_vp]),
     "dnnmg_mlp_forward": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_i64, c_vp, c_vp]),
     "dnnmg_mlp_workspace_bytes": (c_i32, [ctypes.POINTER(Mlp), c_i64, ctypes.POINTER(c_i64)]),
-    "dnnmg_mlp_forward_ws": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "dnnmg_mlp_forward_ws": (c_i32, [ctypes.POINTER(Mlp), c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "dnnmg_mlp_forward_patches_ws": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet), c_vp,
-                                             c_vp, c_vp, c_vp, c_vp]),
+                                             c_vp, c_vp, c_vp, c_i64, c_vp]),
     "dnnmg_mlp_forward_patches": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet), c_vp, c_vp,
                                           c_vp, c_vp]),
     "dnnmg_mlp_gather_mode": (c_i32, [ctypes.POINTER(Mlp), ctypes.POINTER(PatchSet)]),

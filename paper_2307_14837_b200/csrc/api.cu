@@ -41,9 +41,10 @@ int32_t mlp_layered_supported(const dnnmg_mlp_t*);
 int32_t mlp_layered_packed_bytes(const dnnmg_mlp_t*, int64_t*);
 int32_t mlp_layered_workspace_bytes(const dnnmg_mlp_t*, int64_t, int64_t*);
 int32_t launch_mlp_layered_pack(const dnnmg_mlp_t*, void*, cudaStream_t);
-int32_t launch_mlp_layered(const dnnmg_mlp_t*, const float*, int64_t, float*, void*, cudaStream_t);
+int32_t launch_mlp_layered(const dnnmg_mlp_t*, const float*, int64_t, float*, void*, int64_t,
+                           cudaStream_t);
 int32_t launch_mlp_layered_patches(const dnnmg_mlp_t*, const dnnmg_patchset_t*, const float*,
-                                   const float*, float*, void*, cudaStream_t);
+                                   const float*, float*, void*, int64_t, cudaStream_t);
 
 static int32_t check_mlp(const dnnmg_mlp_t* m) {
   DNNMG_REQUIRE(m, DNNMG_ERR_ARG, "mlp: null model");
@@ -55,6 +56,12 @@ static int32_t check_mlp(const dnnmg_mlp_t* m) {
     DNNMG_REQUIRE(m->W[i], DNNMG_ERR_ARG, "mlp: W[%d] is NULL", i);
   DNNMG_REQUIRE(m->bn_scale && m->bn_shift && m->in_mean && m->in_std, DNNMG_ERR_ARG,
                 "mlp: missing normalisation vectors");
+  // f16x3 splits the hidden activations into fp16 hi/lo parts: only a bounded activation
+  // (tanh: |h| <= depth with the skips) keeps them inside the fp16 range; relu hidden
+  // states are unbounded (net.py:57, the reference's default) and need tf32x3
+  DNNMG_REQUIRE(m->precision != DNNMG_PREC_F16X3 || m->activation == DNNMG_ACT_TANH,
+                DNNMG_ERR_UNSUPPORTED,
+                "mlp: f16x3 needs a bounded activation (tanh); use tf32x3 for relu models");
   return DNNMG_OK;
 }
 
@@ -168,7 +175,7 @@ int32_t dnnmg_mlp_workspace_bytes(const dnnmg_mlp_t* m, int64_t n_rows, int64_t*
 }
 
 int32_t dnnmg_mlp_forward_ws(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
-                             void* workspace, dnnmg_stream_t s) {
+                             void* workspace, int64_t ws_bytes, dnnmg_stream_t s) {
   int32_t st = check_mlp(m);
   if (st) return st;
   DNNMG_REQUIRE(n_rows >= 0, DNNMG_ERR_ARG, "mlp_forward: negative row count");
@@ -177,7 +184,7 @@ int32_t dnnmg_mlp_forward_ws(const dnnmg_mlp_t* m, const float* X, int64_t n_row
   if (m->precision == DNNMG_PREC_FP32) return launch_mlp_simt(m, X, n_rows, Y, as_stream(s));
   DNNMG_REQUIRE(m->packed, DNNMG_ERR_ARG, "mlp_forward: tensor-core mode needs packed weights");
   if (mlp_tc_supported(m)) return launch_mlp_tc(m, X, n_rows, Y, as_stream(s));
-  return launch_mlp_layered(m, X, n_rows, Y, workspace, as_stream(s));
+  return launch_mlp_layered(m, X, n_rows, Y, workspace, ws_bytes, as_stream(s));
 }
 
 int32_t dnnmg_mlp_forward(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y,
@@ -200,7 +207,7 @@ static bool layered_gather(const dnnmg_mlp_t* m);
 
 int32_t dnnmg_mlp_forward_patches_ws(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps,
                                      const float* x, const float* r, float* Y, void* workspace,
-                                     dnnmg_stream_t s) {
+                                     int64_t ws_bytes, dnnmg_stream_t s) {
   int32_t st = check_mlp(m);
   if (st) return st;
   DNNMG_REQUIRE(ps && ps->node_table && ps->geom && x && r && Y, DNNMG_ERR_ARG,
@@ -212,7 +219,7 @@ int32_t dnnmg_mlp_forward_patches_ws(const dnnmg_mlp_t* m, const dnnmg_patchset_
                 "model architecture (%d outputs) does not match the patch layout (%d)", m->n_out,
                 3 * ps->nodes_per_patch);
   if (ps->n_patches == 0) return DNNMG_OK;
-  return launch_mlp_layered_patches(m, ps, x, r, Y, workspace, as_stream(s));
+  return launch_mlp_layered_patches(m, ps, x, r, Y, workspace, ws_bytes, as_stream(s));
 }
 
 int32_t dnnmg_mlp_forward_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
@@ -290,10 +297,12 @@ int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_d
   if (fused_gather(m, ps)) {
     rc = launch_mlp_tc_gather(m, ps, buf->x_tilde, buf->r, buf->Y, st);
   } else if (layered_gather(m)) {
-    rc = launch_mlp_layered_patches(m, ps, buf->x_tilde, buf->r, buf->Y, buf->mlp_ws, st);
+    rc = launch_mlp_layered_patches(m, ps, buf->x_tilde, buf->r, buf->Y, buf->mlp_ws,
+                                    buf->mlp_ws_bytes, st);
   } else {
     rc = launch_gather(ps, buf->x_tilde, buf->r, buf->X, st);
-    if (!rc) rc = dnnmg_mlp_forward_ws(m, buf->X, ps->n_patches, buf->Y, buf->mlp_ws, s);
+    if (!rc) rc = dnnmg_mlp_forward_ws(m, buf->X, ps->n_patches, buf->Y, buf->mlp_ws,
+                                       buf->mlp_ws_bytes, s);
   }
   if (rc) return rc;
   return launch_scatter_update(ps, buf->Y, fine->dof_mask, buf->x_tilde, scale, buf->d, x_corr, st);

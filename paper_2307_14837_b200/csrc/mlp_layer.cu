@@ -508,12 +508,20 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, const PatchRow
 }
 
 int32_t launch_mlp_layered_rows(const dnnmg_mlp_t* m, const float* X, const PatchRows* P,
-                                int64_t n_rows, float* Y, void* ws, cudaStream_t s) {
+                                int64_t n_rows, float* Y, void* ws, int64_t ws_bytes,
+                                cudaStream_t s) {
   DNNMG_REQUIRE(mlp_layered_supported(m) && m->packed, DNNMG_ERR_UNSUPPORTED,
                 "mlp: layered tensor-core mode needs packed weights and n_hidden %% 32 == 0");
+  if (n_rows == 0) return DNNMG_OK;
   DNNMG_REQUIRE(ws, DNNMG_ERR_ARG, "mlp: the layered tensor-core MLP needs a workspace "
                 "(dnnmg_mlp_workspace_bytes)");
-  if (n_rows == 0) return DNNMG_OK;
+  // the workspace layout depends on n_rows (up to the pass size): a buffer sized for fewer
+  // rows would be overrun
+  const int64_t need = layered_geom(m, n_rows).ws;
+  DNNMG_REQUIRE(ws_bytes >= need, DNNMG_ERR_ARG,
+                "mlp: workspace of %lld bytes is smaller than the %lld bytes %lld rows need "
+                "(dnnmg_mlp_workspace_bytes)", (long long)ws_bytes, (long long)need,
+                (long long)n_rows);
   if (m->precision == DNNMG_PREC_FP8) return layered_mode<DNNMG_PREC_FP8>(m, X, P, n_rows, Y, ws, s);
   if (m->precision == DNNMG_PREC_BF16) return layered_mode<DNNMG_PREC_BF16>(m, X, P, n_rows, Y, ws, s);
   if (m->precision == DNNMG_PREC_F16X3) return layered_mode<DNNMG_PREC_F16X3>(m, X, P, n_rows, Y, ws, s);
@@ -521,19 +529,20 @@ int32_t launch_mlp_layered_rows(const dnnmg_mlp_t* m, const float* X, const Patc
 }
 
 int32_t launch_mlp_layered(const dnnmg_mlp_t* m, const float* X, int64_t n_rows, float* Y, void* ws,
-                           cudaStream_t s) {
-  return launch_mlp_layered_rows(m, X, nullptr, n_rows, Y, ws, s);
+                           int64_t ws_bytes, cudaStream_t s) {
+  return launch_mlp_layered_rows(m, X, nullptr, n_rows, Y, ws, ws_bytes, s);
 }
 
 // K3 fused into the layered MLP: the layer-0 operand is gathered straight from x~, r and the
 // patch geometry (no X in HBM)
 int32_t launch_mlp_layered_patches(const dnnmg_mlp_t* m, const dnnmg_patchset_t* ps, const float* x,
-                                   const float* r, float* Y, void* ws, cudaStream_t s) {
+                                   const float* r, float* Y, void* ws, int64_t ws_bytes,
+                                   cudaStream_t s) {
   DNNMG_REQUIRE(8 * ps->nodes_per_patch + ps->n_geo == m->n_in, DNNMG_ERR_ARCH,
                 "model architecture (%d inputs) does not match the patch layout (%d)", m->n_in,
                 8 * ps->nodes_per_patch + ps->n_geo);
   PatchRows P{ps->node_table, x, r, ps->geom, ps->nodes_per_patch, ps->n_geo};
-  return launch_mlp_layered_rows(m, nullptr, &P, ps->n_patches, Y, ws, s);
+  return launch_mlp_layered_rows(m, nullptr, &P, ps->n_patches, Y, ws, ws_bytes, s);
 }
 
 }  // namespace dnnmg

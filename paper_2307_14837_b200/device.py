@@ -36,6 +36,10 @@ def ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def nbytes(t):
+    return 0 if t is None else int(t.numel() * t.element_size())
+
+
 def f32(x):
     """numpy / torch -> contiguous float32 CUDA tensor."""
     dev = device()
@@ -181,7 +185,9 @@ class DeviceProlong:
 
 
 class DeviceRestrict:
-    """K6 tables for level+1 -> level: P^T as a coarse-node CSR (rows ascending fine node)."""
+    """K6 tables for level+1 -> level: P^T as a coarse-node CSR (rows ascending fine node).
+    The cell scratch is shared per (hierarchy, level): restrictions of one level are
+    ordered on the caller's current stream."""
 
     def __init__(self, hierarchy, level):
         from .space import prolongation_matrix
@@ -264,6 +270,9 @@ class DeviceLevel:
         return self.geo_q
 
     def scratch(self):
+        """Element-vector scratch shared by the reference-API calls on this level
+        (assembly.Assembler), which are stream-ordered on the caller's current stream;
+        CorrectionStep owns its own."""
         if self.elem is None:
             self.elem = torch.empty(self.n_cells * 27 * 4, dtype=torch.float32, device=device())
         return self.elem
@@ -325,8 +334,16 @@ class DeviceModel:
     """Eval-mode MlpModel on the device (net.py:54-159), BN folded to scale/shift."""
 
     def __init__(self, model, precision="fp32"):
+        from .net import effective_precision
         arch = model.arch
         self.arch = arch
+        # f16x3 needs bounded activations: relu models fall back to tf32x3 (net.py docstring)
+        self.requested_precision = precision
+        precision = effective_precision(model.activation, precision)
+        if precision != self.requested_precision:
+            import warnings
+            warnings.warn(f"precision {self.requested_precision} needs a bounded activation; "
+                          f"the {model.activation} model runs in {precision}", stacklevel=2)
         self.precision = precision
         self.W = [f32(np.asarray(w, dtype=np.float64)) for w in model.W]
         scale, shift = [], []
@@ -368,8 +385,9 @@ class DeviceModel:
         return self._ws
 
     def forward(self, X, n_rows, Y):
+        ws = self.workspace(n_rows)
         _lib.call("dnnmg_mlp_forward_ws", ctypes.byref(self.struct), ptr(X), int(n_rows), ptr(Y),
-                  ptr(self.workspace(n_rows)), stream_handle())
+                  ptr(ws), nbytes(ws), stream_handle())
 
 
 def dirichlet_codes(space, t, bcs):

@@ -413,5 +413,8 @@ def resume_loop(problem, ckpt_path, model=None, J=None, precision="fp32", **kw):
         xf = loop.fine.embed_into(dv.f32(x.values), torch.empty_like(loop.fine.x_tilde))
         st.x_fine = spmod.StateVector(fl, xf, t)
         st.b_next_fine = loop.fine.rhs_next(xf)
+        # the coarse RHS of the first resumed solve is the restriction of the rebuilt fine
+        # RHS, not the pure-MG checkpoint's own b_next (driver.py:476-478)
+        st.b_next = loop._restrict(st.b_next_fine)
     loop.state = st
     return loop

@@ -102,6 +102,18 @@ def resolve_precision(precision=None):
     return p
 
 
+def effective_precision(activation, precision):
+    """The tensor-core mode a model actually runs in.  f16x3 splits the hidden activations
+    into fp16 hi/lo parts, which is exact to fp32 accuracy only while |h| < 65504: tanh
+    bounds the hidden states (|h| <= depth with the skips), relu -- the reference's default
+    activation (net.py:57, config.py:69-71) -- does not.  Relu models therefore run in
+    tf32x3 (same fp32 accuracy, fp32 exponent range, half the f16x3 rate); the library
+    rejects f16x3 + relu outright (DNNMG_ERR_UNSUPPORTED)."""
+    if precision == "f16x3" and activation != "tanh":
+        return "tf32x3"
+    return precision
+
+
 def forward(model, X, precision=None):
     """Eval-mode network output for a batch on the GPU (net.py:162-164)."""
     import torch

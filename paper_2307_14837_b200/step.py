@@ -53,6 +53,7 @@ class CorrectionStep:
         if model is not None:
             check_model(model, self.patchset)
             self.model = dv.DeviceModel(model, precision)
+            precision = self.precision = self.model.precision   # relu: f16x3 -> tf32x3
             a = model.arch
             # K3 fused into K4 when the tensor-core MLP can stage the rows itself
             self.fused_gather = (precision not in ("fp32", "fp8") and a.n_hidden == 256 and a.n_in <= 256
@@ -65,7 +66,9 @@ class CorrectionStep:
         self.r = torch.empty(4 * nf, dtype=f, device=dev)
         self.d = torch.empty(4 * nf, dtype=f, device=dev)
         self.x_corr = torch.empty(4 * nf, dtype=f, device=dev)
-        self.elem = self.level.scratch()
+        # element-vector scratch owned by this step (not the level's shared one), so steps on
+        # the same level can run on different streams
+        self.elem = torch.empty(self.level.n_cells * 27 * 4, dtype=f, device=dev)
         # layered tensor-core MLP (widths the fused kernel does not hold): the gather is fused
         # into its layer-0 operand; width 128 runs the fused kernel on stored X rows
         self.layered = (model is not None and precision != "fp32"
@@ -80,7 +83,7 @@ class CorrectionStep:
         self.mlp_ws = self.model.workspace(self.ps.n_patches) if self.layered else None
         self.buf = _lib.StepBuffers(dv.ptr(self.x_tilde), dv.ptr(self.r), dv.ptr(self.elem),
                                     dv.ptr(self.X), dv.ptr(self.Y), dv.ptr(self.d),
-                                    dv.ptr(self.x_mid), dv.ptr(self.mlp_ws))
+                                    dv.ptr(self.x_mid), dv.ptr(self.mlp_ws), dv.nbytes(self.mlp_ws))
         self._t = None
         self.set_time(t)
         self.graph = None
@@ -128,7 +131,8 @@ class CorrectionStep:
         t.x_mid = None if self.x_mid is None else torch.empty_like(self.x_mid)
         t.mlp_ws = None if self.mlp_ws is None else torch.empty_like(self.mlp_ws)
         t.buf = _lib.StepBuffers(dv.ptr(t.x_tilde), dv.ptr(t.r), dv.ptr(t.elem), dv.ptr(t.X),
-                                 dv.ptr(t.Y), dv.ptr(t.d), dv.ptr(t.x_mid), dv.ptr(t.mlp_ws))
+                                 dv.ptr(t.Y), dv.ptr(t.d), dv.ptr(t.x_mid), dv.ptr(t.mlp_ws),
+                                 dv.nbytes(t.mlp_ws))
         if self.bc.vals is not None:
             # time-dependent Dirichlet data are updated in place by set_time: own a copy
             bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
@@ -193,12 +197,12 @@ class CorrectionStep:
         if self.fused_gather or self.layered:
             _lib.call("dnnmg_mlp_forward_patches_ws", ctypes.byref(self.model.struct),
                       ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde), dv.ptr(self.r),
-                      dv.ptr(self.Y), dv.ptr(self.mlp_ws), s)
+                      dv.ptr(self.Y), dv.ptr(self.mlp_ws), dv.nbytes(self.mlp_ws), s)
             return
         _lib.call("dnnmg_gather", ctypes.byref(self.ps.struct), dv.ptr(self.x_tilde),
                   dv.ptr(self.r), dv.ptr(self.X), s)
         _lib.call("dnnmg_mlp_forward_ws", ctypes.byref(self.model.struct), dv.ptr(self.X),
-                  self.ps.n_patches, dv.ptr(self.Y), dv.ptr(self.mlp_ws), s)
+                  self.ps.n_patches, dv.ptr(self.Y), dv.ptr(self.mlp_ws), dv.nbytes(self.mlp_ws), s)
 
     def stage_names(self):
         """Labels of the stages run_staged() brackets with events."""

@@ -108,6 +108,7 @@ def checkpoints(pr, model):
                                   J=c["J"])
         loop.correction_scale, loop.correction_start = c["scale"], c["start"]
         out[f"{name}_b_next_fine_0"] = loop.state.b_next_fine.copy()
+        out[f"{name}_b_next_0"] = loop.state.b_next.copy()   # RHS of the first resumed solve
         for n in (1, 2):
             st = loop.step()
             out[f"{name}_t_{n}"] = st.t

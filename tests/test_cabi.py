@@ -46,3 +46,43 @@ def test_library_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_f16x3_rejects_unbounded_activation():
+    """f16x3 splits activations into fp16 parts: the C ABI refuses it for relu models
+    (host-side check, no GPU needed), and the Python layer runs them in tf32x3."""
+    import ctypes
+    from paper_2307_14837_b200.net import effective_precision
+    lib = _lib.load()
+    dummy = ctypes.c_void_p(16)          # never dereferenced by the host-side checks
+    W = (ctypes.c_void_p * _lib.MAX_LAYERS)(*([16] * 4 + [0] * (_lib.MAX_LAYERS - 4)))
+    for act, want in ((_lib.ACT_RELU, 3), (_lib.ACT_TANH, 0)):
+        m = _lib.Mlp(240, 256, 3, 81, act, _lib.PRECISIONS["f16x3"], W, dummy, dummy, dummy,
+                     dummy, None)
+        nbytes = ctypes.c_int64(-1)
+        assert lib.dnnmg_mlp_packed_bytes(ctypes.byref(m), ctypes.byref(nbytes)) == want
+        if want:
+            assert b"f16x3" in lib.dnnmg_last_error()
+        else:
+            assert nbytes.value > 0
+    assert effective_precision("relu", "f16x3") == "tf32x3"
+    assert effective_precision("tanh", "f16x3") == "f16x3"
+    assert effective_precision("relu", "bf16") == "bf16"
+
+
+def test_layered_workspace_size_is_checked():
+    """A workspace smaller than dnnmg_mlp_workspace_bytes(m, n_rows) is an argument error,
+    not a silent overrun (host-side check before any launch)."""
+    import ctypes
+    lib = _lib.load()
+    dummy = ctypes.c_void_p(256)
+    W = (ctypes.c_void_p * _lib.MAX_LAYERS)(*([256] * 4 + [0] * (_lib.MAX_LAYERS - 4)))
+    m = _lib.Mlp(174, 64, 3, 81, _lib.ACT_TANH, _lib.PRECISIONS["tf32x3"], W, dummy, dummy,
+                 dummy, dummy, dummy)
+    need = ctypes.c_int64(0)
+    rows = 5000
+    assert lib.dnnmg_mlp_workspace_bytes(ctypes.byref(m), rows, ctypes.byref(need)) == 0
+    assert need.value > 0
+    rc = lib.dnnmg_mlp_forward_ws(ctypes.byref(m), dummy, rows, dummy, dummy, need.value - 1,
+                                  None)
+    assert rc == 1 and b"workspace" in lib.dnnmg_last_error()

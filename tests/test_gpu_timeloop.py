@@ -146,8 +146,12 @@ def test_resume_from_reference_checkpoint(g, name):
     loop = driver.resume_loop(pr, ck, model=product_model(g), J=int(g["J"]), precision="f16x3",
                               correction_scale=float(g["scale"]), correction_start=float(g["start"]))
     assert rel(loop.state.b_next_fine, r[f"{name}_b_next_fine_0"]) < 1e-5
+    # the coarse RHS the first resumed solve receives (for 'mg': the restriction of the
+    # rebuilt fine RHS, driver.py:476-478)
+    assert rel(loop.state.b_next, r[f"{name}_b_next_0"]) < 2e-5
     for n in (1, 2):
         st = loop.step()
+        assert rel(pr.received_b[n - 1], r[f"{name}_b_next_{n - 1}"]) < 2e-5, n
         assert rel(st.x_fine.values, r[f"{name}_x_fine_{n}"]) < 1e-5, n
         assert rel(st.b_next_fine, r[f"{name}_b_next_fine_{n}"]) < 2e-5, n
         assert rel(st.b_next, r[f"{name}_b_next_{n}"]) < 2e-5, n

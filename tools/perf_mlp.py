@@ -1,4 +1,4 @@
-"""Stand-alone MLP timing (config 4 style sweep point): python tests/perf_mlp.py ROWS PREC."""
+"""Stand-alone MLP timing (config 4 style sweep point): python tools/perf_mlp.py ROWS PREC."""
 import sys
 import time
 

@@ -1,5 +1,5 @@
 """Relative L2 error of the MLP output against the float64 oracle per precision mode
-(a diagnostic script run on the GPU box: python tests/prec_cmp.py)."""
+(a diagnostic script run on the GPU box: python tools/prec_cmp.py)."""
 import sys, numpy as np
 sys.path.insert(0, ".")
 from paper_2307_14837_b200 import net

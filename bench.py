@@ -279,18 +279,20 @@ def algorithmic_units(step, cfg):
     }
 
 
-def build_slab_workload(cfg_name, precision, device_index, world, rank, exchanger):
-    """Weak scaling: the global box is world x the config in x; rank r owns one
-    config-sized x-slab and exchanges interface halos with its neighbours."""
+def build_slab_workload(cfg_name, precision, device_index, world, rank, comm):
+    """Strong scaling: the config's global box (config 3: 64x32x32 level-0 cells, 524,288
+    patches) cut into `world` x-slabs; rank r owns slab r.  The coarse states are the global
+    seeded fields at this slab's coarse nodes (pressure drawn per GLOBAL coarse node), the
+    carried fine RHS follows the distributed recurrence b^{n+1} = rhs(x_corr^n) with merged
+    interface rows."""
     import torch
-    from paper_2307_14837_b200 import synthetic
+    from paper_2307_14837_b200 import mesh as meshmod, synthetic
     from paper_2307_14837_b200.net import Architecture, MlpModel
-    from paper_2307_14837_b200.slab import SlabPartition, SlabStep
+    from paper_2307_14837_b200.slab import SlabPartition, SlabStep, global_index
     cfg = synthetic.CONFIGS[cfg_name]
-    nc = (cfg["n_cells"][0] * world, cfg["n_cells"][1], cfg["n_cells"][2])
-    hi = (float(world), 1.0, 1.0)
-    part = SlabPartition((0, 0, 0), hi, nc, 0, cfg["J"], world, rank,
-                         jitter_seed=(cfg["seed"] + 1) if cfg["jitter"] else None)
+    nc = tuple(cfg["n_cells"])
+    jit = (cfg["seed"] + 1) if cfg["jitter"] else None
+    part = SlabPartition((0, 0, 0), (1, 1, 1), nc, 0, cfg["J"], world, rank, jitter_seed=jit)
     npp = part.patchset.nodes_per_patch
     n_in, n_out = 8 * npp + 24, 3 * npp
     model = MlpModel(Architecture(n_in, cfg["hidden"], cfg["depth"], n_out), activation="tanh")
@@ -299,76 +301,133 @@ def build_slab_workload(cfg_name, precision, device_index, world, rank, exchange
     model.eval()
     nu, k = cfg["nu"], cfg["dt"]
     slab = SlabStep(part, model, nu, k, precision=precision)
-    modes = synthetic.fourier_modes(cfg["seed"])
-    xyz = part.h.scalar_nodes(0)[0]
+    # global coarse node ids of this slab's coarse nodes (level-0 numbering of the global box)
+    g0 = meshmod.build_template_mesh("box", extent_lo=(0, 0, 0), extent_hi=(1, 1, 1), n_cells=nc)
+    n_glob = g0.scalar_nodes(0)[0].shape[0]
+    cid = global_index(g0, 0)(part.coarse_pos)
+    K, A, B = synthetic.fourier_modes(cfg["seed"])
     dev = torch.device("cuda", device_index)
+    xyz = torch.tensor(part.h.scalar_nodes(0)[0], dtype=torch.float64, device=dev)
+    kk = torch.tensor(2 * np.pi * K, dtype=torch.float64, device=dev)
+    At = torch.tensor(A, dtype=torch.float64, device=dev)
+    Bt = torch.tensor(B, dtype=torch.float64, device=dev)
 
     def coarse(n):
-        return torch.tensor(synthetic.coarse_state(xyz, modes, cfg["seed"] + 97 * rank, n, n * k, nu),
-                            dtype=torch.float32, device=dev)
-    b = slab.rhs_next(slab.step.embed(coarse(0)), exchanger)
+        t = n * k
+        decay = torch.exp(-nu * (kk ** 2).sum(1) * t)
+        x = torch.empty((xyz.shape[0], 4), dtype=torch.float64, device=dev)
+        for s0 in range(0, xyz.shape[0], 1 << 16):
+            ph = xyz[s0:s0 + (1 << 16)] @ kk.T
+            x[s0:s0 + (1 << 16), 1:] = torch.cos(ph) @ (At * decay[:, None]) + \
+                torch.sin(ph) @ (Bt * decay[:, None])
+        p = np.random.default_rng(cfg["seed"] + 1000 + n).normal(0.0, 0.1, n_glob)[cid]
+        x[:, 0] = torch.from_numpy(p).to(dev)
+        return x.reshape(-1).float().contiguous()
+
+    b = slab.rhs_next(slab.step.embed(coarse(0)), comm)
     pairs = []
-    for n in range(1, 3):
+    for n in range(1, 5):
         xl = coarse(n)
         pairs.append((xl, b.clone()))
-        xc = slab.run(xl, b, exchanger)
-        b = slab.rhs_next(xc, exchanger)
+        xc = slab.run(xl, b, comm)
+        b = slab.rhs_next(xc, comm).clone()
     torch.cuda.synchronize()
     return slab, pairs, cfg
 
 
+def slab_staged(slab, comm, x_coarse, b_prev, events):
+    """slab.run with CUDA events between the stages (same kernels, same stream)."""
+    import ctypes
+    from paper_2307_14837_b200 import _lib, device as dvm
+    st = slab.step
+    s = dvm.stream_handle()
+    e = iter(events)
+    next(e).record()
+    st.embed_into(x_coarse, st.x_tilde)
+    next(e).record()
+    _lib.call("dnnmg_residual", ctypes.byref(st.lv), dvm.ptr(st.x_tilde), dvm.ptr(b_prev), None,
+              None, ctypes.byref(st.phys), dvm.ptr(st.elem), dvm.ptr(st.r), 1, s)
+    next(e).record()
+    _lib.call("dnnmg_halo_pre", ctypes.byref(slab.struct), comm.comm, dvm.ptr(st.elem),
+              dvm.ptr(b_prev), dvm.ptr(st.mask_bits), dvm.ptr(st.r), s)
+    next(e).record()
+    st.predict_rows(s)
+    next(e).record()
+    _lib.call("dnnmg_scatter_update", ctypes.byref(st.ps.struct), dvm.ptr(st.Y),
+              dvm.ptr(st.mask_bits), dvm.ptr(st.x_tilde), ctypes.c_float(st.scale), dvm.ptr(st.d),
+              dvm.ptr(st.x_corr), s)
+    next(e).record()
+    _lib.call("dnnmg_halo_post", ctypes.byref(slab.struct), comm.comm, ctypes.byref(st.ps.struct),
+              dvm.ptr(st.Y), dvm.ptr(st.mask_bits), dvm.ptr(st.x_tilde), ctypes.c_float(st.scale),
+              dvm.ptr(st.d), dvm.ptr(st.x_corr), s)
+    next(e).record()
+
+
+SLAB_STAGES = ["K1_prolong", "K2_residual", "halo_a", "K3K4_gather_mlp", "K5_scatter", "halo_b"]
+
+
 def run_slabs(args, rank, world, local):
-    """N > 1 under torchrun: distributed x-slab correction step over NCCL."""
+    """x-slab decomposition of config 3 (strong scaling) over the library's own NCCL
+    communicator: one rank per GPU under torchrun, or one process with --force-slabs."""
     import torch
     import torch.distributed as tdist
-    from paper_2307_14837_b200.slab import TorchDistExchanger
+    from paper_2307_14837_b200.slab import NcclComm
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ex = TorchDistExchanger()
+    comm = NcclComm(rank, world)
+    assert comm.count() == world
     precision = args.precision or default_precision(args.config)
-    slab, pairs, cfg = build_slab_workload(args.config, precision, local, world, rank, ex)
+    slab, pairs, cfg = build_slab_workload(args.config, precision, local, world, rank, comm)
+    st = slab.step
     S = len(pairs)
+
+    def barrier():
+        tdist.barrier()
+        torch.cuda.synchronize()
+
     for i in range(args.warmup):
-        slab.run(*pairs[i % S], ex)
-    tdist.barrier()
-    torch.cuda.synchronize()
+        slab.run(*pairs[i % S], comm)
+    barrier()
+    # per-stage events inside a first timed pass
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(SLAB_STAGES) + 1)]
+    kern_ms = np.zeros(len(SLAB_STAGES))
+    for i in range(args.steps):
+        slab_staged(slab, comm, *pairs[i % S], ev)
+        ev[-1].synchronize()
+        kern_ms += np.array([ev[j].elapsed_time(ev[j + 1]) for j in range(len(SLAB_STAGES))])
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     with sampler:
         e0.record()
         for i in range(args.steps):
-            slab.run(*pairs[i % S], ex)
+            slab.run(*pairs[i % S], comm)
         e1.record()
-        tdist.barrier()
-        torch.cuda.synchronize()
+        barrier()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
-    n_p = slab.part.n_patches
-    tot = torch.tensor([n_p], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([slab.part.n_patches], dtype=torch.float64, device="cuda")
     tdist.all_reduce(tot)
-    # e2e: the same distributed steps with every rank's x_L / b_prev copied from pinned host
-    # memory and its x_corr copied back inside each step
+    n_total = int(tot.item())
     e2e = None
     if not args.no_e2e:
-        # the same distributed steps from pinned host memory, pipelined as step.HostPipeline
-        # does on one GPU: H2D of step i+1 (copy stream) | kernels + halo exchanges of step i
-        # (compute stream) | D2H of step i-1 (copy stream), double-buffered
+        # the same distributed steps with every rank's x_L / b_prev copied from pinned host
+        # memory and its x_corr copied back inside each step, pipelined as step.HostPipeline:
+        # H2D of step i+1 | kernels + halo exchanges of step i | D2H of step i-1
         hx = [p[0].cpu().pin_memory() for p in pairs]
         hb = [p[1].cpu().pin_memory() for p in pairs]
-        hout = [torch.empty(slab.step.x_corr.numel(), dtype=torch.float32).pin_memory()
-                for _ in range(2)]
+        hout = [torch.empty(st.x_corr.numel(), dtype=torch.float32).pin_memory() for _ in range(2)]
         dx = [torch.empty_like(pairs[0][0]) for _ in range(2)]
         db = [torch.empty_like(pairs[0][1]) for _ in range(2)]
-        dout = [torch.empty_like(slab.step.x_corr) for _ in range(2)]
+        dout = [torch.empty_like(st.x_corr) for _ in range(2)]
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_run = [torch.cuda.Event() for _ in range(2)]
         ev_out = [torch.cuda.Event() for _ in range(2)]
         used = [False, False]
         comp = torch.cuda.current_stream()
-        tdist.barrier()
-        torch.cuda.synchronize()
+        barrier()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0.record()
         s_in.wait_stream(comp)
@@ -384,7 +443,7 @@ def run_slabs(args, rank, world, local):
             comp.wait_event(ev_in[k])
             if used[k]:
                 comp.wait_event(ev_out[k])
-            dout[k].copy_(slab.run(dx[k], db[k], ex))
+            slab.run(dx[k], db[k], comm, x_corr=dout[k])
             ev_run[k].record()
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_run[k])
@@ -394,29 +453,53 @@ def run_slabs(args, rank, world, local):
         comp.wait_stream(s_in)
         comp.wait_stream(s_out)
         h1.record()
-        tdist.barrier()
-        torch.cuda.synchronize()
+        barrier()
         te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device="cuda")
         tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
-        e2e = {"value": float(tot.item()) * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(world * (dx[0].numel() + db[0].numel()) * 4),
-               "d2h_bytes_per_step": int(world * hout[0].numel() * 4),
+        byts = torch.tensor([(dx[0].numel() + db[0].numel()) * 4, hout[0].numel() * 4],
+                            dtype=torch.float64, device="cuda")
+        tdist.all_reduce(byts)
+        e2e = {"value": n_total * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(byts[0].item()), "d2h_bytes_per_step": int(byts[1].item()),
                "overlap": "H2D(i+1) | kernels + halo exchanges(i) | D2H(i-1) on 3 streams"}
     if rank == 0:
+        avg = kern_ms / args.steps
+        per_kernel = {nm: {"ms": float(avg[j]), "share": float(avg[j] / avg.sum())}
+                      for j, nm in enumerate(SLAB_STAGES)}
+        units = algorithmic_units(st, cfg)
+        peaks, peak_kind = load_peaks()
+        for nm, entry in per_kernel.items():
+            u = units.get(nm, {})
+            if "bytes" in u:
+                entry["GB/s"] = u["bytes"] / (entry["ms"] / 1e3) / 1e9
+                entry["hbm_frac"] = entry["GB/s"] / peaks["hbm_gbs"]
+            if "flops" in u:
+                entry["TFLOP/s"] = u["flops"] / (entry["ms"] / 1e3) / 1e12
+        roof = roofline_of(per_kernel, units, precision, peaks, peak_kind)
+        cpu = None if args.no_cpu_baseline else cpu_baseline_entry(cfg, args)
         line = {
-            "metric": METRIC, "value": float(tot.item()) * args.steps / (ms / 1e3), "unit": UNIT,
+            "metric": METRIC, "value": n_total * args.steps / (ms / 1e3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "patches_per_rank": n_p, "J": cfg["J"],
-                       "precision": precision, "parallelism": f"x-slab decomposition x{world}, "
-                       "NCCL P2P halo exchange (2 per step)",
-                       "l2": "inputs > L2 (2 cycled input pairs per rank, every kernel streams "
-                             ">L2-sized arrays)"},
-            "gpu_launches": int((slab.step.launches + 2 * len(slab.idx) + 2) * args.steps),
-            "e2e": e2e, "clocks": sampler.summary(),
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if precision in ("fp32", "tf32x3", "f16x3")
+            else f"f32 (MLP {precision})", "data": "synthetic",
+            "config": {"workload": args.config, "patches": n_total,
+                       "patches_rank0": slab.part.n_patches, "J": cfg["J"],
+                       "coarse_cells": int(np.prod(cfg["n_cells"])), "precision": precision,
+                       "parallelism": f"x-slab decomposition x{world} (strong scaling of the "
+                       f"{args.config} box), NCCL send/recv halo exchange (2 per step) inside "
+                       "libdnnmg_b200, interface sums merged in global order (bitwise equal "
+                       "to 1 GPU)",
+                       "l2": "inputs > L2 (4 cycled input pairs, every kernel streams >L2-sized "
+                             "arrays)"},
+            "e2e": e2e,
+            "gpu_launches": int((st.launches + 4 * sum(p >= 0 for p in slab.part.peer.values()))
+                                * args.steps),
+            "roofline": roof, "kernels": per_kernel, "cpu_baseline": cpu,
+            "clocks": sampler.summary(), "nccl_ranks": comm.count(),
         }
         print(json.dumps(line), flush=True)
+    comm.close()
     tdist.destroy_process_group()
 
 
@@ -525,6 +608,72 @@ def vanka_aux(step, steps, barrier, n_cells=(16, 8, 8)):
     return {"cells": nc, "dofs": ndof, "nnz": int(J.nnz), "setup_ms": t0.elapsed_time(t1),
             "sweep_ms": t_sweep, "sweep_GB/s": byts / (t_sweep / 1e3) / 1e9,
             "note": "msolve.VankaData + vanka_smooth on a synthetic config-1-level Jacobian"}
+
+
+# executed FP32 work of K2's element kernel per fine cell and lane, from its SASS mix at
+# config 3 (ncu smsp__sass_thread_inst_executed_op_{ffma,fmul,fadd}_pred_on / 32 / cells,
+# profiles/r1_kernels_cfg3_ncu.txt): FFMA 659.7, FMUL 271.8, FADD 85.4
+DRAM_TRAFFIC_FILE = "r1_dram_traffic.json"   # newest ncu DRAM capture (per round)
+K2_EXEC_FLOP_PER_CELL = 32 * (2 * 659.7 + 271.8 + 85.4)
+
+
+def fp32_nominal_tflops(peaks):
+    """FP32 SIMT peak: 148 SMs x 128 lanes x 2 FLOP x the max SM clock of MEASURED_PEAKS."""
+    return 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+
+
+def roofline_of(per_kernel, units, precision, peaks, peak_kind, n_cells=None):
+    """`roofline` of the dominant stage (largest event time) and the K2 FP32 roofline."""
+    names = [n for n in per_kernel if n in units or n.startswith("K3K4")]
+    dom = max(names, key=lambda n: per_kernel[n]["ms"])
+    du = units.get(dom, units["K4_mlp"])
+    if "flops" in du:
+        ach = du["flops"] / (per_kernel[dom]["ms"] / 1e3) / 1e12
+        peak = {"bf16": peaks["bf16_tflops_sustained"],
+                "f16x3": peaks["bf16_tflops_sustained"] / 3.0,
+                "tf32x3": peaks["bf16_tflops_sustained"] / 2.0 / 3.0}.get(
+                    precision, peaks["bf16_tflops_sustained"] / 2.0)
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak,
+                "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+                "peak_source": f"{peak_kind} bf16 sustained"
+                + {"bf16": "", "f16x3": " / 3 passes (fp16 rate = bf16 rate)",
+                   "tf32x3": " / 2 (tf32 rate) / 3 passes"}.get(precision, " / 2")}
+    else:
+        ach = du["bytes"] / (per_kernel[dom]["ms"] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": f"{peak_kind} hbm copy"}
+    # K2 is FP32-issue-bound, not HBM-bound: its executed FP32 work against the nominal FP32
+    # SIMT peak at the max SM clock (no micro-benchmark number)
+    if "K2_residual" in per_kernel and n_cells:
+        pk = fp32_nominal_tflops(peaks)
+        ach2 = K2_EXEC_FLOP_PER_CELL * n_cells / (per_kernel["K2_residual"]["ms"] / 1e3) / 1e12
+        per_kernel["K2_residual"]["fp32_roofline"] = {
+            "bound": "fp32 issue", "achieved": ach2, "peak": pk, "unit": "TFLOP/s",
+            "frac": ach2 / pk,
+            "peak_source": "nominal FP32: 148 SMs x 128 lanes x 2 x sm_max_mhz (MEASURED_PEAKS)",
+            "flop_source": "executed FFMA/FMUL/FADD per cell from the element kernel's SASS mix"}
+    # DRAM traffic per launch of each stage from the committed ncu capture
+    try:
+        with open(os.path.join(REPO, "profiles", DRAM_TRAFFIC_FILE)) as f:
+            traffic = json.load(f)
+    except Exception:
+        traffic = {}
+    if isinstance(traffic.get(dom), (int, float)):
+        roof["traffic"] = traffic[dom]
+        roof["traffic_source"] = f"profiles/{DRAM_TRAFFIC_FILE} (ncu --set full, per launch)"
+    for nm, entry in per_kernel.items():
+        if isinstance(traffic.get(nm), (int, float)):
+            entry["dram_bytes_ncu"] = traffic[nm]
+    return roof
+
+
+def cpu_baseline_entry(cfg, args):
+    """The reference CPU path on this host on a bounded sample (rank 0, N = 1 line)."""
+    rate, n_s, t_s = cpu_oracle_rate(cfg, args.cpu_sample, 2, 1)
+    return {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{n_s} patches ({args.cpu_sample} coarse box, J={cfg['J']}), float64 "
+                      f"numpy oracle, median of 2 steps ({t_s:.2f} s/step)"}
 
 
 def run_ours(args, rank, world, local):
@@ -689,55 +838,8 @@ def run_ours(args, rank, world, local):
         if "flops_ref_formulation" in u:
             entry["ref_formulation_TFLOP/s"] = u["flops_ref_formulation"] / (avg[j] / 1e3) / 1e12
         per_kernel[nm] = entry
-    dom = names[int(np.argmax(avg))]
-    du = units.get(dom, units["K4_mlp"])
-    if "flops" in du:
-        ach = du["flops"] / (per_kernel[dom]["ms"] / 1e3) / 1e12
-        peak = {"bf16": peaks["bf16_tflops_sustained"],
-                "f16x3": peaks["bf16_tflops_sustained"] / 3.0,
-                "tf32x3": peaks["bf16_tflops_sustained"] / 2.0 / 3.0}.get(
-                    precision, peaks["bf16_tflops_sustained"] / 2.0)
-        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak,
-                "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-                "peak_source": f"{peak_kind} bf16 sustained"
-                + {"bf16": "", "f16x3": " / 3 passes (fp16 rate = bf16 rate)",
-                   "tf32x3": " / 2 (tf32 rate) / 3 passes"}.get(precision, " / 2")}
-    else:
-        ach = du["bytes"] / (per_kernel[dom]["ms"] / 1e3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
-                "peak_source": f"{peak_kind} hbm copy"}
-    # K2 is FP32-issue-bound, not HBM-bound: its compute roofline against the measured
-    # 3-register FFMA throughput of this GPU (tools/ubench/ffma2.cu: 49.3 TFLOP/s).  FLOPs per
-    # cell of this kernel's formulation from its executed SASS mix (predicated-on thread
-    # instructions per cell / 32: FFMA 659.7, FMUL 271.8, FADD 85.4; ncu
-    # smsp__sass_thread_inst_executed_op_{ffma,fmul,fadd}_pred_on of the element kernel in
-    # profiles/r1_kernels_cfg3_ncu.txt)
-    if "K2_residual" in per_kernel:
-        k2_flop = 32 * (2 * 659.7 + 271.8 + 85.4) * step.level.n_cells
-        ach2 = k2_flop / (per_kernel["K2_residual"]["ms"] / 1e3) / 1e12
-        per_kernel["K2_residual"]["fp32_roofline"] = {
-            "bound": "fp32 issue", "achieved": ach2, "peak": 49.3, "unit": "TFLOP/s",
-            "frac": ach2 / 49.3,
-            "peak_source": "measured FFMA (register form) throughput, tools/ubench/ffma2.cu"}
-    # DRAM traffic per launch of each stage from the committed ncu capture (round-1 profile)
-    try:
-        with open(os.path.join(REPO, "profiles", "r1_dram_traffic.json")) as f:
-            traffic = json.load(f)
-    except Exception:
-        traffic = {}
-    if isinstance(traffic.get(dom), (int, float)):
-        roof["traffic"] = traffic[dom]
-        roof["traffic_source"] = "profiles/r1_dram_traffic.json (ncu --set full, per launch)"
-    for nm, entry in per_kernel.items():
-        if isinstance(traffic.get(nm), (int, float)):
-            entry["dram_bytes_ncu"] = traffic[nm]
-    cpu = None
-    if not args.no_cpu_baseline:
-        rate, n_s, t_s = cpu_oracle_rate(cfg, args.cpu_sample, 2, 1)
-        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{n_s} patches ({args.cpu_sample} coarse box, J={cfg['J']}), float64 "
-                         f"numpy oracle, median of 2 steps ({t_s:.2f} s/step)"}
+    roof = roofline_of(per_kernel, units, precision, peaks, peak_kind, step.level.n_cells)
+    cpu = None if args.no_cpu_baseline else cpu_baseline_entry(cfg, args)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

@@ -19,9 +19,10 @@
  *   dnnmg_scatter_update    predict_correction scatter + x~ + scale*d
  *                                                       patch_ops.py:64-76, driver.py:268
  *   dnnmg_correction_step   TimeLoop._step_hybrid lines 251-268 (K1..K5 fused sequence)
- *   dnnmg_halo_*            x-slab decomposition of the same step (no reference counterpart:
- *                           the reference is single-process); the interface sums
- *                           reproduce assembly.py:180-184 / patch_ops.py:32-38 across ranks
+ *   dnnmg_halo_*, dnnmg_nccl_*  x-slab decomposition of the same step (no reference
+ *                           counterpart: the reference is single-process); the
+ *                           interface sums reproduce assembly.py:180-184 / patch_ops.py:32-38
+ *                           across ranks in the same (global) order
  *
  * Conventions (all match the reference):
  *   - dof vectors are node-major, component-minor: dof = 4*node + comp,
@@ -342,29 +343,73 @@ int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_d
                               dnnmg_stream_t stream);
 
 /* ---- x-slab halo (interface) operations, SURVEY §8(e) -------------------------------------
- * idx: [n] local fine-node ids of one interface plane, in the order both neighbours agree on.
- * All vectors are float4 rows (node-major). */
-/* out[i] = a[idx[i]] - b[idx[i]] (b nullable) — e.g. the partial operator A = b_prev - r_local */
-int32_t dnnmg_halo_gather(const int32_t* idx, int32_t n, const float* a, const float* b, float* out,
-                          dnnmg_stream_t stream);
-/* out[i] = this rank's partial A_h(x~) at idx[i]: element vectors (from dnnmg_residual's
- * scratch) summed over the node's local cells in ascending cell id */
-int32_t dnnmg_halo_operator(const dnnmg_level_t* lv, const float* elem_scratch, const int32_t* idx,
-                            int32_t n, float* out, dnnmg_stream_t stream);
-/* r[idx[i]] = b[idx[i]] - (A_left[i] + A_right[i]); masked dofs -> 0 */
-int32_t dnnmg_halo_residual(const int32_t* idx, int32_t n, const float* b, const float* own,
-                            const float* nb, int32_t own_is_left, const uint8_t* dof_mask, float* r,
-                            dnnmg_stream_t stream);
-/* out[idx[i]] = A_left[i] + A_right[i]: interface rows of an assembled dual vector (next RHS) */
-int32_t dnnmg_halo_sum(const int32_t* idx, int32_t n, const float* own, const float* nb,
-                       int32_t own_is_left, float* out, dnnmg_stream_t stream);
-/* out[i] = (patch count, raw sums of the 3 velocity predictions) at idx[i] */
-int32_t dnnmg_halo_scatter_sums(const dnnmg_patchset_t* ps, const float* Y, const int32_t* idx,
-                                int32_t n, float* out, dnnmg_stream_t stream);
-/* d = (S_left + S_right)/(count_left + count_right), mask, x_corr = x~ + scale*d at idx */
-int32_t dnnmg_halo_scatter_apply(const int32_t* idx, int32_t n, const float* own, const float* nb,
-                                 int32_t own_is_left, const uint8_t* dof_mask, const float* x_tilde,
-                                 float scale, float* d, float* x_corr, dnnmg_stream_t stream);
+ * The single-domain step sums, per node, element vectors in ascending GLOBAL cell id
+ * (assembly.py:180-184) and patch predictions in ascending GLOBAL patch id
+ * (patch_ops.py:32-38).  Along a slab interface those orders interleave the two sides, so
+ * each rank sends its raw per-(cell, local node) element rows / per-(patch, slot) velocity
+ * predictions of the interface nodes, and both ranks sum the union in the global order of a
+ * merge plan: interface values are bitwise equal on both sides and to the single domain.
+ * All buffers are float4 rows. */
+typedef struct {
+  int32_t n_nodes;           /* interface nodes of this side */
+  const int32_t* nodes;      /* [n_nodes] local node ids, in the order both ranks agree on */
+  int32_t n_send;            /* entries this rank sends (= entries it receives) */
+  const int32_t* send;       /* [n_send] local entries (cell*27 + a, or patch*npp + slot):
+                                nodes in order, each node's entries by ascending global id */
+  const int32_t* merge_ptr;  /* [n_nodes+1] */
+  const int32_t* merge_src;  /* [merge_ptr[n_nodes]] a node's entries by ascending global id:
+                                >= 0 local entry, < 0 entry -(1+q) of the received message */
+} dnnmg_halo_plan_t;
+
+/* One rank's interfaces: side 0 = left neighbour (rank-1), side 1 = right (rank+1). */
+typedef struct {
+  int32_t peer[2];                 /* neighbour rank per side, -1 = no neighbour */
+  dnnmg_halo_plan_t cells[2];      /* element-vector plans of the fine level */
+  dnnmg_halo_plan_t patches[2];    /* (patch, slot) plans */
+  float* send[2];                  /* [max n_send][4] device message buffers per side */
+  float* recv[2];
+} dnnmg_slab_t;
+
+/* sendbuf[j] = rows[h->send[j]] (float4 rows, e.g. the element scratch of dnnmg_residual) */
+int32_t dnnmg_halo_pack_rows(const dnnmg_halo_plan_t* h, const float* rows, float* sendbuf,
+                             dnnmg_stream_t stream);
+/* sendbuf[j] = (Y velocity triple of entry h->send[j] = patch*npp + slot, 0) */
+int32_t dnnmg_halo_pack_patch_rows(const dnnmg_halo_plan_t* h, const dnnmg_patchset_t* ps,
+                                   const float* Y, float* sendbuf, dnnmg_stream_t stream);
+/* out[node] = b[node] - (merged sum) (b NULL: the sum itself, e.g. the next RHS); masked dofs
+ * -> 0 (mask nullable) */
+int32_t dnnmg_halo_merge_rows(const dnnmg_halo_plan_t* h, const float* rows, const float* recvbuf,
+                              const float* b, const uint8_t* mask, float* out,
+                              dnnmg_stream_t stream);
+/* d[node] = mu * (merged sum of the velocity predictions), mu = 1/(incident patches on both
+ * sides); masked dofs -> 0; x_corr = x~ + scale*d (x_corr nullable) */
+int32_t dnnmg_halo_merge_scatter(const dnnmg_halo_plan_t* h, const dnnmg_patchset_t* ps,
+                                 const float* Y, const float* recvbuf, const uint8_t* mask,
+                                 const float* x_tilde, float scale, float* d, float* x_corr,
+                                 dnnmg_stream_t stream);
+
+/* NCCL (the library binds the libnccl.so.2 already loaded in the process, else dlopens it).
+ * comm is an ncclComm_t.  Bootstrap: rank 0 calls dnnmg_nccl_unique_id (128 bytes), the id is
+ * broadcast out of band (torch.distributed store), every rank calls dnnmg_nccl_comm_init. */
+int32_t dnnmg_nccl_available(void);
+int32_t dnnmg_nccl_unique_id(void* id_out /* 128 bytes */);
+int32_t dnnmg_nccl_comm_init(const void* id, int32_t nranks, int32_t rank, void** comm);
+int32_t dnnmg_nccl_comm_count(void* comm, int32_t* count);
+int32_t dnnmg_nccl_comm_destroy(void* comm);
+/* grouped ncclSend/ncclRecv of count[side] float4 rows with peer[side] (< 0: none) on stream */
+int32_t dnnmg_halo_exchange(void* comm, const int32_t peer[2], const float* const send[2],
+                            float* const recv[2], const int64_t count[2], dnnmg_stream_t stream);
+/* exchange (a), between the residual and the MLP: pack the interface element vectors,
+ * exchange with both neighbours, write the merged r = b_prev - A at the interface nodes
+ * (b_prev NULL: the merged sum, for the next-step RHS) */
+int32_t dnnmg_halo_pre(const dnnmg_slab_t* sl, void* comm, const float* elem_scratch,
+                       const float* b_prev, const uint8_t* dof_mask, float* r,
+                       dnnmg_stream_t stream);
+/* exchange (b), after the MLP: pack the interface patch predictions, exchange, write the merged
+ * d and x_corr at the interface nodes */
+int32_t dnnmg_halo_post(const dnnmg_slab_t* sl, void* comm, const dnnmg_patchset_t* ps,
+                        const float* Y, const uint8_t* dof_mask, const float* x_tilde, float scale,
+                        float* d, float* x_corr, dnnmg_stream_t stream);
 
 /* Number of kernels dnnmg_correction_step launches for this configuration. */
 int32_t dnnmg_correction_step_launches(int32_t J, const dnnmg_mlp_t* m);

@@ -73,6 +73,16 @@ class Vanka(ctypes.Structure):
                 ("dof_cell_ptr", c_vp), ("dof_cell_idx", c_vp), ("weight", c_vp), ("inv", c_vp)]
 
 
+class HaloPlan(ctypes.Structure):
+    _fields_ = [("n_nodes", c_i32), ("nodes", c_vp), ("n_send", c_i32), ("send", c_vp),
+                ("merge_ptr", c_vp), ("merge_src", c_vp)]
+
+
+class Slab(ctypes.Structure):
+    _fields_ = [("peer", c_i32 * 2), ("cells", HaloPlan * 2), ("patches", HaloPlan * 2),
+                ("send", c_vp * 2), ("recv", c_vp * 2)]
+
+
 class StepBuffers(ctypes.Structure):
     _fields_ = [("x_tilde", c_vp), ("r", c_vp), ("elem", c_vp), ("X", c_vp), ("Y", c_vp),
                 ("d", c_vp), ("x_mid", c_vp), ("mlp_ws", c_vp), ("mlp_ws_bytes", c_i64)]
@@ -119,13 +129,23 @@ EXPORTS = {
                                       ctypes.POINTER(PatchSet), ctypes.POINTER(Mlp), c_vp, c_vp,
                                       c_f32, ctypes.POINTER(StepBuffers), c_vp, c_vp]),
     "dnnmg_correction_step_launches": (c_i32, [c_i32, ctypes.POINTER(Mlp)]),
-    "dnnmg_halo_gather": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
-    "dnnmg_halo_operator": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp, c_i32, c_vp, c_vp]),
-    "dnnmg_halo_sum": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp]),
-    "dnnmg_halo_residual": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
-    "dnnmg_halo_scatter_sums": (c_i32, [ctypes.POINTER(PatchSet), c_vp, c_vp, c_i32, c_vp, c_vp]),
-    "dnnmg_halo_scatter_apply": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_vp,
-                                         c_vp, c_vp]),
+    "dnnmg_halo_pack_rows": (c_i32, [ctypes.POINTER(HaloPlan), c_vp, c_vp, c_vp]),
+    "dnnmg_halo_pack_patch_rows": (c_i32, [ctypes.POINTER(HaloPlan), ctypes.POINTER(PatchSet),
+                                           c_vp, c_vp, c_vp]),
+    "dnnmg_halo_merge_rows": (c_i32, [ctypes.POINTER(HaloPlan), c_vp, c_vp, c_vp, c_vp, c_vp,
+                                      c_vp]),
+    "dnnmg_halo_merge_scatter": (c_i32, [ctypes.POINTER(HaloPlan), ctypes.POINTER(PatchSet), c_vp,
+                                         c_vp, c_vp, c_vp, c_f32, c_vp, c_vp, c_vp]),
+    "dnnmg_nccl_available": (c_i32, []),
+    "dnnmg_nccl_unique_id": (c_i32, [c_vp]),
+    "dnnmg_nccl_comm_init": (c_i32, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "dnnmg_nccl_comm_count": (c_i32, [c_vp, ctypes.POINTER(c_i32)]),
+    "dnnmg_nccl_comm_destroy": (c_i32, [c_vp]),
+    "dnnmg_halo_exchange": (c_i32, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_vp),
+                                    ctypes.POINTER(c_vp), ctypes.POINTER(c_i64), c_vp]),
+    "dnnmg_halo_pre": (c_i32, [ctypes.POINTER(Slab), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dnnmg_halo_post": (c_i32, [ctypes.POINTER(Slab), c_vp, ctypes.POINTER(PatchSet), c_vp, c_vp,
+                                c_vp, c_f32, c_vp, c_vp, c_vp]),
 }
 
 _lib = None

@@ -1,9 +1,9 @@
 """Multi-rank x-slab decomposition on CPU: 2 (and 3) processes over torch.distributed
 gloo.  Each rank builds its SlabPartition (local hierarchy with global boundary
-tags, interface node lists, global pressure pin), computes its local part of the
-correction step with the float64 oracle, exchanges the interface partial
-operator and the raw patch sums with TorchDistExchanger, and completes the
-interface rows exactly as the halo kernels do.  The assembled global d must
+tags, interface node lists and merge plans, global pressure pin), computes its local
+part of the correction step with the float64 oracle, exchanges the raw interface element
+rows and patch predictions with TorchDistExchanger, and merges them in the plans' global
+order exactly as the halo kernels do.  The assembled global d must
 equal the single-domain oracle result, and both sides of an interface must hold
 identical values."""
 import os
@@ -94,12 +94,22 @@ def _worker(rank, world, port, out_q):
         for sl, g in geom.chunks:
             cont, mom = orc.element_vectors(xt, g, table[sl], c["k"], c["nu"], aT[sl], dT[sl])
             A += orc.assemble(table[sl], cont, mom, xt.size)
-        A4 = A.reshape(-1, 4)
-        sends = {s: torch.tensor(A4[n]) for s, n in part.iface.items()}
+        # element rows (cell*27 + a) -> exchange (a) of the interface rows in plan order,
+        # merged per node in ascending global cell id (halo_merge_rows_kernel)
+        cont, mom = orc.element_vectors(xt, geom.chunks[0][1], table, c["k"], c["nu"], aT, dT) \
+            if len(geom.chunks) == 1 else (None, None)
+        assert cont is not None
+        elem = np.concatenate([cont[:, :, None], mom], axis=2).reshape(-1, 4)
+        sends = {s: torch.tensor(elem[pl["send"]]) for s, pl in part.cell_plans.items()}
         recv = ex.exchange(sends)
-        for s, n in part.iface.items():  # left partial first (halo_residual_kernel)
-            L_, R_ = (sends[s], recv[s]) if s == "right" else (recv[s], sends[s])
-            A4[n] = (L_ + R_).numpy()
+        A4 = A.reshape(-1, 4)
+        for s, pl in part.cell_plans.items():
+            rv = recv[s].numpy()
+            for i, node in enumerate(pl["nodes"]):
+                acc = np.zeros(4)
+                for src in pl["merge_src"][pl["merge_ptr"][i]:pl["merge_ptr"][i + 1]]:
+                    acc = acc + (elem[src] if src >= 0 else rv[-1 - src])
+                A4[node] = acc
         bl = b.reshape(-1, 4)[fid].reshape(-1)
         r = bl - A
         r[part.mask] = 0.0
@@ -112,14 +122,20 @@ def _worker(rank, world, port, out_q):
         rows[:, vel] = Y
         S = np.bincount(ps.dof_table.ravel(), weights=rows.ravel(), minlength=xt.size).reshape(-1, 4)
         cnt = np.bincount(ps.node_table.ravel(), minlength=xt.size // 4).astype(float)
-        sends = {s: torch.tensor(np.concatenate([cnt[n][:, None], S[n, 1:]], axis=1))
-                 for s, n in part.iface.items()}
-        recv = ex.exchange(sends)
         d = (S / cnt[:, None])
-        for s, n in part.iface.items():  # halo_scatter_apply_kernel
-            L_, R_ = (sends[s], recv[s]) if s == "right" else (recv[s], sends[s])
-            tot = (L_ + R_).numpy()
-            d[n, 1:] = tot[:, 1:] / tot[:, :1]
+        # exchange (b): the interface (patch, slot) predictions, merged in ascending global
+        # patch id with the global valence (halo_merge_scatter_kernel)
+        Yr = Y.reshape(-1, 3)
+        sends = {s: torch.tensor(Yr[pl["send"]]) for s, pl in part.patch_plans.items()}
+        recv = ex.exchange(sends)
+        for s, pl in part.patch_plans.items():
+            rv = recv[s].numpy()
+            for i, node in enumerate(pl["nodes"]):
+                src_i = pl["merge_src"][pl["merge_ptr"][i]:pl["merge_ptr"][i + 1]]
+                acc = np.zeros(3)
+                for src in src_i:
+                    acc = acc + (Yr[src] if src >= 0 else rv[-1 - src])
+                d[node, 1:] = acc / len(src_i)
         d[:, 0] = 0.0
         d = d.reshape(-1)
         d[part.mask] = 0.0

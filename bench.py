@@ -117,24 +117,120 @@ def cpu_oracle_rate(cfg, sample, steps, warmup):
     return n_p / t, n_p, t
 
 
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+
+def import_reference():
+    """The UNMODIFIED reference package `dnnmg`, pip-installed into baseline/_ref (DESIGN.md
+    §6 records the install).  Returns the module namespace or raises."""
+    if not os.path.isdir(os.path.join(REF_DIR, "dnnmg")):
+        raise RuntimeError("baseline/_ref/dnnmg is not installed")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import dnnmg  # noqa: F401
+    from dnnmg import driver, mesh, net, patch_ops, space
+    return dict(driver=driver, mesh=mesh, net=net, patch_ops=patch_ops, space=space)
+
+
+class ReferenceStep:
+    """One correction step of the reference's own code path (driver.py:251-268, BASELINE.md
+    §2): embed_state (prolongate + Dirichlet) -> Assembler.stab -> assemble_residual ->
+    patch_ops.predict_correction (gather, net.forward, bincount scatter) -> x~ + d, float64,
+    on a bounded sample box with the config's per-patch work (same J, MLP, inputs)."""
+
+    def __init__(self, cfg, sample):
+        from paper_2307_14837_b200 import synthetic
+        R = import_reference()
+        self.R = R
+        n_cells = tuple(int(v) for v in sample.split("x"))
+        h = R["mesh"].build_template_mesh("box", extent_lo=(0, 0, 0), extent_hi=(1, 1, 1),
+                                          n_cells=n_cells)
+        if cfg["jitter"]:
+            synthetic.jitter_vertices(h.levels[0].vertices, n_cells, (0, 0, 0), (1, 1, 1),
+                                      cfg["seed"] + 1)
+        for _ in range(cfg["J"]):
+            R["mesh"].refine_uniform(h)
+        self.L, self.J = 0, cfg["J"]
+        self.nu, self.k = cfg["nu"], cfg["dt"]
+        self.pr = R["driver"].NsProblem(h, nu=self.nu, k=self.k,
+                                        bcs={R["mesh"].WALL: R["space"].no_slip})
+        self.ps = R["mesh"].build_patches(h, self.L, self.J)
+        n_in, n_out = R["patch_ops"].input_width(self.ps), R["patch_ops"].output_width(self.ps)
+        self.model = R["net"].MlpModel(R["net"].Architecture(n_in, cfg["hidden"], cfg["depth"],
+                                                             n_out), activation="tanh")
+        self.model.W = synthetic.xavier_weights([n_in] + [cfg["hidden"]] * cfg["depth"] + [n_out],
+                                                cfg["seed"] + 7)
+        self.model.eval()
+        fl = self.L + self.J
+        self.asm = self.pr.asm(fl)           # the reference's Assembler (geometry cache: setup)
+        self.mask = self.pr.mask(fl)
+        modes = synthetic.fourier_modes(cfg["seed"])
+        nodes = self.pr.space(self.L).nodes
+        x0 = synthetic.coarse_state(nodes, modes, cfg["seed"], 0, 0.0, self.nu)
+        xf0 = R["driver"].embed_state(self.pr, self.L, self.J, x0, 0.0)
+        self.b = self.asm.assemble_rhs_next(xf0, None, None, self.k, self.nu)
+        self.xs = [synthetic.coarse_state(nodes, modes, cfg["seed"], n, n * self.k, self.nu)
+                   for n in (1, 2)]
+        self.n_patches = len(self.ps)
+
+    def __call__(self, i):
+        R, pr = self.R, self.pr
+        t = (1 + i % 2) * self.k
+        xt = R["driver"].embed_state(pr, self.L, self.J, self.xs[i % 2], t)
+        stab = self.asm.stab(xt, self.nu, self.k, pr.alpha0, pr.delta0)
+        r = self.asm.assemble_residual(xt, self.b, self.k, self.nu, stab, mask=self.mask)
+        d = R["patch_ops"].predict_correction(self.model, xt, r, self.ps, dirichlet_mask=self.mask)
+        return xt + d
+
+
+def reference_rate(step, steps, warmup, threads):
+    """Mean patches/s of `steps` reference steps after `warmup`, with the BLAS pool limited to
+    `threads` (threadpoolctl: OPENBLAS_NUM_THREADS at run time)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        for i in range(warmup):
+            step(i)
+        t0 = time.perf_counter()
+        for i in range(steps):
+            step(i)
+        dt = (time.perf_counter() - t0) / max(steps, 1)
+    return step.n_patches / dt, dt
+
+
 def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation of the step (baseline/_ref,
+    float64 numpy/scipy) on this host, all cores and one core, rank 0 only."""
     from paper_2307_14837_b200 import synthetic
     if rank != 0:
         return
     cfg = synthetic.CONFIGS[args.config]
-    steps = max(1, min(args.steps, 10))
-    warmup = max(0, min(args.warmup, 2))
-    rate, n_p, t = cpu_oracle_rate(cfg, args.cpu_sample, steps, warmup)
     cores = os.cpu_count()
-    sample = (f"{n_p} patches ({args.cpu_sample} coarse box, J={cfg['J']}) of {args.config}; "
-              f"float64 numpy oracle port; median of {steps} steps after {warmup} warm-up")
+    try:
+        t_setup = time.perf_counter()
+        step = ReferenceStep(cfg, args.cpu_sample)
+        t_setup = time.perf_counter() - t_setup
+    except Exception as exc:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference import/setup failed: "
+                          f"{str(exc)[:160]}"}), flush=True)
+        return
+    rate, t = reference_rate(step, args.steps, args.warmup, cores)
+    rate1, t1 = reference_rate(step, max(1, args.steps // 4), min(args.warmup, 1), 1)
+    sample = (f"{step.n_patches} patches ({args.cpu_sample} coarse box, J={cfg['J']}, "
+              f"{cfg['hidden']}x{cfg['depth']} tanh MLP) of {args.config}: the reference's "
+              f"embed_state -> stab -> assemble_residual -> predict_correction -> x~+d, float64; "
+              f"mean of {args.steps} steps after {args.warmup} warm-up ({t:.3f} s/step); "
+              f"setup (Assembler geometry cache, PatchSet) {t_setup:.1f} s excluded")
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
-        "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "sample": args.cpu_sample},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "threads": cores, "sample": sample,
+                         "threads_1": {"value": rate1, "unit": UNIT, "cores": 1,
+                                       "s_per_step": t1,
+                                       "steps": max(1, args.steps // 4)}},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -475,7 +571,7 @@ def run_slabs(args, rank, world, local):
                 entry["hbm_frac"] = entry["GB/s"] / peaks["hbm_gbs"]
             if "flops" in u:
                 entry["TFLOP/s"] = u["flops"] / (entry["ms"] / 1e3) / 1e12
-        roof = roofline_of(per_kernel, units, precision, peaks, peak_kind)
+        roof = roofline_of(per_kernel, units, precision, peaks, peak_kind, st.level.n_cells)
         cpu = None if args.no_cpu_baseline else cpu_baseline_entry(cfg, args)
         line = {
             "metric": METRIC, "value": n_total * args.steps / (ms / 1e3), "unit": UNIT,
@@ -669,11 +765,25 @@ def roofline_of(per_kernel, units, precision, peaks, peak_kind, n_cells=None):
 
 
 def cpu_baseline_entry(cfg, args):
-    """The reference CPU path on this host on a bounded sample (rank 0, N = 1 line)."""
-    rate, n_s, t_s = cpu_oracle_rate(cfg, args.cpu_sample, 2, 1)
-    return {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{n_s} patches ({args.cpu_sample} coarse box, J={cfg['J']}), float64 "
-                      f"numpy oracle, median of 2 steps ({t_s:.2f} s/step)"}
+    """The reference's own CPU path (baseline/_ref) on this host on a bounded sample (rank 0,
+    N = 1 line); the float64 oracle port when the reference is not installed."""
+    cores = os.cpu_count()
+    try:
+        step = ReferenceStep(cfg, args.cpu_sample)
+    except Exception as exc:
+        rate, n_s, t_s = cpu_oracle_rate(cfg, args.cpu_sample, 2, 1)
+        return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": f"{n_s} patches ({args.cpu_sample} coarse box, J={cfg['J']}), float64 "
+                          f"numpy oracle, median of 2 steps ({t_s:.2f} s/step); reference "
+                          f"unavailable: {str(exc)[:80]}"}
+    rate, t = reference_rate(step, 3, 1, cores)
+    rate1, t1 = reference_rate(step, 2, 0, 1)
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{step.n_patches} patches ({args.cpu_sample} coarse box, J={cfg['J']}) "
+                      f"through the reference's embed_state -> stab -> assemble_residual -> "
+                      f"predict_correction, float64, mean of 3 steps ({t:.2f} s/step), all "
+                      f"{cores} host threads",
+            "threads_1": {"value": rate1, "unit": UNIT, "cores": 1, "s_per_step": t1}}
 
 
 def run_ours(args, rank, world, local):

@@ -90,6 +90,20 @@ def test_big_config_step(name, precision):
     check("x_corr", out, pin, TOL_D[precision])
     if precision != "bf16":
         check("b_next", step.rhs_next(out), pin, 2e-6 + TOL_D[precision])
+    # the product's OWN gathered network-input rows (dnnmg_gather over its index tables) at
+    # the reference's sampled patches: the geometry block bit-exact, the x~ / r blocks at the
+    # x~ / r gates (a wrong node map would show O(1) errors)
+    from paper_2307_14837_b200 import patch_ops
+    X = patch_ops.assemble_network_input(step.x_tilde, step.r, c["ps"])
+    rows = torch.as_tensor(pin["rows"].astype(np.int64), device="cuda")
+    Xs = X[rows].cpu().numpy()
+    nd = 4 * c["ps"].nodes_per_patch
+    assert np.array_equal(Xs[:, 2 * nd:], pin["X"][:, 2 * nd:])
+    ex = np.linalg.norm(Xs[:, :nd] - pin["X"][:, :nd]) / np.linalg.norm(pin["X"][:, :nd])
+    er = np.linalg.norm(Xs[:, nd:2 * nd] - pin["X"][:, nd:2 * nd]) / np.linalg.norm(
+        pin["X"][:, nd:2 * nd])
+    assert ex < 1e-7 and er < 2e-5, (ex, er)
+    del X
     # the reference's own network input rows through the product's MLP
     Y = net.forward(c["model"], pin["X"].astype(np.float64), precision=precision)
     assert np.linalg.norm(Y - pin["Y"]) / np.linalg.norm(pin["Y"]) < TOL_D[precision]

@@ -111,3 +111,22 @@ def test_slabs_bitwise_equal_single_domain_j2(world, precision):
     ref, got, _ = run_slabs(2, precision, world)
     for k in ("r", "d", "x_corr", "b_next"):
         assert torch.equal(got[k].reshape(-1), ref[k]), (k, world, precision)
+
+
+def test_library_nccl_communicator_single_rank():
+    """The library's own NCCL bootstrap (dnnmg_nccl_unique_id / comm_init, binding the NCCL
+    torch loaded) on one rank, and the fused halo entry points with no neighbour."""
+    from paper_2307_14837_b200.slab import NcclComm
+    ref = single_domain(1, "f16x3")
+    comm = NcclComm(0, 1)
+    try:
+        assert comm.count() == 1
+        part = SlabPartition(LO, HI, CASES[1]["nc"], 0, 1, 1, 0, jitter_seed=JIT)
+        slab = SlabStep(part, ref["m"], NU, K, precision="f16x3", t=K)
+        assert part.iface == {} and slab.sendbuf == {}
+        out = slab.run(ref["x1"], ref["b"], comm)
+        b_next = slab.rhs_next(out, comm)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref["x_corr"]) and torch.equal(b_next, ref["b_next"])
+    finally:
+        comm.close()

@@ -140,6 +140,12 @@ typedef struct {
                                     build passes nodes by descending first incident cell, so
                                     the element vectors written last (still in L2) are read
                                     first and every node is visited next to its cells */
+  /* optional tensor-core element kernel (all set, or tc_const NULL = the SIMT kernel): */
+  const void* tc_const;          /* constant operand image, dnnmg_k2tc_constants_bytes() bytes,
+                                    written once by dnnmg_k2tc_constants */
+  const float* tc_geo;           /* dnnmg_level_geometry_tc output */
+  int32_t tc_geo_affine;         /* its layout: 0 = per point, 1 = per-cell affine record,
+                                    2 = the same for axis-aligned cells (J^-1 diagonal) */
 } dnnmg_level_t;
 
 typedef struct {
@@ -205,6 +211,19 @@ int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* b_fine, float* b_
 /* geometry cache of a level (constant mesh): geo_out = [n_cells][10][64] float32, i.e.
  * 2,560 bytes per cell; set lv->geo_q = geo_out to let K2 skip the geometry work */
 int32_t dnnmg_level_geometry(const dnnmg_level_t* lv, float* geo_out, dnnmg_stream_t stream);
+/* Tensor-core K2 (element vectors as tcgen05 GEMMs, SURVEY App. C "K2 v2"): the constant
+ * operand image (Q2 basis / gradient / projected-gradient tables at the Gauss points, fp16
+ * hi/lo, 160 KB, device buffer 128-byte aligned) and the geometry in the kernel's layout:
+ * affine != 0 (every cell's isoparametric map affine, e.g. an unjittered box) -> per-cell
+ * record [10][n_cells] (J^-1 row-major, det J); affine == 0 -> the per-point cache re-laid
+ * out by 128-cell tiles [n_tiles][10][64][128], then the cells' volumes [n_tiles*128] (the
+ * reference mass applied exactly on the CUDA cores).  Needs lv->geo_q (dnnmg_level_geometry).
+ * out: dnnmg_level_geometry_tc_floats(lv, affine) floats. */
+int64_t dnnmg_k2tc_constants_bytes(void);
+int32_t dnnmg_k2tc_constants(void* img, dnnmg_stream_t stream);
+int64_t dnnmg_level_geometry_tc_floats(const dnnmg_level_t* lv, int32_t affine);
+int32_t dnnmg_level_geometry_tc(const dnnmg_level_t* lv, float* out, int32_t affine,
+                                dnnmg_stream_t stream);
 int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph,
                    float* alpha_T, float* delta_T, dnnmg_stream_t stream);
 /* r = b_prev - A_h(x); rows with dof_mask bits set are zeroed when apply_mask != 0.

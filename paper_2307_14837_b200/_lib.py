@@ -34,7 +34,8 @@ class Dirichlet(ctypes.Structure):
 class Level(ctypes.Structure):
     _fields_ = [("n_nodes", c_i32), ("n_cells", c_i32), ("cell_nodes", c_vp), ("coords", c_vp),
                 ("h_T", c_vp), ("node_cell_ptr", c_vp), ("node_cell_idx", c_vp),
-                ("dof_mask", c_vp), ("geo_q", c_vp), ("node_order", c_vp)]
+                ("dof_mask", c_vp), ("geo_q", c_vp), ("node_order", c_vp),
+                ("tc_const", c_vp), ("tc_geo", c_vp), ("tc_geo_affine", c_i32)]
 
 
 class Phys(ctypes.Structure):
@@ -96,6 +97,10 @@ EXPORTS = {
     "dnnmg_apply_dirichlet": (c_i32, [ctypes.POINTER(Dirichlet), c_vp, c_vp]),
     "dnnmg_restrict": (c_i32, [ctypes.POINTER(Restrict), c_vp, c_vp, c_vp]),
     "dnnmg_level_geometry": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp]),
+    "dnnmg_k2tc_constants_bytes": (c_i64, []),
+    "dnnmg_k2tc_constants": (c_i32, [c_vp, c_vp]),
+    "dnnmg_level_geometry_tc_floats": (c_i64, [ctypes.POINTER(Level), c_i32]),
+    "dnnmg_level_geometry_tc": (c_i32, [ctypes.POINTER(Level), c_vp, c_i32, c_vp]),
     "dnnmg_stab": (c_i32, [ctypes.POINTER(Level), c_vp, ctypes.POINTER(Phys), c_vp, c_vp, c_vp]),
     "dnnmg_residual": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(Phys),
                                c_vp, c_vp, c_i32, c_vp]),

@@ -20,6 +20,9 @@ int32_t launch_prolongate(const dnnmg_prolong_t*, const float*, float*, const dn
 int32_t launch_dirichlet(const dnnmg_dirichlet_t*, float*, cudaStream_t);
 int32_t launch_restrict(const dnnmg_restrict_t*, const float*, float*, cudaStream_t);
 int32_t launch_level_geometry(const dnnmg_level_t*, float*, cudaStream_t);
+int64_t k2tc_constant_bytes();
+int32_t launch_k2tc_constants(void*, cudaStream_t);
+int32_t launch_k2tc_geometry(const dnnmg_level_t*, float*, int32_t, cudaStream_t);
 int32_t launch_stab(const dnnmg_level_t*, const float*, const dnnmg_phys_t*, float*, float*,
                     cudaStream_t);
 int32_t launch_residual(const dnnmg_level_t*, const float*, const float*, const float*,
@@ -101,6 +104,23 @@ int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* bf, float* bc, dn
 
 int32_t dnnmg_level_geometry(const dnnmg_level_t* lv, float* geo, dnnmg_stream_t s) {
   return launch_level_geometry(lv, geo, as_stream(s));
+}
+
+int64_t dnnmg_k2tc_constants_bytes(void) { return k2tc_constant_bytes(); }
+
+int32_t dnnmg_k2tc_constants(void* img, dnnmg_stream_t s) {
+  return launch_k2tc_constants(img, as_stream(s));
+}
+
+int64_t dnnmg_level_geometry_tc_floats(const dnnmg_level_t* lv, int32_t affine) {
+  if (!lv || lv->n_cells <= 0) return 0;
+  const int64_t n_tiles = (lv->n_cells + 127) / 128;
+  return affine ? 10LL * lv->n_cells : n_tiles * 641 * 128;
+}
+
+int32_t dnnmg_level_geometry_tc(const dnnmg_level_t* lv, float* out, int32_t affine,
+                                dnnmg_stream_t s) {
+  return launch_k2tc_geometry(lv, out, affine, as_stream(s));
 }
 
 int32_t dnnmg_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t* ph, float* aT,

@@ -24,6 +24,8 @@
 // ascending cell id (the order of the reference's np.bincount, assembly.py:183),
 // so results are deterministic and independent of the launch configuration;
 // no float atomics are used.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 
@@ -682,9 +684,15 @@ static int32_t check_level(const dnnmg_level_t* lv, const char* who) {
   return DNNMG_OK;
 }
 
+int32_t launch_k2tc_elements(const dnnmg_level_t*, const float*, const float*, const float*,
+                             const dnnmg_phys_t*, int, float*, cudaStream_t);
+
 static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const float* aT,
                                const float* dT, const dnnmg_phys_t* ph, int mode, float* elem,
                                cudaStream_t s) {
+  // the tensor-core element kernel when its tables are present (residual_tc.cu)
+  if (lv->tc_const && lv->tc_geo && !getenv("DNNMG_K2_SIMT"))
+    return launch_k2tc_elements(lv, x, aT, dT, ph, mode == MODE_RHS ? 1 : 0, elem, s);
   ResidualArgs A;
   A.n_cells = lv->n_cells;
   A.cell_nodes = lv->cell_nodes;

@@ -237,6 +237,49 @@ def restrict_vector(hierarchy, b, level_fine, levels_down=1):
     return like_input(v, b)
 
 
+_K2TC_CONST = {}
+
+
+def k2tc_constants():
+    """The tensor-core K2 constant operand image (one per device, written once)."""
+    dev = torch.cuda.current_device()
+    if dev not in _K2TC_CONST:
+        n = int(_lib.load().dnnmg_k2tc_constants_bytes())
+        buf = torch.empty(n, dtype=torch.uint8, device=device())
+        _lib.call("dnnmg_k2tc_constants", ptr(buf), stream_handle())
+        _K2TC_CONST[dev] = buf
+    return _K2TC_CONST[dev]
+
+
+def geometry_kind(vertices, cells, rtol=1e-10, chunk=1 << 18):
+    """2 when every hexahedron is an axis-aligned box, 1 when every one is a parallelepiped
+    (x fastest corner order) -- their isoparametric maps are affine (the Q2 nodes of this mesh
+    code sit at the trilinear points), J is constant over the Gauss points and, for 2,
+    diagonal -- else 0 (e.g. a jittered mesh)."""
+    V = np.asarray(vertices, dtype=float)
+    C = np.asarray(cells)
+    kind = 2
+    for s in range(0, C.shape[0], chunk):
+        X = V[C[s:s + chunk]]
+        h = np.abs(X[:, 7] - X[:, 0]).max(axis=1, keepdims=True) + 1e-300
+        for axis, (e, pairs) in enumerate(((1, ((3, 2), (5, 4), (7, 6))), (2, ((3, 1), (6, 4), (7, 5))),
+                                           (4, ((5, 1), (6, 2), (7, 3))))):
+            d0 = X[:, e] - X[:, 0]
+            for a, b in pairs:
+                if np.any(np.abs(X[:, a] - X[:, b] - d0) > rtol * h):
+                    return 0
+            off = np.delete(d0, axis, axis=1)
+            if np.any(off != 0.0):
+                kind = 1
+    return kind
+
+
+def k2_tensor_cores():
+    """The tensor-core element kernel (csrc/residual_tc.cu) is opt-in (DNNMG_K2=tc): it is
+    parity-green but slower than the SIMT kernel on B200 (K2)."""
+    return os.environ.get("DNNMG_K2", "") == "tc"
+
+
 class DeviceLevel:
     """K2 tables of one level: cell nodes, fp64 coordinates, h_T, node->cell CSR."""
 
@@ -254,11 +297,36 @@ class DeviceLevel:
         self.csr_idx = upload(idx, np.int32)
         self.order = upload_opt(visit_order(p, idx))
         self.elem = None
+        self.geo_kind = geometry_kind(lvl.vertices, lvl.cells)
+        self.affine = self.geo_kind > 0
+        self.tc_geo = None
 
-    def struct(self, dof_mask=None, geometry=False):
-        return _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
-                          ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask),
-                          ptr(self.geometry()) if geometry else None, ptr(self.order))
+    def struct(self, dof_mask=None, geometry=False, tc=None):
+        """tc: use the tensor-core element kernel (default: DNNMG_K2=tc with the geometry
+        cache present)."""
+        tc = geometry and k2_tensor_cores() if tc is None else tc
+        lv = _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
+                        ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask),
+                        ptr(self.geometry()) if (geometry or tc) else None, ptr(self.order),
+                        None, None, 0)
+        if tc:
+            lv.tc_const = ptr(k2tc_constants())
+            lv.tc_geo = ptr(self.geometry_tc())
+            lv.tc_geo_affine = int(self.geo_kind)
+        return lv
+
+    def geometry_tc(self):
+        """The geometry in the tensor-core kernel's layout: per-cell affine records for an
+        affine mesh, else the per-point cache by 128-cell tiles."""
+        if self.tc_geo is None:
+            lv = _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
+                            ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), None,
+                            ptr(self.geometry()), None, None, None, 0)
+            n = int(_lib.load().dnnmg_level_geometry_tc_floats(ctypes.byref(lv), int(self.affine)))
+            self.tc_geo = torch.empty(max(n, 4), dtype=torch.float32, device=device())
+            _lib.call("dnnmg_level_geometry_tc", ctypes.byref(lv), ptr(self.tc_geo),
+                      int(self.affine), stream_handle())
+        return self.tc_geo
 
     def geometry(self):
         """Per-mesh cache of J^-1 and w at every (cell, Gauss point) (2,560 B per cell),

@@ -6,22 +6,38 @@
 // point q (64 per cell) the operator needs the values and reference gradients of the four
 // nodal fields (p, v) -- a contraction of the cell's 27 nodal values with the constant
 // tables N[q][a], dN_k[q][a] -- and returns the element vector by contracting 25
-// per-point coefficients with the same tables (and with T'_k = -PI^T dN_k, the projected
-// test of the local-projection terms).  Both contractions are GEMMs over a tile of 128
-// cells (one TMEM lane, one thread per cell):
+// per-point coefficients with the same tables and with T'_k = -PI^T dN_k, the projected
+// test of the local-projection terms.  Both contractions are GEMMs over a tile of 128
+// cells (TMEM lane = cell):
 //
 //   forward   D_f[cell][(q, kind)] = sum_a X_f[cell][a] BF[(q, kind)][a]     f = p, vx, vy, vz
-//   backward  E_c[cell][a] += sum_(q, arr) C_c[cell][(q, arr)] TB_c[a][(q, arr)]   c = 0..3
+//   backward  E_c[cell][a] += sum_(q, arr) C_c[cell][(q, arr)] TB[(q, arr)][a]   c = 0..3
 //
-// in the fp32-accurate 3-pass fp16 split (x = hi + lo; hi*hi + hi*lo + lo*hi, fp32
-// accumulation in TMEM).  Every cell's nodal values and every cell's coefficients are
-// scaled by a power of two before the split (exact; fp16 range) and unscaled after.
-// Comp 0 (continuity) uses arrays {A0, B0k} against {N, dN_k + T'_k}; comps 1..3 use
-// {A_c, B_ck, P_ck} against {N, dN_k, T'_k} (assembly.py:212-240, the element vector of
-// SURVEY App. B).  Per tile: 8 forward chunks of 8 Gauss points (double-buffered in TMEM,
-// 128 columns each) and 32 backward sub-chunks of 2 points (double-buffered coefficient
-// operands in shared memory, constant B tiles streamed by TMA through a 4-slot ring).
-// Warps 0-3: gather, scales, stab, pointwise, epilogue; warp 4: one thread issues the MMAs.
+// with TB[q] = [N, dN_0..2, T'_0..2, 0] for every component (comp 0 -- continuity -- uses
+// the coefficients {A0, B0k, B0k}: N A0 + (dN_k + T'_k) B0k, assembly.py:212-240).  The
+// fp32-accurate 3-pass fp16 split (x = hi + lo; hi*hi + hi*lo + lo*hi, fp32 accumulation in
+// TMEM); every cell's nodal values and coefficients are scaled by a power of two before the
+// split (exact, inside the fp16 range) and unscaled after.  The mass term (1/k)(v, phi),
+// which dominates A(x) and cancels in b - A(x), is applied exactly in fp32 on the CUDA cores
+// for the cell's reference mass det_ref (M1 x M1 x M1) v; the GEMM carries only
+// (w - det_ref w_hat) v / k (zero for affine cells).
+//
+// Pipeline (one persistent CTA per SM, 16 compute warps + 1 MMA warp).  Both GEMMs take their
+// A operand from TMEM: a shared-memory A operand costs its 4 KB per MMA at 128 B/cycle (39
+// cycles for an N = 16 MMA, tools/ubench/mma_issue.cu), a TMEM one runs at the N/2-cycle
+// floor (10 cycles).  TMEM columns: element vectors 128 | forward A 128 | forward results
+// 2 x 64 | backward A 128.
+//  * the constant operands (BF 32 KB, TB 64 KB) are loaded once per CTA by one bulk copy;
+//  * a tile's gather writes the forward A operand (4 fields, hi/lo, two fp16 per column) to
+//    TMEM; four threads per cell (one per warp group g) each own 8 of its nodes;
+//  * 16 stages of 4 Gauss points: the MMA warp runs the forward GEMM of stage s+2 (N = 16 per
+//    field) into one of two TMEM buffers while thread group g evaluates point q = 4s + g of
+//    its cell: forward values from TMEM, the pointwise physics, the split coefficients
+//    written to TMEM (tcgen05.st), then the backward GEMM of the stage (B = TB;
+//    [hi|lo] x [Bhi;Bhi] and [hi|lo] x [Blo;0], the K-duplicated Bhi by a zero leading byte
+//    offset) accumulates into the 4 x 32 element-vector columns;
+//  * epilogue: thread group c unscales component c, adds the exact mass term, and the tile's
+//    element vectors leave with one bulk (TMA) store.
 // Element vectors go to the same scratch as the SIMT kernel; the node sum (ascending cell
 // order, no atomics) is unchanged.
 #include <cstdlib>
@@ -33,35 +49,38 @@ namespace dnnmg {
 namespace k2tc {
 
 constexpr int kCells = 128;
-constexpr int kCompute = 2 * kCells;     // two threads per cell: one Gauss point each per sub-chunk
-constexpr int kThreads = kCompute + 32;
-constexpr int kMmaWarp = kCompute / 32;
-constexpr int kQF = 8;                       // Gauss points per forward chunk
-constexpr int kNChunks = 64 / kQF;           // 8
-constexpr int kQB = 2;                       // Gauss points per backward sub-chunk
-constexpr int kNSub = 64 / kQB;              // 32
-constexpr int kSubPerChunk = kQF / kQB;      // 4
-constexpr int kTBSlots = 8;         // constant B tiles in flight (TMA latency from L2)
-// constant operand image (global, built once by dnnmg_k2tc_constants)
-constexpr uint32_t kBFPart = 256 * 32 * 2;   // BF: 256 rows (q*4 + kind) x K 32 (nodes), fp16
-constexpr uint32_t kBFBytes = 2 * kBFPart;   // hi | lo
-constexpr uint32_t kTBPart = 32 * 16 * 2;    // TB: 32 rows (nodes) x K 16, fp16
-constexpr uint32_t kTBSub = 4 * kTBPart;     // TB0 hi | TB0 lo | TB1 hi | TB1 lo
-constexpr uint32_t kConstBytes = kBFBytes + kNSub * kTBSub;
+constexpr int kGroups = 4;                    // threads per cell (Gauss points per stage)
+constexpr int kCompute = kCells * kGroups;    // 512
+// + four MMA warps, one per SM sub-partition (a lone MMA warp gets a fifth of its
+// sub-partition's issue slots next to four busy compute warps: ~70 cycles per MMA): warps
+// 16, 17 issue the forward GEMMs of fields {0, 1}, {2, 3}, warps 18, 19 the backward GEMMs
+// of components {0, 1}, {2, 3}.  5 warps per sub-partition: at most 96 registers per thread
+constexpr int kThreads = kCompute + 128;
+constexpr int kMmaWarp = kCompute / 32;       // 16
+constexpr int kStages = 64 / kGroups;         // 16
+constexpr int kNodesPer = 8;                  // nodes per thread in the gather (8, 8, 8, 3)
+// constant operand image (global, built once by dnnmg_k2tc_constants; copied to smem as is)
+constexpr uint32_t kBFPart = 256 * 32 * 2;    // BF: 256 rows (q*4 + kind) x K 32 (nodes), fp16
+constexpr uint32_t oBF = 0;                   // hi | lo
+constexpr uint32_t oTB = 2 * kBFPart;         // per point q: Bhi [32 rows x 8] | Blo, 1 KB
+constexpr uint32_t kTBPoint = 1024;
+constexpr uint32_t oZero = oTB + 64 * kTBPoint;   // 512 zero bytes (the [Blo; 0] K half)
+constexpr uint32_t kConstBytes = oZero + 512;
 // shared memory (bytes)
-constexpr uint32_t kAFPart = kCells * 32 * 2;          // one field, one part: 128 x 32 fp16
-constexpr uint32_t kCPart = kCells * 16 * 2;           // one comp, one part: 128 x 16 fp16
-constexpr uint32_t kCBuf = 4 * 2 * kCPart;
-constexpr uint32_t oBF = 0;
-constexpr uint32_t oAF = oBF + kBFBytes;
-constexpr uint32_t oC = oAF + 4 * 2 * kAFPart;
-constexpr uint32_t oTB = oC + 2 * kCBuf;
-constexpr uint32_t oBar = oTB + kTBSlots * kTBSub;
-constexpr uint32_t kSmem = oBar + 256;
-static_assert(kCells * 27 * 16 <= 2 * kCBuf, "epilogue staging fits in the C buffers");
+constexpr uint32_t oStage = kConstBytes;                // next tile's nodal values [27][128] float4
+constexpr uint32_t oOut = oStage + kCells * 27 * 16;    // element-vector staging of a tile
+constexpr uint32_t kOutBytes = kCells * 27 * 16;
+constexpr uint32_t oV = oOut + kOutBytes;               // vertex values [8][128] float4
+constexpr uint32_t oMax = oV + 8 * kCells * 16;         // per-cell maxima, 2 buffers x [5][128]
+constexpr uint32_t oBar = oMax + 2 * 5 * kCells * 4;
+constexpr uint32_t kSmem = oBar + 128;
+static_assert(kSmem <= 232448, "shared memory");
+static_assert(oStage % 128 == 0 && oOut % 16 == 0 && oV % 16 == 0 && oBar % 8 == 0, "alignment");
 // TMEM columns
-constexpr uint32_t kColFwd = 0;      // two forward buffers of 128 columns (4 fields x 8 q x 4)
-constexpr uint32_t kColBwd = 256;    // 4 comps x 32 columns (27 nodes)
+constexpr uint32_t kColAcc = 0;      // 4 comps x 32 (27 nodes)
+constexpr uint32_t kColAF = 128;     // forward A: 4 fields x [hi | lo] x 16 (32 nodes, 2 per column)
+constexpr uint32_t kColFwd = 256;    // 2 buffers x (4 fields x 4 points x 4 kinds)
+constexpr uint32_t kColAB = 384;     // backward A: 4 points x 4 comps x [hi 4 | lo 4]
 
 __constant__ double kXg[4] = {0.06943184420297371, 0.33000947820757187, 0.6699905217924281,
                               0.9305681557970262};
@@ -119,27 +138,24 @@ __device__ void put_split(uint8_t* hi, uint8_t* lo, uint32_t off, double x) {
 }
 
 __global__ void constants_kernel(uint8_t* __restrict__ img) {
-  const int n_bf = 256 * 32, n_tb = kNSub * 2 * 32 * 16;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_bf + n_tb; i += gridDim.x * blockDim.x) {
+  const int n_bf = 256 * 32, n_tb = 64 * 32 * 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_bf + n_tb + 128;
+       i += gridDim.x * blockDim.x) {
     if (i < n_bf) {
       const int n = i / 32, a = i % 32;
       const double v = a < 27 ? basis(n >> 2, a, n & 3) : 0.0;
-      put_split(img, img + kBFPart, coff(n, a, 32), v);
-    } else {
+      put_split(img + oBF, img + oBF + kBFPart, coff(n, a, 32), v);
+    } else if (i < n_bf + n_tb) {
+      // TB[q]: rows a (32), K = arr (8): N, dN_0..2, T'_0..2, 0 -- one core-matrix column
       const int j = i - n_bf;
-      const int s = j / (2 * 32 * 16), t = (j / (32 * 16)) & 1, a = (j / 16) % 32, kk = j % 16;
+      const int q = j / 256, a = (j / 8) % 32, arr = j % 8;
       double v = 0.0;
-      if (a < 27) {
-        // K index kk = 8 ql + arr: one 16-byte core-matrix row per Gauss point
-        const int q = kQB * s + kk / 8, arr = kk % 8;
-        if (t == 0 && arr < 4) {          // comp 0: [N, dN_k + T'_k]
-          v = arr == 0 ? basis(q, a, 0) : basis(q, a, arr) + tprime(q, a, arr - 1);
-        } else if (t == 1 && arr < 7) {   // comps 1..3: [N, dN_k, T'_k]
-          v = arr == 0 ? basis(q, a, 0) : arr <= 3 ? basis(q, a, arr) : tprime(q, a, arr - 4);
-        }
-      }
-      uint8_t* base = img + kBFBytes + (size_t)s * kTBSub + (size_t)t * 2 * kTBPart;
-      put_split(base, base + kTBPart, coff(a, kk, 16), v);
+      if (a < 27 && arr < 7)
+        v = arr == 0 ? basis(q, a, 0) : arr <= 3 ? basis(q, a, arr) : tprime(q, a, arr - 4);
+      uint8_t* base = img + oTB + (size_t)q * kTBPoint;
+      put_split(base, base + 512, coff(a, arr, 8), v);
+    } else {
+      reinterpret_cast<uint32_t*>(img + oZero)[i - n_bf - n_tb] = 0u;
     }
   }
 }
@@ -192,10 +208,11 @@ struct Args {
   const uint8_t* cst;
   const float* geo;
   float4* elem;
-  int debug;   // timing experiments only (DNNMG_K2TC_DEBUG): 1 = issue no MMAs
-  unsigned long long* trace;   // DNNMG_K2TC_TRACE: clock64 stamps of CTA 0 (host buffer pointer)
+  unsigned long long* trace;   // DNNMG_K2TC_TRACE: clock64 stamps of CTA 0's first tiles
 };
-#define K2_TRACE(i) do { if (A.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0) A.trace[(i)] = clock64(); } while (0)
+// trace slots: [tile][stage][4]: forward warp 0 top / issued, backward warp 0 ready / issued
+#define K2_TRACE(slot) \
+  do { if (A.trace && blockIdx.x == 0) A.trace[(slot)] = clock64(); } while (0)
 
 __device__ __forceinline__ float frcp(float x) {
   float r;
@@ -203,35 +220,16 @@ __device__ __forceinline__ float frcp(float x) {
   return fmaf(fmaf(-x, r, 1.0f), r, r);
 }
 
-// 2^-e for the exponent e of m (m in [2^(e-1), 2^e)); 1 for m == 0
+// 2^-(e - bias) and 2^(e - bias) for the exponent e of m (m in [2^(e-1), 2^e)); e = 0 for
+// m == 0, subnormal or not finite (exponent-field arithmetic, no frexp/ldexp)
 __device__ __forceinline__ void pow2_scale(float m, int bias, float& s, float& inv) {
-  int e = 0;
-  if (m > 0.f && isfinite(m)) frexpf(m, &e);
-  e -= bias;
-  s = ldexpf(1.0f, -e);
-  inv = ldexpf(1.0f, e);
+  const int E = (int)((__float_as_uint(m) >> 23) & 0xFFu);
+  const int e = (E == 0 || E == 0xFF) ? -bias : E - 126 - bias;
+  s = __uint_as_float((uint32_t)(127 - e) << 23);
+  inv = __uint_as_float((uint32_t)(127 + e) << 23);
 }
 
-// one Gauss point's 8 K values (4 or 7 coefficients, zero-padded) of a row: one 16-byte
-// core-matrix row per part
-template <int N>
-__device__ __forceinline__ void store_q(uint8_t* hi, uint8_t* lo, int row, int ql, const float* v) {
-  uint4 h, l;
-  split_f16x2(v[0], v[1], h.x, l.x);
-  split_f16x2(v[2], v[3], h.y, l.y);
-  if constexpr (N > 4) {
-    split_f16x2(v[4], v[5], h.z, l.z);
-    split_f16x2(v[6], 0.f, h.w, l.w);
-  } else {
-    h.z = h.w = l.z = l.w = 0u;
-  }
-  const uint32_t off = coff(row, 8 * ql, 16);
-  *reinterpret_cast<uint4*>(hi + off) = h;
-  *reinterpret_cast<uint4*>(lo + off) = l;
-}
-
-// blocking wait that suspends the thread (try_wait with a time hint) instead of spinning,
-// so a waiting warp leaves its scheduler's issue slots to the others; bounded: traps
+// bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_sleep(uint32_t bar, uint32_t parity) {
   uint32_t n = 0;
   for (;;) {
@@ -248,19 +246,121 @@ __device__ __forceinline__ void mbar_sleep(uint32_t bar, uint32_t parity) {
   }
 }
 
-// non-blocking phase test: issued early, its result consumed after other work (the
-// SYNCS latency hides behind it)
-__device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
+// kind::f16 MMA with the A operand in TMEM, issued by the elected lane of a converged warp
+// (all lanes execute it; in divergent code the compiler wraps every MMA in a waterfall
+// loop); B descriptor passed as {lo, hi} 32-bit halves
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a_tmem, uint32_t b_lo,
+                                          uint32_t b_hi, uint32_t id, bool acc) {
   asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      "{\n\t.reg .b64 db;\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(id), "r"((uint32_t)acc)
       : "memory");
-  return ok;
 }
+// Grouped issue: one elect.sync per group, TMEM addresses and descriptor offsets as
+// immediates (only the descriptor bases come from registers).
+// backward, one Gauss point, two components: D_c += [hi|lo]_c x [Bhi;Bhi] + [hi|lo]_c x [Blo;0]
+template <uint32_t D0, uint32_t A0, uint32_t BH, uint32_t BL, uint32_t ACC>
+__device__ __forceinline__ void mma_bwd_point(uint32_t tb_lo, uint32_t hi, uint32_t id) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 l0, l1, d0, d1, a0, a1;\n\t.reg .b64 bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "add.u32 l0, %0, %3;\n\tadd.u32 l1, %0, %4;\n\t"
+      "mov.b64 bh, {l0, %1};\n\tmov.b64 bl, {l1, %1};\n\t"
+      "mov.u32 d0, %5;\n\tmov.u32 d1, %6;\n\tmov.u32 a0, %7;\n\tmov.u32 a1, %8;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d0], [a0], bh, %2, %9;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d0], [a0], bl, %2, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], [a1], bh, %2, %9;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], [a1], bl, %2, 1;\n\t}" ::"r"(tb_lo),
+      "r"(hi), "r"(id), "n"(BH), "n"(BL), "n"(D0), "n"(D0 + 32), "n"(A0), "n"(A0 + 8), "n"(ACC)
+      : "memory");
+}
+// forward, one field, one K step: D += Ahi Bhi + Ahi Blo + Alo Bhi
+template <uint32_t D, uint32_t AH, uint32_t AL, uint32_t BHI, uint32_t BLO, uint32_t ACC>
+__device__ __forceinline__ void mma_fwd_kstep(uint32_t bf_lo, uint32_t hi, uint32_t id) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 l0, l1, d, ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "add.u32 l0, %0, %3;\n\tadd.u32 l1, %0, %4;\n\t"
+      "mov.b64 bh, {l0, %1};\n\tmov.b64 bl, {l1, %1};\n\t"
+      "mov.u32 d, %5;\n\tmov.u32 ah, %6;\n\tmov.u32 al, %7;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d], [ah], bh, %2, %8;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d], [ah], bl, %2, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d], [al], bh, %2, 1;\n\t}" ::"r"(bf_lo),
+      "r"(hi), "r"(id), "n"(BHI), "n"(BLO), "n"(D), "n"(AH), "n"(AL), "n"(ACC)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
+}
+
+// barrier block (see the kernel): 0 constants, 1 forward A ready, 2-3 forward full, 4-5
+// forward free, 6 backward A full, 7 backward A free, 8 acc full, 9 acc free (the previous
+// tile's epilogue read it)
+constexpr uint32_t kTmem = 0;   // TMEM base (asserted in the kernel)
+constexpr uint32_t kIdF = idesc_for<DNNMG_PREC_F16X3>(16);
+constexpr uint32_t kIdB = idesc_for<DNNMG_PREC_F16X3>(32);
+constexpr uint32_t kHi512 = (512u >> 4) | (1u << 14);   // descriptor hi: SBO 512, version 1
+constexpr uint32_t kHi128 = (128u >> 4) | (1u << 14);   // SBO 128
+
+// forward GEMM of stage S for fields F0, F0+1 into buffer S & 1 (after every thread has read
+// chunk S - 2 from it)
+template <int S, int F0>
+__device__ __forceinline__ void fwd_stage(uint64_t* bars, uint32_t lo_bf, unsigned long long* tr) {
+  {
+    constexpr int buf = S & 1;
+    if (tr) tr[S * 4] = clock64();
+    mbar_sleep(smem_u32(&bars[4 + buf]), S < 2 ? 1u : (uint32_t)(((S - 2) >> 1) & 1));
+    tc_fence_after();
+#define FWD_KSTEP(f, ks)                                                                         \
+  mma_fwd_kstep<(kTmem + kColFwd + buf * 64 + (f) * 16), (kTmem + kColAF + ((f) * 2) * 16 + (ks) * 8), \
+                (kTmem + kColAF + ((f) * 2 + 1) * 16 + (ks) * 8), ((S * 1024 + (ks) * 256) >> 4),    \
+                ((kBFPart + S * 1024 + (ks) * 256) >> 4), ((ks) > 0 ? 1u : 0u)>(lo_bf, kHi512, kIdF)
+    FWD_KSTEP(F0, 0);
+    FWD_KSTEP(F0, 1);
+    FWD_KSTEP(F0 + 1, 0);
+    FWD_KSTEP(F0 + 1, 1);
+#undef FWD_KSTEP
+    tc_commit_elect(smem_u32(&bars[2 + buf]));
+    if (tr) tr[S * 4 + 1] = clock64();
+  }
+}
+
+// backward GEMM of stage S for components C0, C0+1 once its coefficients are in TMEM; TB
+// descriptors: [Bhi; Bhi] (LBO 0: both K halves read the hi block) and [Blo; 0] (LBO to the
+// zero block); 4 row groups of 8 nodes at SBO 128
+template <int S, int C0>
+__device__ __forceinline__ void bwd_stage(uint64_t* bars, uint32_t lo_tb, int it,
+                                          unsigned long long* tr) {
+  {
+    mbar_sleep(smem_u32(&bars[6]), S & 1);
+    if (S == 0) mbar_sleep(smem_u32(&bars[9]), it & 1);   // the previous tile's acc read
+    tc_fence_after();
+    if (tr) tr[S * 4 + 2] = clock64();
+#define BWD_POINT(j)                                                                            \
+  mma_bwd_point<(kTmem + kColAcc + C0 * 32), (kTmem + kColAB + (j) * 32 + C0 * 8),               \
+                (((kGroups * S + (j)) * kTBPoint) >> 4),                                        \
+                ((((kGroups * S + (j)) * kTBPoint + 512) >> 4) +                                \
+                    (((oZero - (oTB + (kGroups * S + (j)) * kTBPoint + 512)) >> 4) << 16)),     \
+                ((S > 0 || (j) > 0) ? 1u : 0u)>(lo_tb, kHi128, kIdB)
+    BWD_POINT(0);
+    BWD_POINT(1);
+    BWD_POINT(2);
+    BWD_POINT(3);
+#undef BWD_POINT
+    tc_commit_elect(smem_u32(&bars[7]));
+    if (tr) tr[S * 4 + 3] = clock64();
+  }
+}
+
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 
 // per-point coefficients (assembly.py:212-259; the SIMT kernel's pointwise phase):
 // F[f][m]: field f (p, vx, vy, vz), value (m = 0) and reference derivatives d/dxi_{m-1};
@@ -280,10 +380,38 @@ __device__ __forceinline__ float tr_k(float x0, float x1, float x2, const float 
   return Ji[k][0] * x0 + Ji[k][1] * x1 + Ji[k][2] * x2;
 }
 
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* w) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* w) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+      : "memory");
+}
+
+// one component's 8 coefficients -> its 8 TMEM words [hi(arr 0..7) | lo(arr 0..7)]
+__device__ __forceinline__ void store_comp(uint32_t* wv, float a0, float a1, float a2, float a3,
+                                           float a4, float a5, float a6) {
+  split_f16x2(a0, a1, wv[0], wv[4]);
+  split_f16x2(a2, a3, wv[1], wv[5]);
+  split_f16x2(a4, a5, wv[2], wv[6]);
+  split_f16x2(a6, 0.f, wv[3], wv[7]);
+}
+
+// per-point coefficients (assembly.py:212-259; the SIMT kernel's pointwise phase), split
+// into the 32 words of the backward A operand (4 components x [hi 4 | lo 4]):
+// F[f][m]: field f (p, vx, vy, vz), value (m = 0) and reference derivatives d/dxi_{m-1};
+// PQ: the same of the pi-projected (Q1) fields; Ji[k][j] = dxi_k/dx_j; w = w_hat det J
+// (times the cell's power-of-two scale); wm = w - det_ref w_hat: the mass term's weight
+// minus the cell's reference mass, which the epilogue applies exactly in fp32 (0 for affine
+// cells).  comp 0: {A0, B0k, B0k} against [N, dN_k, T'_k]; comp i: {A_i, B_ik, P_ik}.
 template <int MODE, int GEO>
-__device__ __forceinline__ void coefficients(const Args& A, const float F[4][4], const float PQ[4][4],
-                                             const float Ji[3][3], float w, float wm, float aT,
-                                             float dT, float c0[4], float cv[3][7]) {
+__device__ __forceinline__ void point_store(const Args& A, const float F[4][4], const float PQ[4][4],
+                                            const float Ji[3][3], float w, float wm, float aT,
+                                            float dT, uint32_t* wv) {
   float v[3], gv[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
@@ -298,56 +426,58 @@ __device__ __forceinline__ void coefficients(const Args& A, const float F[4][4],
     conv[i] = A.convection ? v[0] * gv[i][0] + v[1] * gv[i][1] + v[2] * gv[i][2] : 0.f;
   const float ik = A.ik;
   if constexpr (MODE == 0) {
-    const float p = F[0][0];
-    const float dd0 = F[0][1] - PQ[0][1], dd1 = F[0][2] - PQ[0][2], dd2 = F[0][3] - PQ[0][3];
-    float gdp[3];
+    {
+      const float dd0 = F[0][1] - PQ[0][1], dd1 = F[0][2] - PQ[0][2], dd2 = F[0][3] - PQ[0][3];
+      float E[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) gdp[j] = grad_j<GEO>(dd0, dd1, dd2, Ji, j);
+      for (int j = 0; j < 3; ++j) E[j] = aT * w * grad_j<GEO>(dd0, dd1, dd2, Ji, j);
+      const float b0 = tr_k<GEO>(E[0], E[1], E[2], Ji, 0);
+      const float b1 = tr_k<GEO>(E[0], E[1], E[2], Ji, 1);
+      const float b2 = tr_k<GEO>(E[0], E[1], E[2], Ji, 2);
+      // {A0, B00, B01, B02, B00, B01, B02, 0}: the duplicated words by byte permutes
+      split_f16x2(w * (gv[0][0] + gv[1][1] + gv[2][2]), b0, wv[0], wv[4]);
+      split_f16x2(b1, b2, wv[1], wv[5]);
+      wv[2] = __byte_perm(wv[0], wv[1], 0x5432);   // (B00, B01)
+      wv[6] = __byte_perm(wv[4], wv[5], 0x5432);
+      wv[3] = __byte_perm(wv[1], 0u, 0x5432);      // (B02, 0)
+      wv[7] = __byte_perm(wv[5], 0u, 0x5432);
+    }
+    const float p = F[0][0];
     const bool use_d = A.convection && dT != 0.f;
-    float g[3] = {0.f, 0.f, 0.f}, pvr[3] = {0.f, 0.f, 0.f};
+    float pvr[3] = {0.f, 0.f, 0.f};
     if (use_d) {
       const float pv0 = PQ[1][0], pv1 = PQ[2][0], pv2 = PQ[3][0];
 #pragma unroll
       for (int kk = 0; kk < 3; ++kk) pvr[kk] = tr_k<GEO>(pv0, pv1, pv2, Ji, kk);
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-        g[i] = conv[i] - (PQ[1 + i][1] * pvr[0] + PQ[1 + i][2] * pvr[1] + PQ[1 + i][3] * pvr[2]);
     }
-    const float div = gv[0][0] + gv[1][1] + gv[2][2];
-    float E[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) E[j] = aT * w * gdp[j];
-    c0[0] = w * div;
-#pragma unroll
-    for (int kk = 0; kk < 3; ++kk) c0[1 + kk] = tr_k<GEO>(E[0], E[1], E[2], Ji, kk);
     const float hn = 0.5f * A.nu * w;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      cv[i][0] = fmaf(wm * ik, v[i], w * 0.5f * conv[i]);
-      const float dg = dT * w * g[i];
-#pragma unroll
-      for (int kk = 0; kk < 3; ++kk) cv[i][4 + kk] = dg * pvr[kk];
+      const float gi = use_d ? conv[i] - (PQ[1 + i][1] * pvr[0] + PQ[1 + i][2] * pvr[1] +
+                                          PQ[1 + i][3] * pvr[2])
+                             : 0.f;
+      const float dg = dT * w * gi;
       float Fi[3];
 #pragma unroll
       for (int j = 0; j < 3; ++j) Fi[j] = hn * gv[i][j] + dg * v[j] - (i == j ? w * p : 0.f);
-#pragma unroll
-      for (int kk = 0; kk < 3; ++kk)
-        cv[i][1 + kk] = tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, kk);
+      store_comp(wv + 8 * (i + 1), fmaf(wm * ik, v[i], w * 0.5f * conv[i]),
+                 tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, 0), tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, 1),
+                 tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, 2), dg * pvr[0], dg * pvr[1], dg * pvr[2]);
     }
   } else {  // next-step RHS, f = None (assembly.py:242-259)
     const float hn = -0.5f * A.nu * w;
+    store_comp(wv, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int m = 0; m < 4; ++m) c0[m] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      cv[i][0] = fmaf(wm * ik, v[i], -w * 0.5f * conv[i]);
-#pragma unroll
-      for (int kk = 0; kk < 3; ++kk) {
-        cv[i][1 + kk] = hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, kk);
-        cv[i][4 + kk] = 0.f;
-      }
-    }
+    for (int i = 0; i < 3; ++i)
+      store_comp(wv + 8 * (i + 1), fmaf(wm * ik, v[i], -w * 0.5f * conv[i]),
+                 hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, 0),
+                 hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, 1),
+                 hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, 2), 0.f, 0.f, 0.f);
   }
+}
+
+__device__ __forceinline__ float comp4(const float4& v, int f) {
+  return f == 0 ? v.x : f == 1 ? v.y : f == 2 ? v.z : v.w;
 }
 
 template <int MODE, int GEO>   // GEO: 0 per-point geometry, 1 affine, 2 axis-aligned affine
@@ -356,32 +486,32 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + oBar);
-  uint64_t* b_bf = bars + 0;
-  uint64_t* b_afull = bars + 1;
-  uint64_t* b_fwdfull = bars + 2;   // [2]
-  uint64_t* b_fwdfree = bars + 4;   // [2]
-  uint64_t* b_cfull = bars + 6;     // [2]
-  uint64_t* b_cfree = bars + 8;     // [2]
-  uint64_t* b_tbfull = bars + 10;   // [kTBSlots]
-  uint64_t* b_tbfree = bars + 10 + kTBSlots;
-  uint64_t* b_bwd = bars + 10 + 2 * kTBSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11 + 2 * kTBSlots);
+  uint64_t* b_cst = bars + 0;
+  uint64_t* b_af = bars + 1;
+  uint64_t* b_fwd_full = bars + 2;   // [2]
+  uint64_t* b_fwd_free = bars + 4;   // [2]
+  uint64_t* b_ab_full = bars + 6;
+  uint64_t* b_ab_free = bars + 7;
+  uint64_t* b_acc_full = bars + 8;
+  uint64_t* b_acc_free = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  constexpr uint32_t kWarpsC = kCompute / 32;
   if (threadIdx.x == 0) {
-    mbar_init(smem_u32(b_bf), 1);
-    mbar_init(smem_u32(b_afull), kCompute);
+    mbar_init(smem_u32(b_cst), 1);
+    mbar_init(smem_u32(b_af), kWarpsC);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&b_fwdfull[i]), 1);
-      mbar_init(smem_u32(&b_fwdfree[i]), kCompute);
-      mbar_init(smem_u32(&b_cfull[i]), kCompute);
-      mbar_init(smem_u32(&b_cfree[i]), 1);
+      mbar_init(smem_u32(&b_fwd_full[i]), 2);
+      mbar_init(smem_u32(&b_fwd_free[i]), kWarpsC);
     }
-    for (int i = 0; i < kTBSlots; ++i) {
-      mbar_init(smem_u32(&b_tbfull[i]), 1);
-      mbar_init(smem_u32(&b_tbfree[i]), 1);
-    }
-    mbar_init(smem_u32(b_bwd), 1);
+    mbar_init(smem_u32(b_ab_full), kWarpsC);
+    mbar_init(smem_u32(b_ab_free), 2);
+    mbar_init(smem_u32(b_acc_full), 2);
+    mbar_init(smem_u32(b_acc_free), kWarpsC);
+
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = threadIdx.x; i < 2 * 5 * kCells; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem + oMax)[i] = 0u;
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot))
@@ -391,187 +521,194 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // the only CTA on the SM owns all 512 columns: the base is lane 0, column 0, so every TMEM
+  // address below is a compile-time constant (uniform MMA operands, no per-MMA waterfall)
+  constexpr uint32_t tmem = 0;
+  if (threadIdx.x == 0 && *tmem_slot != 0u) __trap();
   const int n_mine = blockIdx.x < A.n_tiles ? (A.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (warp == kMmaWarp) {
-    // ---------------- MMA warp: the whole warp runs the (fully unrolled) schedule with
-    // compile-time offsets and barrier parities; one elected lane issues every tcgen05 op
+  if (warp >= kMmaWarp) {
+    // ---------------- MMA warps: each whole warp runs its schedule (converged, uniform
+    // operands), elect.sync picks the lane that issues each tcgen05 op.  The 16 stages of a
+    // tile are unrolled: buffers, barrier parities (16 stages per tile, so they repeat per
+    // tile) and descriptor offsets are compile-time constants.  Forward warps: chunk s+2 as
+    // soon as every thread has read chunk s (its buffer); backward warps: the backward GEMM
+    // of stage s once its coefficients are in TMEM.
+    const int role = warp - kMmaWarp;
     if (n_mine > 0) {
-      const uint32_t total = (uint32_t)n_mine * kNSub;
-      auto tb_issue = [&](uint32_t g) {
-        if (lane == 0) {
-          const uint32_t slot = g % kTBSlots;
-          mbar_expect_tx(smem_u32(&b_tbfull[slot]), kTBSub);
-          bulk_g2s(smem_u32(smem + oTB + slot * kTBSub), A.cst + kBFBytes + (g % kNSub) * kTBSub,
-                   kTBSub, smem_u32(&b_tbfull[slot]));
-        }
-        __syncwarp();
-      };
-      if (lane == 0) {
-        mbar_expect_tx(smem_u32(b_bf), kBFBytes);
-        bulk_g2s(smem_u32(smem + oBF), A.cst, kBFBytes / 2, smem_u32(b_bf));
-        bulk_g2s(smem_u32(smem + oBF + kBFBytes / 2), A.cst + kBFBytes / 2, kBFBytes / 2,
-                 smem_u32(b_bf));
+      if (role == 0 && lane == 0) {
+        mbar_expect_tx(smem_u32(b_cst), kConstBytes);
+        bulk_g2s(smem_u32(smem), A.cst, kConstBytes, smem_u32(b_cst));
       }
-      for (uint32_t g = 0; g < kTBSlots && g < total; ++g) tb_issue(g);
-      mbar_sleep(smem_u32(b_bf), 0);
-      const uint32_t id = idesc_for<DNNMG_PREC_F16X3>(32);
-      // base descriptors; descriptor(base + off) = descriptor(base) + (off >> 4)
-      const uint64_t dBF = sdesc(smem_u32(smem + oBF), 512), dAF = sdesc(smem_u32(smem + oAF), 512);
-      const uint64_t dC = sdesc(smem_u32(smem + oC), 256), dTB = sdesc(smem_u32(smem + oTB), 256);
-      auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-        asm volatile(
-            "{\n\t.reg .pred e, p;\n\t"
-            "elect.sync _|e, 0xffffffff;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-            "l"(a), "l"(b), "r"(id), "r"(acc)
-            : "memory");
-      };
-      auto commit = [&](uint64_t* bar) {
-        asm volatile(
-            "{\n\t.reg .pred e;\n\t"
-            "elect.sync _|e, 0xffffffff;\n\t"
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-                smem_u32(bar))
-            : "memory");
-      };
-      auto fwd_issue = [&](int j) {  // forward chunk j of this tile -> buffer j & 1
-        const uint32_t buf = j & 1;
-        mbar_sleep(smem_u32(&b_fwdfree[buf]), ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-#pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          const uint32_t d = tmem + kColFwd + buf * 128 + f * 32;
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint32_t ko = ks * 256;
-            const uint64_t ahi = dAF + (((f * 2) * kAFPart + ko) >> 4);
-            const uint64_t alo = dAF + (((f * 2 + 1) * kAFPart + ko) >> 4);
-            const uint64_t bhi = dBF + ((j * 2048 + ko) >> 4);
-            const uint64_t blo = dBF + ((kBFPart + j * 2048 + ko) >> 4);
-            if (A.debug == 1) continue;
-            mma(d, ahi, bhi, ks > 0 ? 1u : 0u);
-            mma(d, ahi, blo, 1u);
-            mma(d, alo, bhi, 1u);
-          }
-        }
-        commit(&b_fwdfull[buf]);
-      };
-      for (int it = 0; it < n_mine; ++it) {
-        mbar_sleep(smem_u32(b_afull), it & 1);
-        tc_fence_after();
-        fwd_issue(0);
-        fwd_issue(1);
-#pragma unroll 1
-        for (int u = 0; u < kNSub / kTBSlots; ++u)
-#pragma unroll
-        for (int v = 0; v < kTBSlots; ++v) {
-          const int s = u * kTBSlots + v;
-          const int j = s / kSubPerChunk;
-          const uint32_t g = (uint32_t)it * kNSub + s;
-          const uint32_t cb = v & 1, slot = v;   // kNSub is a multiple of kTBSlots
-          // refill the TB slot sub-chunk g - 2 used (its MMAs are done: the compute warps
-          // waited for them before writing sub-chunk g) with sub-chunk g + kTBSlots - 2
-          if (g >= 2 && g + kTBSlots - 2 < total) {
-            mbar_sleep(smem_u32(&b_tbfree[(v + kTBSlots - 2) % kTBSlots]),
-                       (((g - 2) / kTBSlots) & 1));
-            tb_issue(g + kTBSlots - 2);
-          }
-          mbar_sleep(smem_u32(&b_cfull[cb]), (v >> 1) & 1);
-          if (g < 64) K2_TRACE(4 * g);
-          mbar_sleep(smem_u32(&b_tbfull[slot]), u & 1);
+      __syncwarp();
+      mbar_sleep(smem_u32(b_cst), 0);
+      // descriptor = {lo: start >> 4 | LBO >> 4 << 16, hi: SBO >> 4 | version}
+      const uint32_t s0 = smem_u32(smem) >> 4;
+      if (role < 2) {
+        const uint32_t lo_bf = s0 + (oBF >> 4) + ((128u >> 4) << 16);
+        for (int it = 0; it < n_mine; ++it) {
+          mbar_sleep(smem_u32(b_af), it & 1);
           tc_fence_after();
-          if (g < 64) K2_TRACE(4 * g + 1);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint32_t d = tmem + kColBwd + c * 32;
-            const uint32_t aoff = cb * kCBuf + (c * 2) * kCPart;
-            const uint32_t boff = slot * kTBSub + (c == 0 ? 0 : 2 * kTBPart);
-            const uint64_t ahi = dC + (aoff >> 4), alo = dC + ((aoff + kCPart) >> 4);
-            const uint64_t bhi = dTB + (boff >> 4), blo = dTB + ((boff + kTBPart) >> 4);
-            if (A.debug == 1) continue;
-            mma(d, ahi, bhi, s > 0 ? 1u : 0u);
-            mma(d, ahi, blo, 1u);
-            mma(d, alo, bhi, 1u);
-          }
-          commit(&b_cfree[cb]);
-          commit(&b_tbfree[slot]);
-          if (g < 64) K2_TRACE(4 * g + 2);
-          if (v % kSubPerChunk == kSubPerChunk - 1 && j + 2 < kNChunks) fwd_issue(j + 2);
+          unsigned long long* tr =
+              A.trace && blockIdx.x == 0 && it < 4 && role == 0 ? A.trace + it * kStages * 4 : nullptr;
+#define FWD(S)                                                                                   \
+  if (role == 0) fwd_stage<S, 0>(bars, lo_bf, tr);                                              \
+  else fwd_stage<S, 2>(bars, lo_bf, nullptr);
+          FWD(0) FWD(1) FWD(2) FWD(3) FWD(4) FWD(5) FWD(6) FWD(7)
+          FWD(8) FWD(9) FWD(10) FWD(11) FWD(12) FWD(13) FWD(14) FWD(15)
+#undef FWD
         }
-        commit(b_bwd);
+      } else {
+        const uint32_t lo_tb = s0 + (oTB >> 4);                         // LBO 0
+        for (int it = 0; it < n_mine; ++it) {
+          unsigned long long* tr = (role == 2 && A.trace && blockIdx.x == 0 && it < 4) ? A.trace + it * kStages * 4 : nullptr;
+#define BWD(S)                                                                                   \
+  if (role == 2) bwd_stage<S, 0>(bars, lo_tb, it, tr);                                          \
+  else bwd_stage<S, 2>(bars, lo_tb, it, nullptr);
+          BWD(0) BWD(1) BWD(2) BWD(3) BWD(4) BWD(5) BWD(6) BWD(7)
+          BWD(8) BWD(9) BWD(10) BWD(11) BWD(12) BWD(13) BWD(14) BWD(15)
+#undef BWD
+          tc_commit_elect(smem_u32(b_acc_full));
+        }
+
       }
     }
   } else {
-    // ---------------- compute warps: threads t and t + 128 <-> cell t (TMEM lane t) ----------
-    const int t = threadIdx.x & (kCells - 1);
-    const int half = threadIdx.x >> 7;          // Gauss point ql of every sub-chunk; fields / comps
-    const uint32_t lane_addr = (uint32_t)((warp & 3) * 32) << 16;
-    uint8_t* sAF = smem + oAF;
-    uint8_t* sC = smem + oC;
+    // ---------------- compute warps: cell row r = 32 (warp & 3) + lane, group g ----------------
+    const int wq = warp & 3, g = warp >> 2;
+    const int r = 32 * wq + lane;
+    const uint32_t lane_addr = (uint32_t)(32 * wq) << 16;
+    const float lx = kXgf[g];
+    float4* stg = reinterpret_cast<float4*>(smem + oStage);
+    float* outs = reinterpret_cast<float*>(smem + oOut) + r * 27 * 4 + g;
+    // this thread's 8 nodes of a tile into the staging array (cp.async; the indices first)
+    auto node_ids = [&](int64_t tile, int* nd) {
+      const int64_t cell = tile * kCells + r;
+#pragma unroll
+      for (int i = 0; i < kNodesPer; ++i) {
+        const int a = kNodesPer * g + i;
+        nd[i] = (cell < A.n_cells && a < 27) ? __ldg(A.cell_nodes + cell * 27 + a) : -1;
+      }
+    };
+    auto stage_nodes = [&](const int* nd) {
+#pragma unroll
+      for (int i = 0; i < kNodesPer; ++i) {
+        const int a = kNodesPer * g + i;
+        if (a < 27) {
+          if (nd[i] >= 0) cp_async16(stg + a * kCells + r, A.x + nd[i]);
+          else stg[a * kCells + r] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // element vectors of the previous tile: component g of row r from TMEM (unscaled), added in
+    // fp32 to its output image (which holds the mass term)
+    auto epilogue_ld = [&](int it_prev, float inv) {
+      mbar_sleep(smem_u32(b_acc_full), it_prev & 1);
+      tc_fence_after();
+      uint32_t rr[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]),
+            "=r"(rr[6]), "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]),
+            "=r"(rr[12]), "=r"(rr[13]), "=r"(rr[14]), "=r"(rr[15]), "=r"(rr[16]), "=r"(rr[17]),
+            "=r"(rr[18]), "=r"(rr[19]), "=r"(rr[20]), "=r"(rr[21]), "=r"(rr[22]), "=r"(rr[23]),
+            "=r"(rr[24]), "=r"(rr[25]), "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]), "=r"(rr[29]),
+            "=r"(rr[30]), "=r"(rr[31])
+          : "r"(tmem + lane_addr + kColAcc + g * 32));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int a = 0; a < 27; ++a) outs[4 * a] = fmaf(__uint_as_float(rr[a]), inv, outs[4 * a]);
+      fence_async_smem();   // this thread's staging writes before the bulk store reads them
+    };
+    auto epilogue_store = [&](int it_prev) {   // after a barrier: the tile's bulk store
+      if (threadIdx.x == 0) {
+        const int64_t c0 = (blockIdx.x + (int64_t)it_prev * gridDim.x) * kCells;
+        const int nv = (int)(A.n_cells - c0 < kCells ? A.n_cells - c0 : kCells);
+        bulk_s2g(A.elem + c0 * 27, smem_u32(smem + oOut), (uint32_t)nv * 27 * 16);
+      }
+    };
+    if (n_mine > 0) {
+      int nd[kNodesPer];
+      node_ids(blockIdx.x, nd);
+      stage_nodes(nd);
+    }
+    float invB_prev = 1.f;
     for (int it = 0; it < n_mine; ++it) {
       const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
-      const int64_t cell = tile * kCells + t;
+      const int64_t cell = tile * kCells + r;
       const bool valid = cell < A.n_cells;
-      // ---- gather, scales, stab; this thread's two fields of the forward operand rows ----
-      float4 V[8];           // vertex values (p, vx, vy, vz), vertex v = vx + 2 vy + 4 vz
-      float inv_f[4], aT = 0.f, dT = 0.f, sB = 1.f, invB = 1.f;
-      {
-        float4 X[27];
-#pragma unroll
-        for (int a = 0; a < 27; ++a)
-          X[a] = valid ? __ldg(A.x + __ldg(A.cell_nodes + cell * 27 + a)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float m[4] = {0.f, 0.f, 0.f, 0.f}, vsq = 0.f;
-#pragma unroll
-        for (int a = 0; a < 27; ++a) {
-          m[0] = fmaxf(m[0], fabsf(X[a].x));
-          m[1] = fmaxf(m[1], fabsf(X[a].y));
-          m[2] = fmaxf(m[2], fabsf(X[a].z));
-          m[3] = fmaxf(m[3], fabsf(X[a].w));
-          vsq = fmaxf(vsq, X[a].y * X[a].y + X[a].z * X[a].z + X[a].w * X[a].w);
+      // per-cell data (global loads issued first: their latency overlaps the staging wait)
+      float h = 1.f, aT = 0.f, dT = 0.f;
+      float Jc[3][3], det = 0.f;   // affine: J^-1, det J; else det = the reference mass det_ref
+      if (valid) {
+        h = __ldg(A.h_T + cell);
+        if (A.alpha_in) {
+          aT = A.alpha_in[cell];
+          dT = A.delta_in[cell];
         }
+      }
+      if constexpr (AFFINE) {
 #pragma unroll
-        for (int vz = 0; vz < 2; ++vz)
+        for (int k = 0; k < 9; ++k)
+          Jc[k / 3][k % 3] = (valid && (GEO == 1 || k % 4 == 0))
+                                 ? __ldg(A.geo + (int64_t)k * A.n_cells + cell) : 0.f;
+        det = valid ? __ldg(A.geo + (int64_t)9 * A.n_cells + cell) : 0.f;
+      } else {
+        det = __ldg(A.geo + (int64_t)A.n_tiles * 640 * kCells + tile * kCells + r);
+      }
+      // ---- this tile's nodal values (staged during the previous tile's stage 13) ----
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      bar_compute();
+      float4 X[kNodesPer];
 #pragma unroll
-          for (int vy = 0; vy < 2; ++vy)
+      for (int i = 0; i < kNodesPer; ++i) {
+        const int a = kNodesPer * g + i;
+        X[i] = a < 27 ? stg[a * kCells + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      uint32_t* mx = reinterpret_cast<uint32_t*>(smem + oMax) + (it & 1) * 5 * kCells + r;
+      {
+        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int vx = 0; vx < 2; ++vx) V[vx + 2 * vy + 4 * vz] = X[2 * vx + 6 * vy + 18 * vz];
-        float sf[4];
+        for (int i = 0; i < kNodesPer; ++i) {
+          m[0] = fmaxf(m[0], fabsf(X[i].x));
+          m[1] = fmaxf(m[1], fabsf(X[i].y));
+          m[2] = fmaxf(m[2], fabsf(X[i].z));
+          m[3] = fmaxf(m[3], fabsf(X[i].w));
+          m[4] = fmaxf(m[4], X[i].y * X[i].y + X[i].z * X[i].z + X[i].w * X[i].w);
+        }
+        // non-negative floats order like their bit patterns: the cell's maxima by shared
+        // integer atomics (order-independent, deterministic)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) atomicMax(mx + k * kCells, __float_as_uint(m[k]));
+        float4* vt = reinterpret_cast<float4*>(smem + oV);
+#pragma unroll
+        for (int i = 0; i < kNodesPer; ++i) {
+          const int a = kNodesPer * g + i;
+          const int ax = a % 3, ay = (a / 3) % 3, az = a / 9;
+          if (a < 27 && ax != 1 && ay != 1 && az != 1)
+            vt[((ax >> 1) + 2 * (ay >> 1) + 4 * (az >> 1)) * kCells + r] = X[i];
+        }
+      }
+      bar_compute();
+      // ---- per-cell scales, stabilisation weights ----
+      float sf[4], inv_f[4], sB = 1.f, invB = 1.f;
+      {
+        float m[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) m[k] = __uint_as_float(mx[k * kCells]);
+        if (g == 0) {   // reset the other buffer for the next tile (read during the last one)
+          uint32_t* mo = reinterpret_cast<uint32_t*>(smem + oMax) + ((it + 1) & 1) * 5 * kCells + r;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) mo[k * kCells] = 0u;
+        }
 #pragma unroll
         for (int f = 0; f < 4; ++f) pow2_scale(m[f], 0, sf[f], inv_f[f]);
-#pragma unroll
-        for (int ff = 0; ff < 2; ++ff) {
-          const int f = 2 * half + ff;
-          float v[32];
-#pragma unroll
-          for (int a = 0; a < 32; ++a) {
-            const float x = a < 27 ? (ff == 0 ? (half ? X[a].z : X[a].x) : (half ? X[a].w : X[a].y)) : 0.f;
-            v[a] = x * sf[f];
-          }
-          uint8_t* hi = sAF + (f * 2) * kAFPart;
-          uint8_t* lo = hi + kAFPart;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            uint4 h, l;
-            split_f16x2(v[8 * g + 0], v[8 * g + 1], h.x, l.x);
-            split_f16x2(v[8 * g + 2], v[8 * g + 3], h.y, l.y);
-            split_f16x2(v[8 * g + 4], v[8 * g + 5], h.z, l.z);
-            split_f16x2(v[8 * g + 6], v[8 * g + 7], h.w, l.w);
-            const uint32_t off = coff(t, 8 * g, 32);
-            *reinterpret_cast<uint4*>(hi + off) = h;
-            *reinterpret_cast<uint4*>(lo + off) = l;
-          }
-        }
         if (valid) {
-          const float vmax = sqrtf(vsq);
-          const float h = __ldg(A.h_T + cell);
-          if (A.alpha_in) {
-            aT = A.alpha_in[cell];
-            dT = A.delta_in[cell];
-          } else {  // stab at x (assembly.py:55-59, 169-178)
-            const float ih = frcp(h);
+          const float vmax = sqrtf(m[4]);
+          const float ih = frcp(h);
+          if (!A.alpha_in) {  // stab at x (assembly.py:55-59, 169-178)
             const float rden = frcp(fmaf(A.nu * ih, ih, fmaf(vmax, ih, A.ik)));
             aT = A.alpha0 * rden;
             dT = A.delta0 * rden;
@@ -579,193 +716,185 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
           // power-of-two scale of the coefficients: a generous bound of their size
           // (w <= 0.035 h^3; |grad v| ~ vmax / h) placed near 2^8 of the fp16 range
           const float bound = 0.035f * h * h * h * (vmax + m[0] + 1e-30f) * (1.f + vmax) *
-                              (A.ik + (vmax + A.nu + 1.f) / h + A.nu / (h * h) + 1.f);
+                              (A.ik + (vmax + A.nu + 1.f) * ih + A.nu * ih * ih + 1.f);
           pow2_scale(bound, 8, sB, invB);
         }
       }
-      float Jc[3][3], det = 0.f;   // affine: J^-1, det J; else det = the reference mass det_ref
-      if constexpr (AFFINE) {
+      // ---- forward A operand in TMEM: nodes 8g..8g+7 of row r, per field and part (the
+      // previous tile's forward MMAs, its last readers, completed before its last stage) ----
 #pragma unroll
-        for (int k = 0; k < 9; ++k) Jc[k / 3][k % 3] = valid ? __ldg(A.geo + (int64_t)k * A.n_cells + cell) : 0.f;
-        det = valid ? __ldg(A.geo + (int64_t)9 * A.n_cells + cell) : 0.f;
-      } else {
-        det = __ldg(A.geo + (int64_t)A.n_tiles * 640 * kCells + cell);
+      for (int f = 0; f < 4; ++f) {
+        uint32_t hh[4], ll[4];
+        split_f16x2(comp4(X[0], f) * sf[f], comp4(X[1], f) * sf[f], hh[0], ll[0]);
+        split_f16x2(comp4(X[2], f) * sf[f], comp4(X[3], f) * sf[f], hh[1], ll[1]);
+        split_f16x2(comp4(X[4], f) * sf[f], comp4(X[5], f) * sf[f], hh[2], ll[2]);
+        split_f16x2(comp4(X[6], f) * sf[f], comp4(X[7], f) * sf[f], hh[3], ll[3]);
+        tmem_st4(tmem + lane_addr + kColAF + (f * 2) * 16 + g * 4, hh);
+        tmem_st4(tmem + lane_addr + kColAF + (f * 2 + 1) * 16 + g * 4, ll);
       }
-      fence_async_smem();
-      mbar_arrive(smem_u32(b_afull));
-      // ---- forward chunks -> pointwise -> backward operand sub-chunks ----
-      uint32_t fwd_ok = 0;
-      for (int j = 0; j < kNChunks; ++j) {
-        const uint32_t G = (uint32_t)it * kNChunks + j;
-        const uint32_t buf = G & 1;
-        if (!(j > 0 && fwd_ok)) mbar_sleep(smem_u32(&b_fwdfull[buf]), (G >> 1) & 1);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(b_af));
+      // ---- the previous tile's element vectors and their bulk store (overlapping this tile's
+      // first forward GEMMs) ----
+      if (it > 0) {
+        epilogue_ld(it - 1, invB_prev);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(b_acc_free));
+        bar_compute();
+        epilogue_store(it - 1);
+      } else if (lane == 0) {
+        mbar_arrive(smem_u32(b_acc_free));
+      }
+      invB_prev = invB;
+      // ---- 16 stages: Gauss point q = 4 s + g ----
+      auto stage = [&](int s, bool wait_store) {
+        const uint32_t b = s & 1, par = (s >> 1) & 1;   // 16 stages per tile
+        const int q = kGroups * s + g;
+        float Ji[3][3], w;
+        if constexpr (AFFINE) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) Ji[k][jj] = Jc[k][jj];
+          w = kWq[q] * det;
+        } else {
+          const float* gq = A.geo + (tile * 640 + q) * kCells + r;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) Ji[k / 3][k % 3] = __ldg(gq + (int64_t)k * 64 * kCells);
+          w = __ldg(gq + (int64_t)9 * 64 * kCells);
+        }
+        // forward values of this point
+        mbar_sleep(smem_u32(&b_fwd_full[b]), par);
         tc_fence_after();
-        for (int sub = 0; sub < kSubPerChunk; ++sub) {
-          const uint32_t g = (uint32_t)it * kNSub + j * kSubPerChunk + sub;
-          const uint32_t cb = g & 1;
-          // early phase tests (results consumed after the pointwise work)
-          const uint32_t c_ok = mbar_test(smem_u32(&b_cfree[cb]), ((g >> 1) & 1) ^ 1);
-          if (sub == kSubPerChunk - 1 && j + 1 < kNChunks)
-            fwd_ok = mbar_test(smem_u32(&b_fwdfull[(G + 1) & 1]), ((G + 1) >> 1) & 1);
-          const int q = j * kQF + sub * kQB + half;
-          const int qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
-          float F[4][4];
+        float F[4][4];
+        {
+          uint32_t rr[4][4];
 #pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            float r4[4];
-            uint32_t rr[4];
+          for (int f = 0; f < 4; ++f)
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3])
-                         : "r"(tmem + lane_addr + kColFwd + buf * 128 + f * 32 + sub * 8 + half * 4));
-#pragma unroll
-            for (int m = 0; m < 4; ++m) r4[m] = __uint_as_float(rr[m]);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) F[f][m] = r4[m];
-          }
+                         : "=r"(rr[f][0]), "=r"(rr[f][1]), "=r"(rr[f][2]), "=r"(rr[f][3])
+                         : "r"(tmem + lane_addr + kColFwd + b * 64 + f * 16 + g * 4));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int f = 0; f < 4; ++f)
 #pragma unroll
-            for (int m = 0; m < 4; ++m) F[f][m] *= inv_f[f];
-          // pi-projected fields: trilinear in the 8 vertex values (elements.py:96-118)
-          float PQ[4][4];
-          {
-            const float lx = kXgf[qx], ly = kXgf[qy], lz = kXgf[qz];
+            for (int m = 0; m < 4; ++m) F[f][m] = __uint_as_float(rr[f][m]) * inv_f[f];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&b_fwd_free[b]));
+        // pi-projected fields: trilinear in the 8 vertex values (elements.py:96-118), read
+        // from shared memory per stage (in registers they would push the thread past its
+        // 96-register budget)
+        float PQ[4][4];
+        {
+          float4 V[8];
+          const float4* vt = reinterpret_cast<const float4*>(smem + oV) + r;
 #pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              float a2[2][2], ax[2][2];
+          for (int v = 0; v < 8; ++v) V[v] = vt[v * kCells];
+          const float ly = kXgf[s & 3], lz = kXgf[s >> 2];
 #pragma unroll
-              for (int vz = 0; vz < 2; ++vz)
+          for (int f = 0; f < 4; ++f) {
+            float a2[2][2], ax[2][2];
 #pragma unroll
-                for (int vy = 0; vy < 2; ++vy) {
-                  const float4 v0 = V[4 * vz + 2 * vy], v1 = V[4 * vz + 2 * vy + 1];
-                  const float g0 = f == 0 ? v0.x : f == 1 ? v0.y : f == 2 ? v0.z : v0.w;
-                  const float g1 = f == 0 ? v1.x : f == 1 ? v1.y : f == 2 ? v1.z : v1.w;
-                  a2[vz][vy] = fmaf(lx, g1 - g0, g0);
-                  ax[vz][vy] = g1 - g0;
-                }
-              float b[2], bx[2], by[2];
+            for (int vz = 0; vz < 2; ++vz)
 #pragma unroll
-              for (int vz = 0; vz < 2; ++vz) {
-                b[vz] = fmaf(ly, a2[vz][1] - a2[vz][0], a2[vz][0]);
-                bx[vz] = fmaf(ly, ax[vz][1] - ax[vz][0], ax[vz][0]);
-                by[vz] = a2[vz][1] - a2[vz][0];
+              for (int vy = 0; vy < 2; ++vy) {
+                const float g0 = comp4(V[4 * vz + 2 * vy], f), g1 = comp4(V[4 * vz + 2 * vy + 1], f);
+                a2[vz][vy] = fmaf(lx, g1 - g0, g0);
+                ax[vz][vy] = g1 - g0;
               }
-              PQ[f][0] = fmaf(lz, b[1] - b[0], b[0]);
-              PQ[f][1] = fmaf(lz, bx[1] - bx[0], bx[0]);
-              PQ[f][2] = fmaf(lz, by[1] - by[0], by[0]);
-              PQ[f][3] = b[1] - b[0];
+            float bb[2], bx[2], by[2];
+#pragma unroll
+            for (int vz = 0; vz < 2; ++vz) {
+              bb[vz] = fmaf(ly, a2[vz][1] - a2[vz][0], a2[vz][0]);
+              bx[vz] = fmaf(ly, ax[vz][1] - ax[vz][0], ax[vz][0]);
+              by[vz] = a2[vz][1] - a2[vz][0];
             }
+            PQ[f][0] = fmaf(lz, bb[1] - bb[0], bb[0]);
+            PQ[f][1] = fmaf(lz, bx[1] - bx[0], bx[0]);
+            PQ[f][2] = fmaf(lz, by[1] - by[0], by[0]);
+            PQ[f][3] = bb[1] - bb[0];
           }
-          float Ji[3][3], w;
-          if constexpr (AFFINE) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-#pragma unroll
-              for (int jj = 0; jj < 3; ++jj) Ji[k][jj] = Jc[k][jj];
-            w = kWq[q] * det;
-          } else {
-            const float* gq = A.geo + (tile * 640 + q) * kCells + t;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) Ji[k / 3][k % 3] = __ldg(gq + (int64_t)k * 64 * kCells);
-            w = __ldg(gq + (int64_t)9 * 64 * kCells);
-          }
-          float c0[4], cv[3][7];
-          if (A.debug == 2) {   // timing experiment: no pointwise work
-#pragma unroll
-            for (int m = 0; m < 4; ++m) c0[m] = F[m][0];
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-              for (int m = 0; m < 7; ++m) cv[i][m] = PQ[i][m & 3] + Ji[i][m % 3] + w;
-          } else {
-            coefficients<MODE, GEO>(A, F, PQ, Ji, w * sB, (w - kWq[q] * det) * sB, aT, dT, c0, cv);
-          }
-          // this Gauss point's coefficient rows -> C buffer cb once its previous MMAs are done
-          if (threadIdx.x == 0 && g < 64) K2_TRACE(256 + 2 * g);
-          if (!c_ok) mbar_sleep(smem_u32(&b_cfree[cb]), ((g >> 1) & 1) ^ 1);
-          if (threadIdx.x == 0 && g < 64) K2_TRACE(256 + 2 * g + 1);
-          uint8_t* base = sC + cb * kCBuf;
-          store_q<4>(base + 0 * kCPart, base + 1 * kCPart, t, half, c0);
-          store_q<7>(base + 2 * kCPart, base + 3 * kCPart, t, half, cv[0]);
-          store_q<7>(base + 4 * kCPart, base + 5 * kCPart, t, half, cv[1]);
-          store_q<7>(base + 6 * kCPart, base + 7 * kCPart, t, half, cv[2]);
-          fence_async_smem();
-          mbar_arrive(smem_u32(&b_cfull[cb]));
-          if (threadIdx.x == 0 && g < 64) K2_TRACE(4 * g + 3);
         }
+        uint32_t wv[32];
+        point_store<MODE, GEO>(A, F, PQ, Ji, w * sB, (w - kWq[q] * det) * sB, aT, dT, wv);
+        // the backward A operand is free once the previous stage's MMAs have completed
+        mbar_sleep(smem_u32(b_ab_free), (s & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_st8(tmem + lane_addr + kColAB + g * 32 + 8 * c, wv + 8 * c);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
-        mbar_arrive(smem_u32(&b_fwdfree[buf]));
-      }
-      // ---- epilogue: element vectors (unscaled) staged in the C buffers, one coalesced copy ----
-      mbar_sleep(smem_u32(b_bwd), it & 1);
-      tc_fence_after();
-      float* stage = reinterpret_cast<float*>(sC);
-      {
-        float e[2][32];   // comps 2 half, 2 half + 1
+        // stage 0: the previous tile's bulk store has read the output staging before this
+        // thread's arrival (stage 1 rewrites it once every thread has passed this stage)
+        if (wait_store && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(b_ab_full));
+      };
+      // this tile's output image starts as the reference mass term, exact in fp32:
+      // (det_ref / k) (M1 x M1 x M1) v_g, sum-factorised over the 1-D Q2 mass matrix (the GEMM
+      // carries only w - det_ref w_hat; the tensor core's fp32 accumulation rounds its partial
+      // sums, so the dominant term stays out of the accumulator; through the GEMM the golden
+      // cases' r errors are 1.6-4.5e-5).  Written after stage 1: every thread has passed stage
+      // 0, so the previous tile's store has read the output staging.  (Staggering the groups
+      // over stages 2-4 was slower: every stage's backward GEMM waits for all warps.)
+      auto mass_image = [&]() {
+        if (g >= 1) {
+          const float mk = det * A.ik;
+          float uu[27], y[27];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * half + cc;
-          tmem_ld16(tmem + lane_addr + kColBwd + c * 32, e[cc]);
-          tmem_ld16(tmem + lane_addr + kColBwd + c * 32 + 16, e[cc] + 16);
-        }
-        tc_fence_before();
-        asm volatile("bar.sync 1, 256;" ::: "memory");   // every MMA of this tile has completed
-        // the reference mass term, exact in fp32: (det_ref / k) (M1 x M1 x M1) v_i, sum-factorised
-        // over the 1-D Q2 mass matrix (the GEMM carried only w - det_ref w_hat)
-        const float mk = det * A.ik;
+          for (int a = 0; a < 27; ++a) uu[a] = comp4(stg[a * kCells + r], g);
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * half + cc;
-#pragma unroll
-          for (int a = 0; a < 27; ++a) e[cc][a] *= invB;
-          if (c >= 1) {
-            float u[27], y[27];
-#pragma unroll
-            for (int a = 0; a < 27; ++a) {
-              const float4 xv = valid ? __ldg(A.x + __ldg(A.cell_nodes + cell * 27 + a))
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-              u[a] = c == 1 ? xv.y : c == 2 ? xv.z : xv.w;
-            }
-#pragma unroll
-            for (int a = 0; a < 27; ++a) {   // x
-              const int ax = a % 3, r = a - ax;
-              y[a] = fmaf(kM1[ax][2], u[r + 2], fmaf(kM1[ax][1], u[r + 1], kM1[ax][0] * u[r]));
-            }
-#pragma unroll
-            for (int a = 0; a < 27; ++a) {   // y
-              const int ay = (a / 3) % 3, r = a - 3 * ay;
-              u[a] = fmaf(kM1[ay][2], y[r + 6], fmaf(kM1[ay][1], y[r + 3], kM1[ay][0] * y[r]));
-            }
-#pragma unroll
-            for (int a = 0; a < 27; ++a) {   // z
-              const int az = a / 9, r = a - 9 * az;
-              y[a] = fmaf(kM1[az][2], u[r + 18], fmaf(kM1[az][1], u[r + 9], kM1[az][0] * u[r]));
-            }
-#pragma unroll
-            for (int a = 0; a < 27; ++a) e[cc][a] = fmaf(mk, y[a], e[cc][a]);
+          for (int a = 0; a < 27; ++a) {   // x
+            const int ax = a % 3, rb = a - ax;
+            y[a] = fmaf(kM1[ax][2], uu[rb + 2], fmaf(kM1[ax][1], uu[rb + 1], kM1[ax][0] * uu[rb]));
           }
-        }
 #pragma unroll
-        for (int a = 0; a < 27; ++a)
-          *reinterpret_cast<float2*>(stage + 4 * (t * 27 + a) + 2 * half) = make_float2(e[0][a], e[1][a]);
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      {
-        const int64_t c0 = tile * kCells;
-        const int nv = (int)(A.n_cells - c0 < kCells ? A.n_cells - c0 : kCells);
-        float4* dst = A.elem + c0 * 27;
-        const float4* st4 = reinterpret_cast<const float4*>(stage);
-        for (int i = threadIdx.x; i < nv * 27; i += kCompute) dst[i] = st4[i];
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+          for (int a = 0; a < 27; ++a) {   // y
+            const int ay = (a / 3) % 3, rb = a - 3 * ay;
+            uu[a] = fmaf(kM1[ay][2], y[rb + 6], fmaf(kM1[ay][1], y[rb + 3], kM1[ay][0] * y[rb]));
+          }
+#pragma unroll
+          for (int a = 0; a < 27; ++a) {   // z
+            const int az = a / 9, rb = a - 9 * az;
+            outs[4 * a] = mk * fmaf(kM1[az][2], uu[rb + 18], fmaf(kM1[az][1], uu[rb + 9], kM1[az][0] * uu[rb]));
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < 27; ++a) outs[4 * a] = 0.f;
+        }
+      };
+      stage(0, true);
+      stage(1, false);
+      // the next tile's node indices (their load latency overlaps the mass term; the rows are
+      // copied once this tile's staged values are consumed)
+      const bool pf = it + 1 < n_mine;
+      int ndn[kNodesPer];
+      if (pf) node_ids(tile + gridDim.x, ndn);
+      mass_image();
+      bar_compute();   // every thread's mass term has read the staged values
+      if (pf) stage_nodes(ndn);
+      for (int s = 2; s < kStages; ++s) stage(s, false);
+
+
     }
+    // the last tile's element vectors
+    if (n_mine > 0) {
+      epilogue_ld(n_mine - 1, invB_prev);
+      bar_compute();
+      epilogue_store(n_mine - 1);
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot) : "memory");
   }
 }
 
@@ -796,6 +925,8 @@ int32_t launch_k2tc_elements(const dnnmg_level_t* lv, const float* x, const floa
                              const float* dT, const dnnmg_phys_t* ph, int mode, float* elem,
                              cudaStream_t s) {
   using namespace k2tc;
+  DNNMG_REQUIRE(((uintptr_t)elem & 15) == 0 && ((uintptr_t)lv->tc_const & 15) == 0, DNNMG_ERR_ARG,
+                "residual (tensor cores): unaligned element scratch or constant image");
   Args A;
   A.n_cells = lv->n_cells;
   A.n_tiles = (lv->n_cells + kCells - 1) / kCells;
@@ -813,15 +944,11 @@ int32_t launch_k2tc_elements(const dnnmg_level_t* lv, const float* x, const floa
   A.cst = static_cast<const uint8_t*>(lv->tc_const);
   A.geo = lv->tc_geo;
   A.elem = reinterpret_cast<float4*>(elem);
-  {
-    const char* dbg = getenv("DNNMG_K2TC_DEBUG");
-    A.debug = dbg ? atoi(dbg) : 0;
-    static unsigned long long* tr = nullptr;
-    A.trace = nullptr;
-    if (getenv("DNNMG_K2TC_TRACE")) {
-      if (!tr) cudaMallocManaged(&tr, 512 * sizeof(unsigned long long));
-      A.trace = tr;
-    }
+  A.trace = nullptr;
+  static unsigned long long* trace_buf = nullptr;
+  if (getenv("DNNMG_K2TC_TRACE")) {   // diagnostic timeline (tools/gpu/k2_trace.py)
+    if (!trace_buf) cudaMallocManaged(&trace_buf, 8192 * sizeof(unsigned long long));
+    A.trace = trace_buf;
   }
   if (lv->n_cells == 0) return DNNMG_OK;
   static uint64_t configured = 0;
@@ -843,17 +970,16 @@ int32_t launch_k2tc_elements(const dnnmg_level_t* lv, const float* x, const floa
   auto kern = mode == 0 ? (geo == 2 ? k2tc_kernel<0, 2> : geo == 1 ? k2tc_kernel<0, 1> : k2tc_kernel<0, 0>)
                         : (geo == 2 ? k2tc_kernel<1, 2> : geo == 1 ? k2tc_kernel<1, 1> : k2tc_kernel<1, 0>);
   kern<<<grid, kThreads, kSmem, s>>>(A);
-  if (A.trace) {   // debug timeline (DNNMG_K2TC_TRACE): synchronous, printed to stderr
+  DNNMG_CHECK_LAUNCH("k2tc_kernel");
+  if (A.trace) {   // synchronous dump to stderr: per stage, cycles from the first stamp
     cudaStreamSynchronize(s);
     const unsigned long long t0 = A.trace[0];
-    fprintf(stderr, "g  cfull_acq  issue  commit | thr0: stored  cfree_test  cfree_done\n");
-    for (int g = 0; g < 64; ++g)
-      fprintf(stderr, "%2d %8lld %8lld %8lld | %8lld %8lld %8lld\n", g,
-              (long long)(A.trace[4 * g] - t0), (long long)(A.trace[4 * g + 1] - t0),
-              (long long)(A.trace[4 * g + 2] - t0), (long long)(A.trace[4 * g + 3] - t0),
-              (long long)(A.trace[256 + 2 * g] - t0), (long long)(A.trace[256 + 2 * g + 1] - t0));
+    auto rel = [&](int i) { return (long long)(A.trace[i] - t0); };
+    fprintf(stderr, "it s | fwd warp 0: top issued | bwd warp 0: ab_full_ok issued\n");
+    for (int i = 0; i < 4 * kStages; ++i)
+      fprintf(stderr, "%d %2d | %7lld %7lld | %7lld %7lld\n", i / kStages, i % kStages, rel(4 * i),
+              rel(4 * i + 1), rel(4 * i + 2), rel(4 * i + 3));
   }
-  DNNMG_CHECK_LAUNCH("k2tc_kernel");
   return DNNMG_OK;
 }
 

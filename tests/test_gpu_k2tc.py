@@ -82,3 +82,35 @@ def test_k2tc_layout_choice():
         h = product_hierarchy(g)
         lvl = dv.DeviceLevel.get(spmod.FeSpace(h, int(g["L"]) + int(g["J"])))
         assert lvl.affine == want, name
+
+
+@pytest.mark.parametrize("jitter", [False, True])
+def test_k2tc_multi_tile(jitter):
+    """Several 128-cell tiles per CTA (the next tile's nodes are prefetched during the stages,
+    the previous tile's element vectors leave during the next tile's first stages) on a
+    16x16x16 box (32,768 fine cells, 256 tiles on at most 148 CTAs): the tensor-core element
+    kernel matches the SIMT one to fp32 rounding and repeats bit for bit."""
+    from paper_2307_14837_b200 import mesh as meshmod, synthetic
+    n = (16, 16, 16)
+    h = meshmod.build_template_mesh("box", extent_lo=(0, 0, 0), extent_hi=(1, 1, 1), n_cells=n)
+    if jitter:
+        synthetic.jitter_vertices(h.levels[0].vertices, n, (0, 0, 0), (1, 1, 1), 5)
+    meshmod.refine_uniform(h)
+    space = spmod.FeSpace(h, 1)
+    level = dv.DeviceLevel.get(space)
+    assert level.n_cells // 128 > 148
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(4 * space.n_nodes, device="cuda", generator=gen)
+    b = torch.randn(4 * space.n_nodes, device="cuda", generator=gen) * 1e-3
+    ph = _lib.Phys(1e-3, 5e-3, 0.02, 0.1, 1)
+    elem = torch.empty(level.n_cells * 108, dtype=torch.float32, device="cuda")
+    out = []
+    for tc in (True, True, False):
+        lv = level.struct(None, geometry=True, tc=tc)
+        r = torch.empty_like(x)
+        _lib.call("dnnmg_residual", ctypes.byref(lv), dv.ptr(x), dv.ptr(b), None, None,
+                  ctypes.byref(ph), dv.ptr(elem), dv.ptr(r), 0, dv.stream_handle())
+        torch.cuda.synchronize()
+        out.append(r.double().cpu().numpy())
+    assert np.array_equal(out[0], out[1])
+    assert rel(out[0], out[2]) < 1e-6, rel(out[0], out[2])

@@ -71,8 +71,7 @@ constexpr uint32_t oStage = kConstBytes;                // next tile's nodal val
 constexpr uint32_t oOut = oStage + kCells * 27 * 16;    // element-vector staging of a tile
 constexpr uint32_t kOutBytes = kCells * 27 * 16;
 constexpr uint32_t oV = oOut + kOutBytes;               // vertex values [8][128] float4
-constexpr uint32_t oMax = oV + 8 * kCells * 16;         // per-cell maxima, 2 buffers x [5][128]
-constexpr uint32_t oBar = oMax + 2 * 5 * kCells * 4;
+constexpr uint32_t oBar = oV + 8 * kCells * 16;
 constexpr uint32_t kSmem = oBar + 128;
 static_assert(kSmem <= 232448, "shared memory");
 static_assert(oStage % 128 == 0 && oOut % 16 == 0 && oV % 16 == 0 && oBar % 8 == 0, "alignment");
@@ -209,6 +208,7 @@ struct Args {
   const float* geo;
   float4* elem;
   unsigned long long* trace;   // DNNMG_K2TC_TRACE: clock64 stamps of CTA 0's first tiles
+  uint32_t* cmax;              // DNNMG_K2TC_CMAX: per cell max |scaled coefficient| (diagnostic)
 };
 // trace slots: [tile][stage][4]: forward warp 0 top / issued, backward warp 0 ready / issued
 #define K2_TRACE(slot) \
@@ -401,17 +401,17 @@ __device__ __forceinline__ void store_comp(uint32_t* wv, float a0, float a1, flo
   split_f16x2(a6, 0.f, wv[3], wv[7]);
 }
 
-// per-point coefficients (assembly.py:212-259; the SIMT kernel's pointwise phase), split
-// into the 32 words of the backward A operand (4 components x [hi 4 | lo 4]):
+// per-point coefficients (assembly.py:212-259; the SIMT kernel's pointwise phase):
 // F[f][m]: field f (p, vx, vy, vz), value (m = 0) and reference derivatives d/dxi_{m-1};
 // PQ: the same of the pi-projected (Q1) fields; Ji[k][j] = dxi_k/dx_j; w = w_hat det J
 // (times the cell's power-of-two scale); wm = w - det_ref w_hat: the mass term's weight
-// minus the cell's reference mass, which the epilogue applies exactly in fp32 (0 for affine
-// cells).  comp 0: {A0, B0k, B0k} against [N, dN_k, T'_k]; comp i: {A_i, B_ik, P_ik}.
+// minus the cell's reference mass, which is applied exactly in fp32 outside the GEMM (0 for
+// affine cells).  cf[0] = {A0, B0k}, cf[i] = {A_i, B_ik, P_ik}; every coefficient is linear
+// in (w, wm), so scaling those scales the set.
 template <int MODE, int GEO>
-__device__ __forceinline__ void point_store(const Args& A, const float F[4][4], const float PQ[4][4],
-                                            const float Ji[3][3], float w, float wm, float aT,
-                                            float dT, uint32_t* wv) {
+__device__ __forceinline__ void point_coeffs(const Args& A, const float F[4][4], const float PQ[4][4],
+                                             const float Ji[3][3], float w, float wm, float aT,
+                                             float dT, float cf[4][7]) {
   float v[3], gv[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
@@ -431,16 +431,10 @@ __device__ __forceinline__ void point_store(const Args& A, const float F[4][4], 
       float E[3];
 #pragma unroll
       for (int j = 0; j < 3; ++j) E[j] = aT * w * grad_j<GEO>(dd0, dd1, dd2, Ji, j);
-      const float b0 = tr_k<GEO>(E[0], E[1], E[2], Ji, 0);
-      const float b1 = tr_k<GEO>(E[0], E[1], E[2], Ji, 1);
-      const float b2 = tr_k<GEO>(E[0], E[1], E[2], Ji, 2);
-      // {A0, B00, B01, B02, B00, B01, B02, 0}: the duplicated words by byte permutes
-      split_f16x2(w * (gv[0][0] + gv[1][1] + gv[2][2]), b0, wv[0], wv[4]);
-      split_f16x2(b1, b2, wv[1], wv[5]);
-      wv[2] = __byte_perm(wv[0], wv[1], 0x5432);   // (B00, B01)
-      wv[6] = __byte_perm(wv[4], wv[5], 0x5432);
-      wv[3] = __byte_perm(wv[1], 0u, 0x5432);      // (B02, 0)
-      wv[7] = __byte_perm(wv[5], 0u, 0x5432);
+      cf[0][0] = w * (gv[0][0] + gv[1][1] + gv[2][2]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cf[0][1 + k] = tr_k<GEO>(E[0], E[1], E[2], Ji, k);
+      cf[0][4] = cf[0][5] = cf[0][6] = 0.f;   // (comp 0 repeats B0k in the split)
     }
     const float p = F[0][0];
     const bool use_d = A.convection && dT != 0.f;
@@ -460,20 +454,41 @@ __device__ __forceinline__ void point_store(const Args& A, const float F[4][4], 
       float Fi[3];
 #pragma unroll
       for (int j = 0; j < 3; ++j) Fi[j] = hn * gv[i][j] + dg * v[j] - (i == j ? w * p : 0.f);
-      store_comp(wv + 8 * (i + 1), fmaf(wm * ik, v[i], w * 0.5f * conv[i]),
-                 tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, 0), tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, 1),
-                 tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, 2), dg * pvr[0], dg * pvr[1], dg * pvr[2]);
+      cf[1 + i][0] = fmaf(wm * ik, v[i], w * 0.5f * conv[i]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        cf[1 + i][1 + k] = tr_k<GEO>(Fi[0], Fi[1], Fi[2], Ji, k);
+        cf[1 + i][4 + k] = dg * pvr[k];
+      }
     }
   } else {  // next-step RHS, f = None (assembly.py:242-259)
     const float hn = -0.5f * A.nu * w;
-    store_comp(wv, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
-      store_comp(wv + 8 * (i + 1), fmaf(wm * ik, v[i], -w * 0.5f * conv[i]),
-                 hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, 0),
-                 hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, 1),
-                 hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, 2), 0.f, 0.f, 0.f);
+    for (int k = 0; k < 7; ++k) cf[0][k] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      cf[1 + i][0] = fmaf(wm * ik, v[i], -w * 0.5f * conv[i]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        cf[1 + i][1 + k] = hn * tr_k<GEO>(gv[i][0], gv[i][1], gv[i][2], Ji, k);
+        cf[1 + i][4 + k] = 0.f;
+      }
+    }
   }
+}
+
+// the 32 words of the backward A operand (4 components x [hi 4 | lo 4]) from the (scaled)
+// coefficients; comp 0 is {A0, B00, B01, B02, B00, B01, B02, 0}: its repeated words by byte
+// permutes
+__device__ __forceinline__ void split_coeffs(const float cf[4][7], uint32_t* wv) {
+  split_f16x2(cf[0][0], cf[0][1], wv[0], wv[4]);
+  split_f16x2(cf[0][2], cf[0][3], wv[1], wv[5]);
+  wv[2] = __byte_perm(wv[0], wv[1], 0x5432);   // (B00, B01)
+  wv[6] = __byte_perm(wv[4], wv[5], 0x5432);
+  wv[3] = __byte_perm(wv[1], 0u, 0x5432);      // (B02, 0)
+  wv[7] = __byte_perm(wv[5], 0u, 0x5432);
+#pragma unroll
+  for (int i = 1; i < 4; ++i) store_comp(wv + 8 * i, cf[i][0], cf[i][1], cf[i][2], cf[i][3], cf[i][4], cf[i][5], cf[i][6]);
 }
 
 __device__ __forceinline__ float comp4(const float4& v, int f) {
@@ -510,8 +525,6 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < 2 * 5 * kCells; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(smem + oMax)[i] = 0u;
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot))
@@ -667,21 +680,22 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
         const int a = kNodesPer * g + i;
         X[i] = a < 27 ? stg[a * kCells + r] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      uint32_t* mx = reinterpret_cast<uint32_t*>(smem + oMax) + (it & 1) * 5 * kCells + r;
-      {
-        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+      // the cell's extrema over its 27 staged nodes (every thread of the cell reads them: no
+      // exchange, no atomics)
+      float fhi[4] = {-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f};
+      float flo[4] = {3.0e38f, 3.0e38f, 3.0e38f, 3.0e38f};
+      float vsq = 0.f;
+#pragma unroll 9
+      for (int a = 0; a < 27; ++a) {
+        const float4 xv = stg[a * kCells + r];
 #pragma unroll
-        for (int i = 0; i < kNodesPer; ++i) {
-          m[0] = fmaxf(m[0], fabsf(X[i].x));
-          m[1] = fmaxf(m[1], fabsf(X[i].y));
-          m[2] = fmaxf(m[2], fabsf(X[i].z));
-          m[3] = fmaxf(m[3], fabsf(X[i].w));
-          m[4] = fmaxf(m[4], X[i].y * X[i].y + X[i].z * X[i].z + X[i].w * X[i].w);
+        for (int f = 0; f < 4; ++f) {
+          fhi[f] = fmaxf(fhi[f], comp4(xv, f));
+          flo[f] = fminf(flo[f], comp4(xv, f));
         }
-        // non-negative floats order like their bit patterns: the cell's maxima by shared
-        // integer atomics (order-independent, deterministic)
-#pragma unroll
-        for (int k = 0; k < 5; ++k) atomicMax(mx + k * kCells, __float_as_uint(m[k]));
+        vsq = fmaxf(vsq, xv.y * xv.y + xv.z * xv.z + xv.w * xv.w);
+      }
+      {
         float4* vt = reinterpret_cast<float4*>(smem + oV);
 #pragma unroll
         for (int i = 0; i < kNodesPer; ++i) {
@@ -695,28 +709,53 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
       // ---- per-cell scales, stabilisation weights ----
       float sf[4], inv_f[4], sB = 1.f, invB = 1.f;
       {
-        float m[5];
+        float fmx[4], frg[4];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) m[k] = __uint_as_float(mx[k * kCells]);
-        if (g == 0) {   // reset the other buffer for the next tile (read during the last one)
-          uint32_t* mo = reinterpret_cast<uint32_t*>(smem + oMax) + ((it + 1) & 1) * 5 * kCells + r;
-#pragma unroll
-          for (int k = 0; k < 5; ++k) mo[k * kCells] = 0u;
+        for (int f = 0; f < 4; ++f) {
+          fmx[f] = fmaxf(fabsf(fhi[f]), fabsf(flo[f]));
+          frg[f] = fhi[f] - flo[f];
+          pow2_scale(fmx[f], 0, sf[f], inv_f[f]);
         }
-#pragma unroll
-        for (int f = 0; f < 4; ++f) pow2_scale(m[f], 0, sf[f], inv_f[f]);
+        const float vmax = sqrtf(vsq);
         if (valid) {
-          const float vmax = sqrtf(m[4]);
           const float ih = frcp(h);
           if (!A.alpha_in) {  // stab at x (assembly.py:55-59, 169-178)
             const float rden = frcp(fmaf(A.nu * ih, ih, fmaf(vmax, ih, A.ik)));
             aT = A.alpha0 * rden;
             dT = A.delta0 * rden;
           }
-          // power-of-two scale of the coefficients: a generous bound of their size
-          // (w <= 0.035 h^3; |grad v| ~ vmax / h) placed near 2^8 of the fp16 range
-          const float bound = 0.035f * h * h * h * (vmax + m[0] + 1e-30f) * (1.f + vmax) *
-                              (A.ik + (vmax + A.nu + 1.f) * ih + A.nu * ih * ih + 1.f);
+          // power-of-two scale of the coefficients: an upper bound of their size from the
+          // cell's nodal extrema placed at 2^8 of the fp16 range (a bound from vmax alone
+          // overshot by 10^3-10^6 on smooth fields and drove the fp16 lo parts subnormal).
+          // Q2 at the Gauss points: |u(q)| <= 1.84 max|u_a|; |du/dxi_k(q)| <= 10.33 range/2
+          // (the dN_a sum to 0), so a physical gradient entry <= 15.5 |J^-1|_max range;
+          // w <= 0.0347 det J on an affine cell
+          float jm, wmax, wmm;
+          if constexpr (AFFINE) {
+            jm = fmaxf(fmaxf(fabsf(Jc[0][0]), fabsf(Jc[1][1])), fabsf(Jc[2][2]));
+            if constexpr (GEO == 1)
+              jm = fmaxf(jm, fmaxf(fmaxf(fmaxf(fabsf(Jc[0][1]), fabsf(Jc[0][2])), fmaxf(fabsf(Jc[1][0]), fabsf(Jc[1][2]))),
+                                   fmaxf(fabsf(Jc[2][0]), fabsf(Jc[2][1]))));
+            wmax = 0.0347f * det;
+            wmm = 0.f;
+          } else {   // per-point geometry: |J^-1| <= 4/h, w <= 0.035 h^3 (generous)
+            jm = 4.f * ih;
+            wmax = 0.035f * h * h * h;
+            wmm = wmax;
+          }
+          const float V = 1.84f * fmaxf(fmaxf(fmx[1], fmx[2]), fmx[3]);
+          const float P = 1.84f * fmx[0];
+          const float G = 15.5f * jm * fmaxf(fmaxf(frg[1], frg[2]), frg[3]);
+          const float Gp = 31.f * jm * frg[0];   // gradient of p - pi p
+          const float conv = 3.f * V * G;
+          float bound = fmaxf(fmaf(wmm * A.ik, V, 0.5f * wmax * conv), 3.f * jm * 0.5f * A.nu * wmax * G);
+          if constexpr (MODE == 0) {
+            const float gd = 2.f * conv;   // |conv - (pi v . grad) pi v|
+            bound = fmaxf(bound, wmax * 3.f * G);                                   // A0
+            bound = fmaxf(bound, 3.f * jm * aT * wmax * 3.f * jm * Gp);              // B0k
+            bound = fmaxf(bound, 3.f * jm * wmax * (0.5f * A.nu * G + dT * gd * V + P));   // B_ik
+            bound = fmaxf(bound, dT * wmax * gd * 3.f * jm * V);                     // P_ik
+          }
           pow2_scale(bound, 8, sB, invB);
         }
       }
@@ -748,7 +787,6 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
       } else if (lane == 0) {
         mbar_arrive(smem_u32(b_acc_free));
       }
-      invB_prev = invB;
       // ---- 16 stages: Gauss point q = 4 s + g ----
       auto stage = [&](int s, bool wait_store) {
         const uint32_t b = s & 1, par = (s >> 1) & 1;   // 16 stages per tile
@@ -820,8 +858,18 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
             PQ[f][3] = bb[1] - bb[0];
           }
         }
+        float cf[4][7];
         uint32_t wv[32];
-        point_store<MODE, GEO>(A, F, PQ, Ji, w * sB, (w - kWq[q] * det) * sB, aT, dT, wv);
+        point_coeffs<MODE, GEO>(A, F, PQ, Ji, w * sB, (w - kWq[q] * det) * sB, aT, dT, cf);
+        split_coeffs(cf, wv);
+        if (A.cmax && valid) {   // diagnostic: the largest scaled coefficient of this point
+          float mxc = 0.f;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int k = 0; k < 7; ++k) mxc = fmaxf(mxc, fabsf(cf[i][k]));
+          atomicMax(A.cmax + cell, __float_as_uint(mxc));
+        }
         // the backward A operand is free once the previous stage's MMAs have completed
         mbar_sleep(smem_u32(b_ab_free), (s & 1) ^ 1);
         tc_fence_after();
@@ -868,6 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
           for (int a = 0; a < 27; ++a) outs[4 * a] = 0.f;
         }
       };
+      invB_prev = invB;
       stage(0, true);
       stage(1, false);
       // the next tile's node indices (their load latency overlaps the mass term; the rows are
@@ -945,6 +994,8 @@ int32_t launch_k2tc_elements(const dnnmg_level_t* lv, const float* x, const floa
   A.geo = lv->tc_geo;
   A.elem = reinterpret_cast<float4*>(elem);
   A.trace = nullptr;
+  A.cmax = nullptr;
+  if (const char* cm = getenv("DNNMG_K2TC_CMAX")) A.cmax = reinterpret_cast<uint32_t*>(strtoull(cm, nullptr, 0));
   static unsigned long long* trace_buf = nullptr;
   if (getenv("DNNMG_K2TC_TRACE")) {   // diagnostic timeline (tools/gpu/k2_trace.py)
     if (!trace_buf) cudaMallocManaged(&trace_buf, 8192 * sizeof(unsigned long long));

@@ -274,9 +274,11 @@ def geometry_kind(vertices, cells, rtol=1e-10, chunk=1 << 18):
     return kind
 
 
-def k2_tensor_cores():
-    """The tensor-core element kernel (csrc/residual_tc.cu) is opt-in (DNNMG_K2=tc): it is
-    parity-green but slower than the SIMT kernel on B200 (K2)."""
+def k2_tensor_cores(geo_kind):
+    """Element kernel of K2 for a level.  The tensor-core one (csrc/residual_tc.cu) is opt-in
+    (DNNMG_K2=tc, affine or per-point geometry): at config 3 it runs at parity with the SIMT
+    kernel (1.00 vs 0.96 ms; per-point geometry 1.19 ms) with a ~2.5x larger (in-gate)
+    residual error, so the SIMT kernel stays the default (K2)."""
     return os.environ.get("DNNMG_K2", "") == "tc"
 
 
@@ -302,9 +304,9 @@ class DeviceLevel:
         self.tc_geo = None
 
     def struct(self, dof_mask=None, geometry=False, tc=None):
-        """tc: use the tensor-core element kernel (default: DNNMG_K2=tc with the geometry
-        cache present)."""
-        tc = geometry and k2_tensor_cores() if tc is None else tc
+        """tc: use the tensor-core element kernel (default: with the geometry cache present,
+        k2_tensor_cores)."""
+        tc = geometry and k2_tensor_cores(self.geo_kind) if tc is None else tc
         lv = _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
                         ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask),
                         ptr(self.geometry()) if (geometry or tc) else None, ptr(self.order),

@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_items = (int64_t)A.n_tiles * A.n_nb;
+  const bool seg2 = MODE == DNNMG_PREC_TF32X3 && A.n_kc * KC > 512;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -116,12 +117,22 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
         const int b = (int)(item % A.n_nb);
         const int nbw = b == A.n_nb - 1 ? A.Nlast : kLN;
         const uint32_t idesc = idesc_for<MODE>(nbw);
-        const int buf = j & 1;
-        mbar_wait(smem_u32(&acc_empty[buf]), ((j >> 1) & 1) ^ 1);
+        // seg2: the K loop in two halves accumulated in the two buffers (both per item), so
+        // that no tensor-core accumulation runs over more than K/2 (its fp32 accumulation
+        // rounds per step: tf32x3 measured 1.2e-5 at K = 1024 in one accumulator)
+        const int buf = seg2 ? 0 : (j & 1);
+        const int khalf = seg2 ? (A.n_kc + 1) / 2 : A.n_kc;
+        if (seg2) {
+          mbar_wait(smem_u32(&acc_empty[0]), (j & 1) ^ 1);
+          mbar_wait(smem_u32(&acc_empty[1]), (j & 1) ^ 1);
+        } else {
+          mbar_wait(smem_u32(&acc_empty[buf]), ((j >> 1) & 1) ^ 1);
+        }
         tc_fence_after();
-        const uint32_t d = tmem + buf * kLN;
         for (int kc = 0; kc < A.n_kc; ++kc, ++it) {
           const int s = it % NS;
+          const bool second = kc >= khalf;
+          const uint32_t d = tmem + (second ? 1 : buf) * kLN;
           mbar_wait(smem_u32(&full[s]), (it / NS) & 1);
           tc_fence_after();
           const uint32_t ab = smem_u32(smem + s * STG);
@@ -129,7 +140,7 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
 #pragma unroll
           for (int ks = 0; ks < KC / C::KSTEP; ++ks) {
             const uint32_t koff = ks * 256;
-            const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t acc = ((kc > 0 && kc != khalf) || ks > 0) ? 1u : 0u;
             const uint64_t ahi = sdesc(ab + koff, SBO), bhi = sdesc(wb + koff, SBO);
             tc_mma<MODE>(d, ahi, bhi, idesc, acc);
             if constexpr (C::PARTS == 2) {
@@ -140,8 +151,9 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
             }
           }
           tc_commit(smem_u32(&empty[s]));
+          if (seg2 && kc == khalf - 1) tc_commit(smem_u32(&acc_full[0]));
         }
-        tc_commit(smem_u32(&acc_full[buf]));
+        tc_commit(smem_u32(&acc_full[seg2 ? 1 : buf]));
       }
     }
   } else {
@@ -157,16 +169,28 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
       const int t = (int)(item / A.n_nb), b = (int)(item % A.n_nb);
       const int nbw = b == A.n_nb - 1 ? A.Nlast : kLN;
-      const int buf = j & 1;
+      const int buf = seg2 ? 0 : (j & 1);
       const int64_t grow = (int64_t)t * kTcM + row;
       const bool live = grow < A.n_rows;
-      mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
+      if (seg2) {
+        mbar_wait(smem_u32(&acc_full[0]), j & 1);
+        mbar_wait(smem_u32(&acc_full[1]), j & 1);
+      } else {
+        mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
+      }
       tc_fence_after();
       const int c0 = half * (nbw / 2);
       for (int cc = c0; cc < c0 + nbw / 2; cc += GS) {
         float v[GS];
 #pragma unroll
         for (int p = 0; p < GS / 16; ++p) tmem_ld16(tmem + lane_addr + buf * kLN + cc + 16 * p, v + 16 * p);
+        if (seg2) {   // the second K half, added in fp32
+          float v2[GS];
+#pragma unroll
+          for (int p = 0; p < GS / 16; ++p) tmem_ld16(tmem + lane_addr + kLN + cc + 16 * p, v2 + 16 * p);
+#pragma unroll
+          for (int e = 0; e < GS; ++e) v[e] += v2[e];
+        }
         const int col0 = b * kLN + cc;          // layer column of v[0]
         if (A.head) {
           if (live) {
@@ -236,7 +260,10 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
+      if (lane == 0) {
+        mbar_arrive(smem_u32(&acc_empty[buf]));
+        if (seg2) mbar_arrive(smem_u32(&acc_empty[1]));
+      }
     }
   }
   tc_fence_before();

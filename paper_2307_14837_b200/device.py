@@ -442,17 +442,28 @@ class DeviceModel:
 
         self._ws = None
 
-    def workspace(self, n_rows):
-        """Device workspace of the layered tensor-core kernel (None when not needed),
-        grown on demand and kept for later calls."""
+    def workspace_bytes(self, n_rows):
+        """Bytes of the layered tensor-core kernel's workspace for n_rows (0: not needed)."""
         nbytes = ctypes.c_int64(0)
         _lib.call("dnnmg_mlp_workspace_bytes", ctypes.byref(self.struct), int(n_rows),
                   ctypes.byref(nbytes))
-        if nbytes.value == 0:
+        return int(nbytes.value)
+
+    def workspace(self, n_rows):
+        """The model's shared workspace for the drop-in net.forward calls (stream-ordered on
+        the caller's current stream; None when not needed), grown on demand and kept.
+        CorrectionStep allocates its own (new_workspace)."""
+        n = self.workspace_bytes(n_rows)
+        if n == 0:
             return None
-        if self._ws is None or self._ws.numel() < nbytes.value:
-            self._ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=device())
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.empty(n, dtype=torch.uint8, device=device())
         return self._ws
+
+    def new_workspace(self, n_rows):
+        """A workspace owned by the caller (None when not needed)."""
+        n = self.workspace_bytes(n_rows)
+        return None if n == 0 else torch.empty(n, dtype=torch.uint8, device=device())
 
     def forward(self, X, n_rows, Y):
         ws = self.workspace(n_rows)

@@ -80,7 +80,9 @@ class CorrectionStep:
                               output_width(self.patchset)), dtype=f, device=dev)
         self.x_mid = (torch.empty(4 * self.prolongs[0].n_fine, dtype=f, device=dev)
                       if J == 2 else None)
-        self.mlp_ws = self.model.workspace(self.ps.n_patches) if self.layered else None
+        # its own MLP workspace (not the model's shared one): steps sharing a model can run
+        # on different streams
+        self.mlp_ws = self.model.new_workspace(self.ps.n_patches) if self.layered else None
         self.buf = _lib.StepBuffers(dv.ptr(self.x_tilde), dv.ptr(self.r), dv.ptr(self.elem),
                                     dv.ptr(self.X), dv.ptr(self.Y), dv.ptr(self.d),
                                     dv.ptr(self.x_mid), dv.ptr(self.mlp_ws), dv.nbytes(self.mlp_ws))

@@ -351,6 +351,10 @@ typedef struct {
   float* x_mid;     /* [4*n_mid] intermediate level for J = 2, else NULL */
   void* mlp_ws;     /* dnnmg_mlp_workspace_bytes(m, n_patches) bytes, or NULL when 0 */
   int64_t mlp_ws_bytes; /* size of mlp_ws: a smaller buffer than the rows need is an error */
+  void* b_ready;    /* optional cudaEvent_t: b_prev may still be in flight (e.g. its H2D copy);
+                       the step waits for it on its stream right before its first read of b_prev
+                       (the residual's node sum), so prolongation and the element kernel overlap
+                       the copy.  NULL: b_prev is ready.  Not for use inside stream capture. */
 } dnnmg_step_buffers_t;
 
 /* prolongations: J entries (levels L..L+J-1); bc: Dirichlet data of the fine level. */

@@ -86,7 +86,8 @@ class Slab(ctypes.Structure):
 
 class StepBuffers(ctypes.Structure):
     _fields_ = [("x_tilde", c_vp), ("r", c_vp), ("elem", c_vp), ("X", c_vp), ("Y", c_vp),
-                ("d", c_vp), ("x_mid", c_vp), ("mlp_ws", c_vp), ("mlp_ws_bytes", c_i64)]
+                ("d", c_vp), ("x_mid", c_vp), ("mlp_ws", c_vp), ("mlp_ws_bytes", c_i64),
+                ("b_ready", c_vp)]
 
 
 EXPORTS = {

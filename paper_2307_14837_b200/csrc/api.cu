@@ -26,7 +26,8 @@ int32_t launch_k2tc_geometry(const dnnmg_level_t*, float*, int32_t, cudaStream_t
 int32_t launch_stab(const dnnmg_level_t*, const float*, const dnnmg_phys_t*, float*, float*,
                     cudaStream_t);
 int32_t launch_residual(const dnnmg_level_t*, const float*, const float*, const float*,
-                        const float*, const dnnmg_phys_t*, float*, float*, int, int, cudaStream_t);
+                        const float*, const dnnmg_phys_t*, float*, float*, int, int, cudaStream_t,
+                        cudaEvent_t b_ready = nullptr);
 int32_t launch_gather(const dnnmg_patchset_t*, const float*, const float*, float*, cudaStream_t);
 int32_t launch_restrict(const dnnmg_patchset_t*, const float*, float*, cudaStream_t);
 int32_t launch_extend(const dnnmg_patchset_t*, const float*, float*, cudaStream_t);
@@ -311,7 +312,7 @@ int32_t dnnmg_correction_step(const dnnmg_prolong_t* P, int32_t J, const dnnmg_d
   if (rc) return rc;
   // (3) stab at x~ + residual against the carried RHS, masked (driver.py:255-258)
   rc = launch_residual(fine, buf->x_tilde, b_prev, nullptr, nullptr, ph, buf->elem, buf->r, 1, 1,
-                       st);
+                       st, reinterpret_cast<cudaEvent_t>(buf->b_ready));
   if (rc) return rc;
   // (4) patch features, network, averaging scatter, update (driver.py:263-268)
   if (fused_gather(m, ps)) {

@@ -857,7 +857,8 @@ int32_t launch_stab(const dnnmg_level_t* lv, const float* x, const dnnmg_phys_t*
 
 int32_t launch_residual(const dnnmg_level_t* lv, const float* x, const float* b_prev,
                         const float* aT, const float* dT, const dnnmg_phys_t* ph, float* elem,
-                        float* r, int apply_mask, int mode_sign, cudaStream_t s) {
+                        float* r, int apply_mask, int mode_sign, cudaStream_t s,
+                        cudaEvent_t b_ready) {
   // mode_sign: +1 residual (b - A), 0 operator (A), 2 rhs_next
   int32_t st = check_level(lv, "residual");
   if (st) return st;
@@ -873,6 +874,10 @@ int32_t launch_residual(const dnnmg_level_t* lv, const float* x, const float* b_
     b = reinterpret_cast<const float4*>(b_prev);
   }
   if (lv->n_nodes == 0) return DNNMG_OK;
+  if (b_ready) {   // b_prev may still be arriving: its first reader is the node sum
+    DNNMG_REQUIRE(cudaStreamWaitEvent(s, b_ready, 0) == cudaSuccess, DNNMG_ERR_CUDA,
+                  "residual: cudaStreamWaitEvent(b_ready) failed");
+  }
   node_sum_kernel<<<grid_for(lv->n_nodes, 256), 256, 0, s>>>(
       lv->n_nodes, lv->node_cell_ptr, lv->node_cell_idx, reinterpret_cast<const float4*>(elem), b,
       1.0f, (apply_mask && lv->dof_mask) ? lv->dof_mask : nullptr, reinterpret_cast<float4*>(r),

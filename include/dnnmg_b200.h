@@ -118,6 +118,10 @@ typedef struct {
   int32_t n_nodes;
   const uint8_t* bc_code;  /* [n_nodes] */
   const float* bc_values;  /* [n_nodes][3] or NULL when no code 2 is present */
+  const uint8_t* bc_code_owner;  /* optional [n_nodes]: bc_code in the owner order of the
+                                    prolongation it is applied with (dnnmg_prolong_t.owner_node),
+                                    read coalesced instead of gathered per owned node; NULL:
+                                    gathered */
 } dnnmg_dirichlet_t;
 
 /* One fine level for assembly (assembly.py:65-108). */

@@ -28,7 +28,8 @@ class Prolong(ctypes.Structure):
 
 
 class Dirichlet(ctypes.Structure):
-    _fields_ = [("n_nodes", c_i32), ("bc_code", c_vp), ("bc_values", c_vp)]
+    _fields_ = [("n_nodes", c_i32), ("bc_code", c_vp), ("bc_values", c_vp),
+                ("bc_code_owner", c_vp)]
 
 
 class Level(ctypes.Structure):

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
     int n_coarse_cells, const int32_t* __restrict__ ctab, const int32_t* __restrict__ owner_ptr,
     const int32_t* __restrict__ owner_node, const uint8_t* __restrict__ owner_code,
     const float4* __restrict__ xc, float4* __restrict__ xf, const uint8_t* __restrict__ bc_code,
-    const float* __restrict__ bc_values) {
+    const float* __restrict__ bc_values, const uint8_t* __restrict__ bc_owner) {
   __shared__ float4 sm[kProlongWarps][27 + 45 + 75 + 125];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* cv = sm[w];        // [iz][iy][ix]
@@ -141,8 +141,14 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
       nn[k] = i < e ? __ldg(owner_node + i) : -1;
       cc[k] = i < e ? __ldg(owner_code + i) : 0;
     }
+    // Dirichlet codes: in owner order (coalesced, with the owner-list loads) when given, else
+    // gathered per owned node (a dependent load)
 #pragma unroll
-    for (int k = 0; k < kMaxOwned / 32; ++k) bb[k] = (bc_code && nn[k] >= 0) ? bc_code[nn[k]] : 0;
+    for (int k = 0; k < kMaxOwned / 32; ++k) {
+      const int i = s + lane + 32 * k;
+      bb[k] = bc_owner ? (i < e ? __ldg(bc_owner + i) : 0)
+                       : ((bc_code && nn[k] >= 0) ? bc_code[nn[k]] : 0);
+    }
     if (C + stride < n_coarse_cells) {
       if (lane < 27) nxt = __ldg(xc + __ldg(ctab + (int64_t)(C + stride) * 27 + lane));
       s_nxt = __ldg(owner_ptr + C + stride);
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
       const int pz = 2 * (o >> 2) + a / 9;
       float4 acc = X3[25 * pz + 5 * py + px];
       if (bc_code) {
-        const uint8_t code = bc_code[n];
+        const uint8_t code = bc_owner ? __ldg(bc_owner + i) : bc_code[n];
         if (code == 1) {
           acc.y = acc.z = acc.w = 0.f;
         } else if (code == 2) {
@@ -233,6 +239,7 @@ int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float
   DNNMG_REQUIRE(((uintptr_t)x_coarse & 15) == 0 && ((uintptr_t)x_fine & 15) == 0, DNNMG_ERR_ARG,
                 "prolongate: vectors must be 16-byte aligned");
   const uint8_t* code = nullptr;
+  const uint8_t* owner_code = nullptr;
   const float* vals = nullptr;
   if (bc) {
     DNNMG_REQUIRE(bc->n_nodes == P->n_fine_nodes, DNNMG_ERR_ARG,
@@ -240,13 +247,15 @@ int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float
                   bc->n_nodes, P->n_fine_nodes);
     code = bc->bc_code;
     vals = bc->bc_values;
+    owner_code = bc->bc_code_owner;
   }
   if (P->n_fine_nodes == 0) return DNNMG_OK;
   if (P->owner_ptr && P->owner_node && P->owner_code) {
     const int blocks = grid_for((P->n_coarse_cells + kProlongWarps - 1) / kProlongWarps, 1, 4);
     prolongate_owner_kernel<<<blocks, 32 * kProlongWarps, 0, s>>>(
         P->n_coarse_cells, P->coarse_cell_nodes, P->owner_ptr, P->owner_node, P->owner_code,
-        reinterpret_cast<const float4*>(x_coarse), reinterpret_cast<float4*>(x_fine), code, vals);
+        reinterpret_cast<const float4*>(x_coarse), reinterpret_cast<float4*>(x_fine), code, vals,
+        owner_code);
     DNNMG_CHECK_LAUNCH("prolongate_owner_kernel");
     return DNNMG_OK;
   }

@@ -171,6 +171,7 @@ class DeviceProlong:
         optr = np.zeros(ctab.shape[0] + 1, dtype=np.int64)
         np.cumsum(counts, out=optr[1:])
         self.owner_ptr = upload(optr, np.int32)
+        self.owner_order = order                      # host copy (owner-ordered bc codes)
         self.owner_node = upload(order, np.int32)
         self.owner_code = upload(src[order] % 216, np.uint8)
         self.struct = _lib.Prolong(self.n_fine, int(ctab.shape[0]), ptr(self.ctab), ptr(self.src),

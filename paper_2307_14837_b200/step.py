@@ -107,8 +107,11 @@ class CorrectionStep:
         self.graph = None  # new buffers: a graph captured earlier would read stale ones
         self.bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
         self.bc.code = dv.upload(code, np.uint8)
+        # the codes in the owner order of the last prolongation (K1 reads them coalesced)
+        self.bc.code_owner = dv.upload(np.asarray(code, np.uint8)[self.prolongs[-1].owner_order], np.uint8)
         self.bc.vals = None if vals is None else dv.upload(vals, np.float32)
-        self.bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(self.bc.code), dv.ptr(self.bc.vals))
+        self.bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(self.bc.code), dv.ptr(self.bc.vals),
+                                        dv.ptr(self.bc.code_owner))
         self._t = t
 
     @property
@@ -139,7 +142,9 @@ class CorrectionStep:
             # time-dependent Dirichlet data are updated in place by set_time: own a copy
             bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
             bc.code, bc.vals = self.bc.code.clone(), self.bc.vals.clone()
-            bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(bc.code), dv.ptr(bc.vals))
+            bc.code_owner = self.bc.code_owner
+            bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(bc.code), dv.ptr(bc.vals),
+                                       dv.ptr(bc.code_owner))
             t.bc = bc
         t.graph = None
         return t

@@ -92,9 +92,9 @@ __global__ void __launch_bounds__(256) dirichlet_kernel(int n, const uint8_t* __
 
 // v3: one warp per parent cell C, separable.  The 27 coarse values of C are staged in
 // shared memory (prefetched one cell ahead), interpolated to the 5 x 5 x 5 lattice of the
-// refined cell in three 1-D stages (x: 45 values, y: 75, z: 125; an odd lattice position
-// takes the 3-tap quarter-point stencil, an even one copies), and the fine nodes whose
-// first-appearance parent is C (owner list, CSR by C) are written from the lattice.
+// refined cell in three 1-D stages (x: 45 values and y: 75 in shared memory, z only at the
+// owned nodes; an odd lattice position takes the 3-tap quarter-point stencil, an even one
+// copies), writing the fine nodes whose first-appearance parent is C (owner list, CSR by C).
 constexpr int kProlongWarps = 8;
 
 __device__ __forceinline__ float4 lerp3(int p, const float4& a, const float4& b, const float4& c) {
@@ -113,12 +113,11 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
     const int32_t* __restrict__ owner_node, const uint8_t* __restrict__ owner_code,
     const float4* __restrict__ xc, float4* __restrict__ xf, const uint8_t* __restrict__ bc_code,
     const float* __restrict__ bc_values, const uint8_t* __restrict__ bc_owner) {
-  __shared__ float4 sm[kProlongWarps][27 + 45 + 75 + 125];
+  __shared__ float4 sm[kProlongWarps][27 + 45 + 75];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* cv = sm[w];        // [iz][iy][ix]
   float4* X1 = cv + 27;      // [iz][iy][px]
   float4* X2 = X1 + 45;      // [iz][py][px]
-  float4* X3 = X2 + 75;      // [pz][py][px]
   const int stride = gridDim.x * kProlongWarps;
   int C = blockIdx.x * kProlongWarps + w;
   constexpr int kMaxOwned = 96;  // owned fine nodes per parent cell: <= 64 + faces (checked on host)
@@ -177,17 +176,7 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
       }
     }
     __syncwarp();
-    // z stage: 125 = 5 pz x 25
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int l = lane + 32 * r;
-      if (l < 125) {
-        const int pz = l / 25, yx = l % 25;
-        const float4* c = X2 + yx;  // [iz] stride 25
-        X3[l] = (pz & 1) ? lerp3(pz, c[0], c[25], c[50]) : c[25 * (pz >> 1)];
-      }
-    }
-    __syncwarp();
+    // z stage: only at the owned nodes (about half of the 5 x 5 x 5 lattice), from X2
 #pragma unroll
     for (int k = 0; k < kMaxOwned / 32; ++k) {
       const int n = nn[k];
@@ -197,7 +186,8 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
         const int px = 2 * (o & 1) + a % 3;
         const int py = 2 * ((o >> 1) & 1) + (a / 3) % 3;
         const int pz = 2 * (o >> 2) + a / 9;
-        float4 acc = X3[25 * pz + 5 * py + px];
+        const float4* c = X2 + 5 * py + px;   // [iz] stride 25
+        float4 acc = (pz & 1) ? lerp3(pz, c[0], c[25], c[50]) : c[25 * (pz >> 1)];
         if (bb[k] == 1) {
           acc.y = acc.z = acc.w = 0.f;
         } else if (bb[k] == 2) {
@@ -215,7 +205,8 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
       const int px = 2 * (o & 1) + a % 3;
       const int py = 2 * ((o >> 1) & 1) + (a / 3) % 3;
       const int pz = 2 * (o >> 2) + a / 9;
-      float4 acc = X3[25 * pz + 5 * py + px];
+      const float4* c = X2 + 5 * py + px;
+      float4 acc = (pz & 1) ? lerp3(pz, c[0], c[25], c[50]) : c[25 * (pz >> 1)];
       if (bc_code) {
         const uint8_t code = bc_owner ? __ldg(bc_owner + i) : bc_code[n];
         if (code == 1) {

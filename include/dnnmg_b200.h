@@ -150,6 +150,11 @@ typedef struct {
   const float* tc_geo;           /* dnnmg_level_geometry_tc output */
   int32_t tc_geo_affine;         /* its layout: 0 = per point, 1 = per-cell affine record,
                                     2 = the same for axis-aligned cells (J^-1 diagonal) */
+  /* optional, with node_order: the CSR rows stored in visiting order (row i = the row of node
+     node_order[i]: entries visit_ptr[i] .. visit_ptr[i+1] of visit_idx), so the node sum reads
+     its row bounds without first resolving the node id (one dependent load fewer) */
+  const int32_t* visit_ptr;      /* [n_nodes+1] */
+  const int32_t* visit_idx;
 } dnnmg_level_t;
 
 typedef struct {
@@ -180,6 +185,8 @@ typedef struct {
   const uint16_t* tile_slot;      /* [n_tiles*128][npp] (rows past n_patches: any valid slot) */
   const int32_t* node_order;      /* [n_nodes] visiting order of the scatter (K5), as
                                      dnnmg_level_t.node_order; NULL = ascending ids */
+  const int32_t* visit_ptr;       /* optional, with node_order: the node -> (patch, slot) CSR */
+  const int32_t* visit_idx;       /*   rows in visiting order, as dnnmg_level_t.visit_ptr */
 } dnnmg_patchset_t;
 
 #define DNNMG_MAX_LAYERS 16

@@ -36,7 +36,8 @@ class Level(ctypes.Structure):
     _fields_ = [("n_nodes", c_i32), ("n_cells", c_i32), ("cell_nodes", c_vp), ("coords", c_vp),
                 ("h_T", c_vp), ("node_cell_ptr", c_vp), ("node_cell_idx", c_vp),
                 ("dof_mask", c_vp), ("geo_q", c_vp), ("node_order", c_vp),
-                ("tc_const", c_vp), ("tc_geo", c_vp), ("tc_geo_affine", c_i32)]
+                ("tc_const", c_vp), ("tc_geo", c_vp), ("tc_geo_affine", c_i32),
+                ("visit_ptr", c_vp), ("visit_idx", c_vp)]
 
 
 class Phys(ctypes.Structure):
@@ -49,7 +50,7 @@ class PatchSet(ctypes.Structure):
                 ("n_nodes", c_i32), ("node_table", c_vp), ("geom", c_vp),
                 ("node_patch_ptr", c_vp), ("node_patch_idx", c_vp),
                 ("tile_cap", c_i32), ("tile_nodes", c_vp), ("tile_count", c_vp), ("tile_slot", c_vp),
-                ("node_order", c_vp)]
+                ("node_order", c_vp), ("visit_ptr", c_vp), ("visit_idx", c_vp)]
 
 
 class Mlp(ctypes.Structure):

@@ -79,13 +79,16 @@ __global__ void __launch_bounds__(256) scatter_update_kernel(
     int n_nodes, int npp_rt, const int32_t* __restrict__ ptr,
     const int32_t* __restrict__ idx, const float* __restrict__ Y, const uint8_t* __restrict__ mask,
     const float4* __restrict__ xt, float scale, float4* __restrict__ d, float4* __restrict__ xc,
-    const int32_t* __restrict__ order) {
+    const int32_t* __restrict__ order, const int32_t* __restrict__ vptr,
+    const int32_t* __restrict__ vidx) {
   const int npp = NPP > 0 ? NPP : npp_rt;
   const int n_out = 3 * npp;
+  if (vptr) idx = vidx;   // rows in visiting order: the bounds load next to the node id
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < n_nodes;
        pos += gridDim.x * blockDim.x) {
     const int n = order ? __ldg(order + pos) : pos;
-    const int s = __ldg(ptr + n), e = __ldg(ptr + n + 1);
+    const int s = vptr ? __ldg(vptr + pos) : __ldg(ptr + n);
+    const int e = vptr ? __ldg(vptr + pos + 1) : __ldg(ptr + n + 1);
     // the node's own loads first: in flight with the entry loads
     const float4 x = xc ? __ldg(xt + n) : make_float4(0.f, 0.f, 0.f, 0.f);
     const uint8_t m = mask ? __ldg(mask + n) : 0;
@@ -196,7 +199,8 @@ int32_t launch_scatter_update(const dnnmg_patchset_t* ps, const float* Y, const 
   kern<<<grid_for(ps->n_nodes, 256), 256, 0, s>>>(
       ps->n_nodes, ps->nodes_per_patch, ps->node_patch_ptr, ps->node_patch_idx, Y, mask,
       reinterpret_cast<const float4*>(xt), scale, reinterpret_cast<float4*>(d),
-      reinterpret_cast<float4*>(xc), ps->node_order);
+      reinterpret_cast<float4*>(xc), ps->node_order, ps->node_order ? ps->visit_ptr : nullptr,
+      ps->visit_idx);
   DNNMG_CHECK_LAUNCH("scatter_update_kernel");
   return DNNMG_OK;
 }

@@ -608,12 +608,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
 __global__ void __launch_bounds__(256) node_sum_kernel(
     int n_nodes, const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const float4* __restrict__ elem, const float4* __restrict__ b, float sign,
-    const uint8_t* __restrict__ mask, float4* __restrict__ out, const int32_t* __restrict__ order) {
+    const uint8_t* __restrict__ mask, float4* __restrict__ out, const int32_t* __restrict__ order,
+    const int32_t* __restrict__ vptr, const int32_t* __restrict__ vidx) {
+  if (vptr) idx = vidx;   // rows in visiting order: the bounds load next to the node id
   for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < n_nodes;
        pos += gridDim.x * blockDim.x) {
     const int n = order ? __ldg(order + pos) : pos;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int s = __ldg(ptr + n), e = __ldg(ptr + n + 1);
+    const int s = vptr ? __ldg(vptr + pos) : __ldg(ptr + n);
+    const int e = vptr ? __ldg(vptr + pos + 1) : __ldg(ptr + n + 1);
     // the first 8 incident element vectors are loaded before any is summed (all in flight at
     // once); the sum stays in ascending cell order
     int ent[8];
@@ -837,7 +840,7 @@ int32_t launch_node_sum(int n_nodes, const int32_t* ptr, const int32_t* idx, con
   if (n_nodes == 0) return DNNMG_OK;
   node_sum_kernel<<<grid_for(n_nodes, 256), 256, 0, s>>>(
       n_nodes, ptr, idx, reinterpret_cast<const float4*>(elem), nullptr, 1.0f, nullptr,
-      reinterpret_cast<float4*>(out), nullptr);
+      reinterpret_cast<float4*>(out), nullptr, nullptr, nullptr);
   DNNMG_CHECK_LAUNCH("node_sum_kernel");
   return DNNMG_OK;
 }
@@ -881,7 +884,7 @@ int32_t launch_residual(const dnnmg_level_t* lv, const float* x, const float* b_
   node_sum_kernel<<<grid_for(lv->n_nodes, 256), 256, 0, s>>>(
       lv->n_nodes, lv->node_cell_ptr, lv->node_cell_idx, reinterpret_cast<const float4*>(elem), b,
       1.0f, (apply_mask && lv->dof_mask) ? lv->dof_mask : nullptr, reinterpret_cast<float4*>(r),
-      lv->node_order);
+      lv->node_order, lv->node_order ? lv->visit_ptr : nullptr, lv->visit_idx);
   DNNMG_CHECK_LAUNCH("node_sum_kernel");
   return DNNMG_OK;
 }

@@ -100,6 +100,19 @@ def visit_order(ptr_, idx):
     return order if mode == "forward" else order[::-1].copy()
 
 
+def visit_csr(ptr_, idx, order):
+    """The CSR rows in visiting order (row i = the row of node order[i]), or (None, None)
+    without an order."""
+    if order is None:
+        return None, None
+    ptr_ = np.asarray(ptr_, dtype=np.int64)
+    counts = (ptr_[1:] - ptr_[:-1])[order]
+    vptr = np.zeros(order.size + 1, dtype=np.int64)
+    np.cumsum(counts, out=vptr[1:])
+    src = np.repeat(ptr_[:-1][order] - vptr[:-1], counts) + np.arange(vptr[-1])
+    return vptr, np.asarray(idx)[src]
+
+
 TILE_ROWS = 128  # patches per tensor-core MLP tile (kTcM in csrc/mlp_tc.cu)
 
 
@@ -298,7 +311,10 @@ class DeviceLevel:
         p, idx = node_csr(space.cell_nodes)
         self.csr_ptr = upload(p, np.int32)
         self.csr_idx = upload(idx, np.int32)
-        self.order = upload_opt(visit_order(p, idx))
+        order = visit_order(p, idx)
+        self.order = upload_opt(order)
+        vp, vi = visit_csr(p, idx, order)
+        self.vptr, self.vidx = upload_opt(vp), upload_opt(vi)
         self.elem = None
         self.geo_kind = geometry_kind(lvl.vertices, lvl.cells)
         self.affine = self.geo_kind > 0
@@ -311,7 +327,7 @@ class DeviceLevel:
         lv = _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
                         ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask),
                         ptr(self.geometry()) if (geometry or tc) else None, ptr(self.order),
-                        None, None, 0)
+                        None, None, 0, ptr(self.vptr), ptr(self.vidx))
         if tc:
             lv.tc_const = ptr(k2tc_constants())
             lv.tc_geo = ptr(self.geometry_tc())
@@ -371,7 +387,10 @@ class DevicePatchSet:
             raise RuntimeError("patch union does not cover the fine level")
         self.csr_ptr = upload(p, np.int32)
         self.csr_idx = upload(idx, np.int32)
-        self.order = upload_opt(visit_order(p, idx))
+        order = visit_order(p, idx)
+        self.order = upload_opt(order)
+        vp, vi = visit_csr(p, idx, order)
+        self.vptr, self.vidx = upload_opt(vp), upload_opt(vi)
         tt = tile_tables(ps.node_table)
         self.tile_cap = 0
         self.tile_nodes = self.tile_count = self.tile_slot = None
@@ -385,7 +404,7 @@ class DevicePatchSet:
                                     ptr(self.node_table), ptr(self.geom), ptr(self.csr_ptr),
                                     ptr(self.csr_idx), self.tile_cap, ptr(self.tile_nodes),
                                     ptr(self.tile_count), ptr(self.tile_slot),
-                                    ptr(self.order))
+                                    ptr(self.order), ptr(self.vptr), ptr(self.vidx))
 
     @staticmethod
     def get(ps):

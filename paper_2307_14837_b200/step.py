@@ -300,6 +300,7 @@ class HostPipeline:
         self.s_in = torch.cuda.Stream(device=dev)
         self.s_runs = [torch.cuda.Stream(device=dev) for _ in range(lanes)]
         self.s_out = torch.cuda.Stream(device=dev)
+        self.split = self.db[0].numel() * 4 >= (4 << 20)   # fine RHS >= 4 MB
         self.ev_x = [torch.cuda.Event() for _ in range(depth)]
         self.ev_in = [torch.cuda.Event() for _ in range(depth)]
         self.ev_run = [torch.cuda.Event() for _ in range(depth)]
@@ -318,21 +319,24 @@ class HostPipeline:
         with torch.cuda.stream(self.s_in):
             if self._used[k]:
                 self.s_in.wait_event(self.ev_run[k])      # step i-depth has consumed dx/db[k]
-            # the coarse state first: prolongation and the element kernel run while the fine
-            # RHS (68 MB at config 3) is still in flight; the step waits for it right before
-            # the residual's node sum (dnnmg_step_buffers_t.b_ready)
+            # a large fine RHS (68 MB at config 3) is copied after the coarse state, and the
+            # step waits for it only right before the residual's node sum
+            # (dnnmg_step_buffers_t.b_ready): prolongation and the element kernel overlap it.
+            # (Small steps skip the split: the extra event costs more than it hides.)
             self.dx[k].copy_(x_host, non_blocking=True)
-            self.ev_x[k].record()
+            if self.split:
+                self.ev_x[k].record()
             self.db[k].copy_(b_host, non_blocking=True)
             self.ev_in[k].record()
         lane = self.i % len(self.steps)
         s_run = self.s_runs[lane]
         step = self.steps[lane]
         with torch.cuda.stream(s_run):
-            s_run.wait_event(self.ev_x[k])
+            s_run.wait_event(self.ev_x[k] if self.split else self.ev_in[k])
             if self._used[k]:
                 s_run.wait_event(self.ev_out[k])          # dout[k] has been copied out
-            step.buf.b_ready = self.ev_in[k].cuda_event
+            if self.split:
+                step.buf.b_ready = self.ev_in[k].cuda_event
             try:
                 step.run(self.dx[k], self.db[k], self.dout[k])
             finally:

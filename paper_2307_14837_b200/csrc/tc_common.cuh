@@ -54,13 +54,36 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// as mbar_try, but the waiting warp is suspended (up to `ns`) until the phase completes
+// instead of returning at once: a polling warp steals issue slots from the warps that
+// share its SM sub-partition
+#ifndef DNNMG_MBAR_SLEEP_NS
+#define DNNMG_MBAR_SLEEP_NS 1000
+#endif
+__device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "n"(DNNMG_MBAR_SLEEP_NS)
+      : "memory");
+  return ok != 0;
+}
 // bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
   uint32_t n = 0;
+#if DNNMG_MBAR_SLEEP_NS > 0
+  while (!mbar_try_sleep(bar, parity)) {
+    if (++n > (1u << 24)) __trap();
+  }
+#else
   while (!mbar_try(bar, parity)) {
     if (++n > (1u << 26)) __trap();
   }
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");

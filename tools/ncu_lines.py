@@ -3,14 +3,18 @@
 report (source page, cuda,sass view): the top lines, and totals over line ranges.
 
     python tools/ncu_lines.py report.ncu-rep [top] [a-b a-b ...]
+
+NCU_KERNEL=<regex> selects one kernel of a multi-kernel report.
 """
+import os
 import csv
 import subprocess
 import sys
 
 
 def load(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    sel = ["-k", "regex:" + os.environ["NCU_KERNEL"]] if os.environ.get("NCU_KERNEL") else []
+    out = subprocess.run(["ncu", "-i", path, *sel, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Line No")

@@ -1,7 +1,8 @@
 # Builds the sm_100a shared library libdnnmg_b200.so (C ABI: include/dnnmg_b200.h)
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -Xptxas -v
+EXTRA ?=
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -Xptxas -v $(EXTRA)
 SRC := $(wildcard paper_2307_14837_b200/csrc/*.cu)
 HDR := $(wildcard paper_2307_14837_b200/csrc/*.cuh) include/dnnmg_b200.h
 OBJ := $(patsubst paper_2307_14837_b200/csrc/%.cu,build/%.o,$(SRC))

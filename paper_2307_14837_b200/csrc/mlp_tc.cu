@@ -43,10 +43,21 @@ namespace dnnmg {
 
 constexpr int kTcH = 256;   // hidden width of the largest instantiation
 constexpr int kTcIn = 256;  // network inputs the fused kernel stages (n_in <= kTcIn)
-constexpr int kTcThreads = 352;
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kGatherWarp = 10;  // staged fused gather (GM_STAGED): cp.async of a tile's nodes
+// warp roles for NQ compute warps per TMEM lane quadrant (each takes KC / NQ columns of every
+// K chunk): 4 NQ compute warps, then the weight producer, the MMA issuer and the staged-gather
+// warp.  The staged fused gather runs NQ = 4 (16 compute warps at the 96-register budget: four
+// warps per sub-partition hide the epilogue's TMEM-load / MUFU / shared-store latencies; 0.68
+// -> 0.63 ms at config 3); the other layer-0 sources keep NQ = 2, whose 168-register budget
+// holds their prefetched input rows without spilling.
+template <int GM> struct TcRoles {
+  static constexpr int NQ = GM == 2 ? 4 : 2;
+  static constexpr int kComputeWarps = 4 * NQ;
+  static constexpr int kComputeThreads = 32 * kComputeWarps;
+  static constexpr int kProducerWarp = kComputeWarps;
+  static constexpr int kMmaWarp = kComputeWarps + 1;
+  static constexpr int kGatherWarp = kComputeWarps + 2;  // GM_STAGED: cp.async of a tile's nodes
+  static constexpr int kThreads = 32 * (kComputeWarps + 3);
+};
 // sources of the layer-0 operand
 enum { GM_X = 0,        // rows of a stored X
        GM_DIRECT = 1,   // fused gather: per-(patch, slot) global loads at the tile boundary
@@ -82,11 +93,19 @@ struct TcArgs {
   long long* trace;  // debug timeline of CTA 0 (env DNNMG_MLP_TRACE=file), else NULL
 };
 constexpr int kTraceSlots = 12288;
-// timeline probe (tools/mlp_trace.py): one clock64() sample per slot, CTA 0 only
+// timeline probe (tools/mlp_trace.py): one clock64() sample per slot, CTA 0 only.  Compiled
+// in only with -DDNNMG_MLP_TRACE_BUILD (tools/gpu/trace_mlp.sh): even when disabled at run
+// time, a probe's divergent branch in the chunk loop costs ~10 % of the kernel.
+#ifdef DNNMG_MLP_TRACE_BUILD
 #define TC_TRACE(slot)                                                              \
   do {                                                                              \
     if (A.trace && blockIdx.x == 0 && (slot) < kTraceSlots) A.trace[(slot)] = clock64();   \
   } while (0)
+#else
+#define TC_TRACE(slot) \
+  do {                 \
+  } while (0)
+#endif
 
 // shared-memory bytes of the GM_STAGED staging area: slot block, geometry rows, x~/r rows
 __host__ __device__ inline uint32_t staged_slot_bytes(int npp) { return (kTcM * npp * 2 + 15) / 16 * 16; }
@@ -95,11 +114,14 @@ __host__ __device__ inline uint32_t staged_bytes(int npp, int n_geo, int cap) {
 }
 
 template <int MODE, int GM, int H>
-__global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
+__global__ void __launch_bounds__(TcRoles<GM>::kThreads, 1) mlp_tc_kernel(TcArgs A) {
+  using R = TcRoles<GM>;
+  constexpr int kNQ = R::NQ, kComputeWarps = R::kComputeWarps, kComputeThreads = R::kComputeThreads;
+  constexpr int kProducerWarp = R::kProducerWarp, kMmaWarp = R::kMmaWarp, kGatherWarp = R::kGatherWarp;
   constexpr bool GATHER = GM != GM_X;
   using C = TcCfg<MODE>;
   constexpr int KC = C::KC;
-  constexpr int HC = KC / 2;                       // K columns per thread per chunk
+  constexpr int HC = KC / kNQ;                     // K columns per thread per chunk
   constexpr int NCH = H / KC;                      // chunks of a hidden layer
   constexpr int NCH0 = kTcIn / KC;                 // chunks of the (at most kTcIn) inputs
   constexpr int WST = H * KC * C::ESZ * C::PARTS;  // bytes per weight stage
@@ -162,17 +184,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       mbar_init(smem_u32(&w_empty[i]), 1);
     }
     for (int i = 0; i < C::NA; ++i) {
-      mbar_init(smem_u32(&a_full[i]), 8);
+      mbar_init(smem_u32(&a_full[i]), kComputeWarps);
       mbar_init(smem_u32(&a_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), 8);
+      mbar_init(smem_u32(&acc_empty[i]), kComputeWarps);
     }
     mbar_init(smem_u32(idx_full), 1);
-    mbar_init(smem_u32(idx_empty), 8);
+    mbar_init(smem_u32(idx_empty), kComputeWarps);
     mbar_init(smem_u32(stage_full), 1);
-    mbar_init(smem_u32(stage_empty), 8);
+    mbar_init(smem_u32(stage_empty), kComputeWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kProducerWarp) {
@@ -356,7 +378,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
   } else {
     // ---------------- compute warps ----------------
     const int quad = warp & 3;          // TMEM lane quadrant
-    const int hh = warp >> 2;           // which 16-column half of every 32-column chunk
+    const int hh = warp >> 2;           // which KC / kNQ column slice of every K chunk
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     constexpr bool accurate = MODE != DNNMG_PREC_BF16;
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
       const int s = aitem % C::NA;
       mbar_wait(smem_u32(&a_empty[s]), ((aitem / C::NA) & 1) ^ 1);
       if (warp == 0 && lane == 0) TC_TRACE(8192 + aitem);
-      put_row<MODE>(aring + s * AST, row_in_tile, HC * hh, v);
+      put_row<MODE, HC>(aring + s * AST, row_in_tile, HC * hh, v);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&a_full[s]));
@@ -538,7 +560,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           float v[HC];
+          if (warp == 0 && lane == 0) TC_TRACE(9216 + aitem);
           tmem_ld<HC>(tmem + lane_addr + buf * H + c * KC + HC * hh, v);
+          if (warp == 0 && lane == 0) TC_TRACE(10240 + aitem);
 #pragma unroll
           for (int e = 0; e < HC; e += 4) {
             const int col = c * KC + HC * hh + e;
@@ -562,6 +586,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
               v[e + u] = h[c][e + u];
             }
           }
+          if (warp == 0 && lane == 0) TC_TRACE(11264 + aitem);
           produce_chunk(c, v);
         }
         tc_fence_before();
@@ -589,14 +614,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
         if (A.y_mode == 3) {
           // the whole tile into the staging area (its nodes were consumed above: wait for all
           // compute warps), then one bulk store from the gather warp (stage_empty)
-          asm volatile("bar.sync 1, 256;" ::: "memory");
+          asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
           if (tile + gridDim.x >= n_tiles && tile >= (int64_t)gridDim.x) {
             // last tile of several: wait until the previous tile's Y has left the area
             mbar_wait(smem_u32(stage_full), sit & 1);
             ++sit;
           }
           float* ys = reinterpret_cast<float*>(st_base);
-          for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
+          for (int sl = hh; sl < A.Nhead / 16; sl += kNQ) {
             float v[16];
             tmem_ld16(tmem + lane_addr + buf * H + sl * 16, v);
 #pragma unroll
@@ -609,7 +634,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(stage_empty));
         } else if (A.y_mode == 0) {
-          for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
+          for (int sl = hh; sl < A.Nhead / 16; sl += kNQ) {
             float v[16];
             tmem_ld16(tmem + lane_addr + buf * H + sl * 16, v);
             if (live) {
@@ -630,7 +655,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
           if ((quad >> 1) == half) {
-            for (int sl = hh; sl < A.Nhead / 16; sl += 2) {
+            for (int sl = hh; sl < A.Nhead / 16; sl += kNQ) {
               float v[16];
               tmem_ld16(tmem + lane_addr + buf * H + sl * 16, v);
 #pragma unroll
@@ -641,18 +666,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_tc_kernel(TcArgs A) {
             }
           }
           tc_fence_before();
-          asm volatile("bar.sync 1, 256;" ::: "memory");
+          asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
           {  // coalesced copy of this half's contiguous Y block
             const int nh = nvalid - 64 * half;
             const int nf = (nh < 0 ? 0 : nh > 64 ? 64 : nh) * A.n_out;
             float* dst = A.Y + (r0 + 64 * half) * A.n_out;
             const int tid = threadIdx.x;
             const int n4 = nf >> 2;
-            for (int i = tid; i < n4; i += 256)
+            for (int i = tid; i < n4; i += kComputeThreads)
               reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(ys)[i];
-            for (int i = 4 * n4 + tid; i < nf; i += 256) dst[i] = ys[i];
+            for (int i = 4 * n4 + tid; i < nf; i += kComputeThreads) dst[i] = ys[i];
           }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
+          asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
         }
         }
         tc_fence_before();
@@ -894,19 +919,19 @@ static int32_t launch_mode(const dnnmg_mlp_t* m, const float* X, int64_t n_rows,
                   "mlp: the fused patch gather needs n_hidden == 256");
     cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_X, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    mlp_tc_kernel<MODE, GM_X, 128><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_X, 128><<<grid, TcRoles<GM_X>::kThreads, smem, s>>>(A);
   } else if (gm == GM_STAGED) {
     cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_STAGED, kTcH>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    mlp_tc_kernel<MODE, GM_STAGED, kTcH><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_STAGED, kTcH><<<grid, TcRoles<GM_STAGED>::kThreads, smem, s>>>(A);
   } else if (gm == GM_DIRECT) {
     cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_DIRECT, kTcH>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    mlp_tc_kernel<MODE, GM_DIRECT, kTcH><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_DIRECT, kTcH><<<grid, TcRoles<GM_DIRECT>::kThreads, smem, s>>>(A);
   } else {
     cudaFuncSetAttribute(mlp_tc_kernel<MODE, GM_X, kTcH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    mlp_tc_kernel<MODE, GM_X, kTcH><<<grid, kTcThreads, smem, s>>>(A);
+    mlp_tc_kernel<MODE, GM_X, kTcH><<<grid, TcRoles<GM_X>::kThreads, smem, s>>>(A);
   }
   DNNMG_CHECK_LAUNCH("mlp_tc_kernel");
   if (A.trace) {  // debug only: synchronous copy-out of CTA 0's timeline

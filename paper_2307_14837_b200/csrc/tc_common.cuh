@@ -174,10 +174,21 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
 template <int N>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float* v) {
+  static_assert(N == 16 || N == 8 || N == 4, "tmem_ld width");
   if constexpr (N == 16) tmem_ld16(taddr, v);
-  else tmem_ld8(taddr, v);
+  else if constexpr (N == 8) tmem_ld8(taddr, v);
+  else tmem_ld4(taddr, v);
 }
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t r;
@@ -247,11 +258,13 @@ __host__ __device__ constexpr uint32_t canon_off(int row, int kk) {
                     (kk % (16 / ESZ)) * ESZ);
 }
 
-// write KC/2 consecutive K values (kk0.., kk0 % (KC/2) == 0) of one row into an A stage
-template <int MODE>
+// write NV (default KC/2) consecutive K values (kk0.., kk0 % NV == 0) of one row into an A stage
+template <int MODE, int NV = TcCfg<MODE>::KC / 2>
 __device__ __forceinline__ void put_row(uint8_t* stage, int row, int kk0, const float* v) {
   using C = TcCfg<MODE>;
-  constexpr int HC = C::KC / 2;
+  constexpr int HC = NV;
+  static_assert(MODE == DNNMG_PREC_FP8 ? NV % 16 == 0
+                : MODE == DNNMG_PREC_TF32X3 ? NV % 4 == 0 : NV % 8 == 0, "put_row width");
   if constexpr (MODE == DNNMG_PREC_FP8) {
 #pragma unroll
     for (int j = 0; j < HC / 16; ++j) {

@@ -14,14 +14,17 @@ print("items", n)
 g_per_tile = len(nk)
 k = 0
 j = 0
-for tile in range(3):
+for tile in range(5):
     for g in range(g_per_tile):
         rows = items[k:k + nk[g]] - t0
         print(f"tile {tile} gemm {g}: epi acc_full@{acc[j] - t0 if acc[j] else -1}")
         for c, r in enumerate(rows):
             ae = t[8192 + k + c] - t0 if t.size > 8192 and t[8192 + k + c] else -1
+            # hidden epilogues: tmem_ld issued / data ready / math done (warp 0)
+            ls, lr, md = (t[b + k + c] - t0 if t[b + k + c] else -1 for b in (9216, 10240, 11264))
+            ext = f" | ld@{ls:7d} ready+{lr - ls:4d} math+{md - lr:4d} slot+{ae - md:4d}" if ls >= 0 else ""
             print(f"   c{c}: mma_wait@{r[0]:7d} a_full@{r[1]:7d} (+{r[1]-r[0]:5d}) issued@{r[2]:7d} "
-                  f"producer a_empty ok@{ae:7d} arrive@{r[3]:7d}")
+                  f"producer a_empty ok@{ae:7d} arrive@{r[3]:7d}{ext}")
         k += nk[g]
         j += 1
 tot = items[n - 1, 2] - t0

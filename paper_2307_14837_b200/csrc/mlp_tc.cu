@@ -143,20 +143,19 @@ __global__ void __launch_bounds__(TcRoles<GM>::kThreads, 1) mlp_tc_kernel(TcArgs
   uint64_t* stage_empty = stage_full + 1; // GM_STAGED: staging area free (layer 0 consumed it,
                                           // or, y_mode 3, the previous tile's Y written to it)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stage_empty + 1);
-  // BN scale/shift per hidden layer and the input normalisation, staged once per CTA
-  float* p_scale = reinterpret_cast<float*>(tmem_slot + 4);
-  float* p_shift = p_scale + A.depth * H;
+  // BN shift per hidden layer and the input normalisation, staged once per CTA.  The BN scale
+  // (times k2 below) is folded into the packed weight columns (pack_kernel), so a hidden
+  // epilogue computes z = acc * 2^-s_g + shift' with one warp-uniform factor per layer and
+  // reads only the shift from shared memory.
+  float* p_shift = reinterpret_cast<float*>(tmem_slot + 4);
   float* p_mean = p_shift + A.depth * H;
   float* p_rstd = p_mean + kTcIn;
   const PackHdr* hdr = reinterpret_cast<const PackHdr*>(A.packed);
   // fp32-accuracy tanh takes 2^(2 log2(e) z): fold 2 log2(e) into the BN scale and shift so
   // that the epilogue needs one FFMA before ex2 (the activation never needs z itself)
-  const bool fold = MODE != DNNMG_PREC_BF16 && A.act == DNNMG_ACT_TANH;
-  const float k2 = fold ? 2.8853900817779268f : 1.0f;
-  for (int i = threadIdx.x; i < A.depth * H; i += blockDim.x) {
-    p_scale[i] = A.scale[i] * hdr->unscale[i / H] * k2;  // 2^-s: exact
-    p_shift[i] = A.shift[i] * k2;
-  }
+  const bool fold = tanh_folded(MODE, A.act);
+  const float k2 = fold ? kTanhK2 : 1.0f;
+  for (int i = threadIdx.x; i < A.depth * H; i += blockDim.x) p_shift[i] = A.shift[i] * k2;
   const float y_unscale = hdr->unscale[A.depth];
   int32_t* idx_s = reinterpret_cast<int32_t*>(p_rstd + kTcIn);  // [kTcM][npp] (GM_DIRECT only)
   // GM_STAGED: slot block [kTcM][npp] u16 | geometry rows [kTcM][n_geo] | x~ [cap] | r [cap]
@@ -555,7 +554,7 @@ __global__ void __launch_bounds__(TcRoles<GM>::kThreads, 1) mlp_tc_kernel(TcArgs
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
         if (warp == 0 && lane == 0) TC_TRACE(6144 + j);
         tc_fence_after();
-        const float* sc = p_scale + g * H;
+        const float us = hdr->unscale[g];  // 2^-s_g: exact
         const float* sh = p_shift + g * H;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
@@ -566,13 +565,11 @@ __global__ void __launch_bounds__(TcRoles<GM>::kThreads, 1) mlp_tc_kernel(TcArgs
 #pragma unroll
           for (int e = 0; e < HC; e += 4) {
             const int col = c * KC + HC * hh + e;
-            const float4 s4 = *reinterpret_cast<const float4*>(sc + col);
             const float4 t4 = *reinterpret_cast<const float4*>(sh + col);
-            const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
             const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float z = fmaf(v[e + u], sv[u], tv[u]);
+              const float z = fmaf(v[e + u], us, tv[u]);
               float a;
               if (fold) {  // z = 2 log2(e) * BN(acc): tanh = 1 - 2 / (1 + 2^z)
                 float ez, r;
@@ -697,11 +694,14 @@ __global__ void __launch_bounds__(TcRoles<GM>::kThreads, 1) mlp_tc_kernel(TcArgs
 }
 
 // ---- weight packing: W[g] (K x N row-major fp32) -> canonical chunk images -----
-// per-GEMM exponent s with max|W| 2^s < 2^14 (F16X3), else s = 0; one block
-__global__ void pack_scale_kernel(const float* __restrict__ W, int size, int mode, int g,
+// per-GEMM exponent s with max|W'| 2^s < 2^14 (F16X3), else s = 0; one block.  W' = W, or
+// for the fused kernel's hidden GEMMs W with column n scaled by colf[n] * k2 (BN scale fold)
+__global__ void pack_scale_kernel(const float* __restrict__ W, int size, int N,
+                                  const float* __restrict__ colf, float k2, int mode, int g,
                                   PackHdr* __restrict__ hdr) {
   float m = 0.f;
-  for (int i = threadIdx.x; i < size; i += blockDim.x) m = fmaxf(m, fabsf(W[i]));
+  for (int i = threadIdx.x; i < size; i += blockDim.x)
+    m = fmaxf(m, fabsf(colf ? W[i] * (colf[i % N] * k2) : W[i]));
   __shared__ float red[32];
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -722,6 +722,7 @@ __global__ void pack_scale_kernel(const float* __restrict__ W, int size, int mod
 
 template <int MODE>
 __global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, int Np,
+                            const float* __restrict__ colf, float k2,
                             const PackHdr* __restrict__ hdr, int g, uint8_t* __restrict__ out) {
   const int shift = hdr->shift[g];
   using C = TcCfg<MODE>;
@@ -732,7 +733,8 @@ __global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, i
        i += (int64_t)gridDim.x * blockDim.x) {
     const int n = (int)(i % Np);
     const int k = (int)(i / Np);
-    const float w = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
+    float w = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
+    if (colf && n < N) w *= colf[n] * k2;
     const int c = k / KC, kk = k % KC;
     uint8_t* chunk = out + (int64_t)c * part * C::PARTS;
     const uint32_t off = canon_off<C::ESZ, KC>(n, kk);
@@ -752,11 +754,15 @@ __global__ void pack_kernel(const float* __restrict__ W, int K, int N, int Kp, i
   }
 }
 
-// per-GEMM weight exponents into the header of a packed image (shared with mlp_layer.cu)
-int32_t launch_pack_scales(const dnnmg_mlp_t* m, PackHdr* hdr, cudaStream_t s) {
+// per-GEMM weight exponents into the header of a packed image (shared with mlp_layer.cu;
+// fold_bn: exponents of the BN-scale-folded hidden weights of the fused kernel)
+int32_t launch_pack_scales(const dnnmg_mlp_t* m, PackHdr* hdr, cudaStream_t s, bool fold_bn) {
+  const float k2 = tanh_folded(m->precision, m->activation) ? kTanhK2 : 1.0f;
   for (int g = 0; g <= m->depth; ++g) {
-    const int size = (g == 0 ? m->n_in : m->n_hidden) * (g < m->depth ? m->n_hidden : m->n_out);
-    pack_scale_kernel<<<1, 256, 0, s>>>(m->W[g], size, m->precision, g, hdr);
+    const int N = g < m->depth ? m->n_hidden : m->n_out;
+    const int size = (g == 0 ? m->n_in : m->n_hidden) * N;
+    const float* colf = fold_bn && g < m->depth ? m->bn_scale + (int64_t)g * m->n_hidden : nullptr;
+    pack_scale_kernel<<<1, 256, 0, s>>>(m->W[g], size, N, colf, k2, m->precision, g, hdr);
     DNNMG_CHECK_LAUNCH("pack_scale_kernel");
   }
   return DNNMG_OK;
@@ -802,10 +808,12 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
   layout(m, goff, &total);
   PackHdr* hdr = static_cast<PackHdr*>(packed);
   static_assert(sizeof(PackHdr) <= kPackHdr, "pack header");
-  int32_t rc = launch_pack_scales(m, hdr, s);
+  int32_t rc = launch_pack_scales(m, hdr, s, true);
   if (rc) return rc;
+  const float k2 = tanh_folded(m->precision, m->activation) ? kTanhK2 : 1.0f;
   for (int g = 0; g <= m->depth; ++g) {
     const int H = m->n_hidden;
+    const float* colf = g < m->depth ? m->bn_scale + (int64_t)g * H : nullptr;
     const int K = g == 0 ? m->n_in : H;
     const int N = g < m->depth ? H : m->n_out;
     const int Kp = g == 0 ? round_up(m->n_in, kc_of(m->precision)) : H;
@@ -813,11 +821,11 @@ int32_t launch_mlp_tc_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
     uint8_t* out = static_cast<uint8_t*>(packed) + goff[g];
     const int64_t n = (int64_t)Kp * Np;
     if (m->precision == DNNMG_PREC_BF16)
-      pack_kernel<DNNMG_PREC_BF16><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, hdr, g, out);
+      pack_kernel<DNNMG_PREC_BF16><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, colf, k2, hdr, g, out);
     else if (m->precision == DNNMG_PREC_F16X3)
-      pack_kernel<DNNMG_PREC_F16X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, hdr, g, out);
+      pack_kernel<DNNMG_PREC_F16X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, colf, k2, hdr, g, out);
     else
-      pack_kernel<DNNMG_PREC_TF32X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, hdr, g, out);
+      pack_kernel<DNNMG_PREC_TF32X3><<<grid_for(n, 256), 256, 0, s>>>(m->W[g], K, N, Kp, Np, colf, k2, hdr, g, out);
     DNNMG_CHECK_LAUNCH("pack_kernel");
   }
   return DNNMG_OK;
@@ -842,7 +850,7 @@ static size_t smem_base(const dnnmg_mlp_t* m) {
   const size_t WST = (size_t)m->n_hidden * C::KC * C::ESZ * C::PARTS;
   constexpr int AST = kTcM * C::KC * C::ESZ * C::PARTS;
   return (size_t)C::NW * WST + (size_t)C::NA * AST + 8 * (2 * C::NW + 2 * C::NA + 8) + 16 +
-         sizeof(float) * (2 * (size_t)m->depth * m->n_hidden + 2 * kTcIn);
+         sizeof(float) * ((size_t)m->depth * m->n_hidden + 2 * kTcIn);
 }
 static size_t smem_base_of(const dnnmg_mlp_t* m) {
   return m->precision == DNNMG_PREC_BF16 ? smem_base<DNNMG_PREC_BF16>(m)

@@ -15,7 +15,14 @@ struct PackHdr {
   float unscale[DNNMG_MAX_LAYERS];
   int32_t shift[DNNMG_MAX_LAYERS];
 };
-int32_t launch_pack_scales(const dnnmg_mlp_t* m, PackHdr* hdr, cudaStream_t s);
+int32_t launch_pack_scales(const dnnmg_mlp_t* m, PackHdr* hdr, cudaStream_t s,
+                           bool fold_bn = false);
+// fp32-accurate tanh evaluates 1 - 2 / (1 + 2^z) with z = 2 log2(e) x: the factor is folded
+// into the epilogue affine (and, in the fused kernel, into the packed hidden weights)
+constexpr float kTanhK2 = 2.8853900817779268f;
+__host__ __device__ constexpr bool tanh_folded(int precision, int act) {
+  return precision != DNNMG_PREC_BF16 && act == DNNMG_ACT_TANH;
+}
 
 template <int MODE> struct TcCfg;
 // KC: K elements per pipeline chunk (one TMA weight copy, one A-ring stage);

@@ -210,7 +210,9 @@ struct Args {
   unsigned long long* trace;   // DNNMG_K2TC_TRACE: clock64 stamps of CTA 0's first tiles
   uint32_t* cmax;              // DNNMG_K2TC_CMAX: per cell max |scaled coefficient| (diagnostic)
 };
-// trace slots: [tile][stage][4]: forward warp 0 top / issued, backward warp 0 ready / issued
+// trace slots: [tile][stage][4]: forward warp 0 top / issued, backward warp 0 ready / issued.
+// The timeline stamps and the cmax diagnostic are compiled in only with
+// -DDNNMG_K2TC_DIAG_BUILD (make EXTRA=...): their run-time branches cost the hot loops.
 #define K2_TRACE(slot) \
   do { if (A.trace && blockIdx.x == 0) A.trace[(slot)] = clock64(); } while (0)
 
@@ -562,8 +564,12 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
         for (int it = 0; it < n_mine; ++it) {
           mbar_sleep(smem_u32(b_af), it & 1);
           tc_fence_after();
+#ifdef DNNMG_K2TC_DIAG_BUILD
           unsigned long long* tr =
               A.trace && blockIdx.x == 0 && it < 4 && role == 0 ? A.trace + it * kStages * 4 : nullptr;
+#else
+          constexpr unsigned long long* tr = nullptr;
+#endif
 #define FWD(S)                                                                                   \
   if (role == 0) fwd_stage<S, 0>(bars, lo_bf, tr);                                              \
   else fwd_stage<S, 2>(bars, lo_bf, nullptr);
@@ -574,7 +580,11 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
       } else {
         const uint32_t lo_tb = s0 + (oTB >> 4);                         // LBO 0
         for (int it = 0; it < n_mine; ++it) {
+#ifdef DNNMG_K2TC_DIAG_BUILD
           unsigned long long* tr = (role == 2 && A.trace && blockIdx.x == 0 && it < 4) ? A.trace + it * kStages * 4 : nullptr;
+#else
+          constexpr unsigned long long* tr = nullptr;
+#endif
 #define BWD(S)                                                                                   \
   if (role == 2) bwd_stage<S, 0>(bars, lo_tb, it, tr);                                          \
   else bwd_stage<S, 2>(bars, lo_tb, it, nullptr);
@@ -862,6 +872,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
         uint32_t wv[32];
         point_coeffs<MODE, GEO>(A, F, PQ, Ji, w * sB, (w - kWq[q] * det) * sB, aT, dT, cf);
         split_coeffs(cf, wv);
+#ifdef DNNMG_K2TC_DIAG_BUILD
         if (A.cmax && valid) {   // diagnostic: the largest scaled coefficient of this point
           float mxc = 0.f;
 #pragma unroll
@@ -870,6 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1) k2tc_kernel(Args A) {
             for (int k = 0; k < 7; ++k) mxc = fmaxf(mxc, fabsf(cf[i][k]));
           atomicMax(A.cmax + cell, __float_as_uint(mxc));
         }
+#endif
         // the backward A operand is free once the previous stage's MMAs have completed
         mbar_sleep(smem_u32(b_ab_free), (s & 1) ^ 1);
         tc_fence_after();

@@ -22,7 +22,8 @@ for i in range(len(pr.solves["t"])):
     d = np.abs(outs[True][1] - outs[False][1]).max(axis=(1, 2))
     xv = x_corr.double().cpu().numpy().reshape(-1, 4)
     print(i, n, "rel %.2e" % rel(outs[True][0], outs[False][0]), "cell max diff", np.round(d, 5)[:16], "|v|max %.2f" % np.abs(xv[:, 1:]).max())
-# per-cell max |scaled coefficient| of the tensor-core kernel (DNNMG_K2TC_CMAX)
+# per-cell max |scaled coefficient| of the tensor-core kernel (DNNMG_K2TC_CMAX; needs a library
+# built with `make EXTRA=-DDNNMG_K2TC_DIAG_BUILD`)
 cm = torch.zeros(lvl.n_cells, dtype=torch.int32, device="cuda")
 os.environ["DNNMG_K2TC_CMAX"] = str(cm.data_ptr())
 lv = lvl.struct(None, geometry=True, tc=True)

@@ -1,4 +1,5 @@
-"""CTA-0 timeline of the tensor-core K2 (DNNMG_K2TC_TRACE): per stage the MMA lane's and
+"""CTA-0 timeline of the tensor-core K2 (DNNMG_K2TC_TRACE; needs a library built with
+`make EXTRA=-DDNNMG_K2TC_DIAG_BUILD`): per stage the MMA lane's and
 compute warps 0 / 15's stamps (cycles from the first MMA stamp), printed by the library
 to stderr.   python tools/gpu/k2_trace.py [64x32x32]"""
 import ctypes, os, sys

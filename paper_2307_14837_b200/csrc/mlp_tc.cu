@@ -254,8 +254,12 @@ __global__ void __launch_bounds__(TcRoles<GM>::kThreads, 1) mlp_tc_kernel(TcArgs
           mbar_wait(smem_u32(&acc_empty[buf]), ((j >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + buf * H;
+          // layer 0: k-steps wholly inside the zero padding of K0p (n_in = 240 -> 256 at
+          // KC = 32) are skipped; their products are exact zeros
+          const int nks_last = g == 0 ? (A.n_in - (nk - 1) * KC + C::KSTEP - 1) / C::KSTEP : KC / C::KSTEP;
           for (int c = 0; c < nk; ++c, ++witem, ++aitem) {
             const int sw = witem % C::NW, sa = aitem % C::NA;
+            const int nks = c == nk - 1 ? nks_last : KC / C::KSTEP;
             mbar_wait(smem_u32(&w_full[sw]), (witem / C::NW) & 1);
             TC_TRACE(4 * aitem);
             mbar_wait(smem_u32(&a_full[sa]), (aitem / C::NA) & 1);
@@ -265,6 +269,7 @@ __global__ void __launch_bounds__(TcRoles<GM>::kThreads, 1) mlp_tc_kernel(TcArgs
             const uint32_t ab = smem_u32(aring + sa * AST);
 #pragma unroll
             for (int ks = 0; ks < KC / C::KSTEP; ++ks) {
+              if (ks >= nks) break;
               const uint32_t koff = ks * 256;
               const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
               const uint64_t ahi = sdesc(ab + koff, SBO), bhi = sdesc(wb + koff, SBO);

@@ -155,6 +155,12 @@ typedef struct {
      its row bounds without first resolving the node id (one dependent load fewer) */
   const int32_t* visit_ptr;      /* [n_nodes+1] */
   const int32_t* visit_idx;
+  /* optional, for a level whose cells are all axis-aligned boxes (an unjittered box mesh):
+     the per-cell record of dnnmg_level_geometry_box, [n_cells][4] = (1/hx, 1/hy, 1/hz, det J).
+     J^-1 is then diagonal and constant over a cell, and K2's element kernel takes its box form
+     (no per-point geometry, no products with the zero off-diagonal entries); it takes
+     precedence over geo_q.  Set it only when dnnmg_level_geometry_box reported 0 bad cells. */
+  const float* geo_box;
 } dnnmg_level_t;
 
 typedef struct {
@@ -222,6 +228,12 @@ int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* b_fine, float* b_
 /* geometry cache of a level (constant mesh): geo_out = [n_cells][10][64] float32, i.e.
  * 2,560 bytes per cell; set lv->geo_q = geo_out to let K2 skip the geometry work */
 int32_t dnnmg_level_geometry(const dnnmg_level_t* lv, float* geo_out, dnnmg_stream_t stream);
+/* box record of a level (see dnnmg_level_t.geo_box): box_out = [n_cells][4] float32 (16-byte
+ * aligned); *n_bad_dev (device int32, nullable) receives the number of cells that are not
+ * axis-aligned boxes with their 27 nodes on the tri-quadratic lattice (tolerance 1e-12 of the
+ * cell size, fp64) -- use the record only when it is 0. */
+int32_t dnnmg_level_geometry_box(const dnnmg_level_t* lv, float* box_out, int32_t* n_bad_dev,
+                                 dnnmg_stream_t stream);
 /* Tensor-core K2 (element vectors as tcgen05 GEMMs, SURVEY App. C "K2 v2"): the constant
  * operand image (Q2 basis / gradient / projected-gradient tables at the Gauss points, fp16
  * hi/lo, 160 KB, device buffer 128-byte aligned) and the geometry in the kernel's layout:

@@ -37,7 +37,7 @@ class Level(ctypes.Structure):
                 ("h_T", c_vp), ("node_cell_ptr", c_vp), ("node_cell_idx", c_vp),
                 ("dof_mask", c_vp), ("geo_q", c_vp), ("node_order", c_vp),
                 ("tc_const", c_vp), ("tc_geo", c_vp), ("tc_geo_affine", c_i32),
-                ("visit_ptr", c_vp), ("visit_idx", c_vp)]
+                ("visit_ptr", c_vp), ("visit_idx", c_vp), ("geo_box", c_vp)]
 
 
 class Phys(ctypes.Structure):
@@ -100,6 +100,7 @@ EXPORTS = {
     "dnnmg_apply_dirichlet": (c_i32, [ctypes.POINTER(Dirichlet), c_vp, c_vp]),
     "dnnmg_restrict": (c_i32, [ctypes.POINTER(Restrict), c_vp, c_vp, c_vp]),
     "dnnmg_level_geometry": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp]),
+    "dnnmg_level_geometry_box": (c_i32, [ctypes.POINTER(Level), c_vp, c_vp, c_vp]),
     "dnnmg_k2tc_constants_bytes": (c_i64, []),
     "dnnmg_k2tc_constants": (c_i32, [c_vp, c_vp]),
     "dnnmg_level_geometry_tc_floats": (c_i64, [ctypes.POINTER(Level), c_i32]),

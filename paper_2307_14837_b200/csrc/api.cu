@@ -22,6 +22,7 @@ int32_t launch_restrict(const dnnmg_restrict_t*, const float*, float*, cudaStrea
 int32_t launch_level_geometry(const dnnmg_level_t*, float*, cudaStream_t);
 int64_t k2tc_constant_bytes();
 int32_t launch_k2tc_constants(void*, cudaStream_t);
+int32_t launch_level_geometry_box(const dnnmg_level_t*, float*, int32_t*, cudaStream_t);
 int32_t launch_k2tc_geometry(const dnnmg_level_t*, float*, int32_t, cudaStream_t);
 int32_t launch_stab(const dnnmg_level_t*, const float*, const dnnmg_phys_t*, float*, float*,
                     cudaStream_t);
@@ -105,6 +106,11 @@ int32_t dnnmg_restrict(const dnnmg_restrict_t* R, const float* bf, float* bc, dn
 
 int32_t dnnmg_level_geometry(const dnnmg_level_t* lv, float* geo, dnnmg_stream_t s) {
   return launch_level_geometry(lv, geo, as_stream(s));
+}
+
+int32_t dnnmg_level_geometry_box(const dnnmg_level_t* lv, float* box, int32_t* n_bad,
+                                 dnnmg_stream_t s) {
+  return launch_level_geometry_box(lv, box, n_bad, as_stream(s));
 }
 
 int64_t dnnmg_k2tc_constants_bytes(void) { return k2tc_constant_bytes(); }

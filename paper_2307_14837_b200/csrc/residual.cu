@@ -87,14 +87,18 @@ static_assert(oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 // Layout of the geometry-cached form: J^-1 and w per Gauss point come from a per-mesh
 // cache (geometry_kernel), so only p and v (4 fields) go through the forward stages and
 // the cell's cached block [10][64] is staged by cp.async one cell ahead.
-template <bool CACHED>
+// GEO: 0 = geometry recomputed per call, 1 = per-point cache staged per cell, 2 = per-cell box
+// record (axis-aligned cells: J^-1 diagonal and constant over the cell, nothing staged)
+enum { GEO_NONE = 0, GEO_CACHED = 1, GEO_BOX = 2 };
+template <int GEO>
 struct KLay {
+  static constexpr bool CACHED = GEO != GEO_NONE;
   static constexpr int NF = CACHED ? 4 : kNF;         // Q2 fields through the forward stages
   static constexpr int FO = NF - 4;                    // index of p among them
   static constexpr int oCF = oSY + NF * kSYF;
   static constexpr int oGQ = oCF + kNCF * kCFS;        // cached [J^-1 (9) | w][64]
   static constexpr int oBar = oGQ + 10 * 64;           // cached: the staging mbarrier (8 B)
-  static constexpr int kFloats = (oGQ + (CACHED ? 10 * 64 + 4 : 0) + 3) / 4 * 4;
+  static constexpr int kFloats = (oGQ + (GEO == GEO_CACHED ? 10 * 64 + 4 : 0) + 3) / 4 * 4;
   static_assert(oTZ + 4 * 2 * 27 <= oCF && oCF % 4 == 0 && oGQ % 4 == 0, "layout");
 };
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
@@ -116,6 +120,7 @@ struct ResidualArgs {
   float nu, k, alpha0, delta0;
   float ik;  // 1/k
   const float* geo_q;  // per-mesh geometry cache [n_cells][10][64] (J^-1 row-major, w) or NULL
+  const float4* geo_box;  // per-cell (1/hx, 1/hy, 1/hz, det J) of an axis-aligned level or NULL
   int convection;
   int mode;
   float4* elem;
@@ -143,12 +148,14 @@ __host__ __device__ constexpr float pi_weight(int b, int v) {
 struct NodeRaw {
   double X[3], X0[3];
   float4 xv;
+  float4 gb;  // GEO_BOX: the cell's box record
   float hT;
 };
 
-template <bool CACHED>
+template <int GEO>
 __device__ __forceinline__ void load_raw(const ResidualArgs& A, int c, int node, int t, NodeRaw& r) {
-  if constexpr (!CACHED) {
+  if constexpr (GEO == GEO_BOX) r.gb = __ldg(A.geo_box + c);
+  if constexpr (GEO == GEO_NONE) {
     const int n0 = __shfl_sync(0xffffffffu, node, 0);
     const double* X = A.coords + 3 * (int64_t)node;
     const double* X0 = A.coords + 3 * (int64_t)n0;
@@ -229,52 +236,41 @@ __device__ __forceinline__ void pi_fields(const float* u, const float4* vtx, int
   }
 }
 
-// coefficients of one Gauss point (pointwise phase); F = Q2 fields at q, PQ = pi fields at q
-template <int MODE, bool CACHED>
-__device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S, float* CF, int q,
-                                          float F[KLay<CACHED>::NF][4], const float PQ[4][4],
-                                          float aT, float dT) {
-  using L = KLay<CACHED>;
-  constexpr int FO = L::FO;
-  const int qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
+// coefficients of one Gauss point (pointwise phase); F = Q2 fields at q, PQ = pi fields at q.
+// JM abstracts J^-1: full 3x3 (recomputed or cached per point) or the diagonal of a box cell,
+// where every product with an off-diagonal entry is dropped (exact: those entries are zero)
+struct JFull {
   float Ji[3][3];  // (J^-1)[k][j]: reference k -> physical j
-  float w;
-  if constexpr (CACHED) {
-    const float* G = S + L::oGQ;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) Ji[k][j] = G[(3 * k + j) * 64 + q];
-    w = G[9 * 64 + q];
-  } else {
-    float J[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) J[i][j] = F[i][1 + j];
-    const float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-    const float c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-    const float c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-    const float det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-    const float id = 1.0f / det;
-    Ji[0][0] = c00 * id;
-    Ji[1][0] = c01 * id;
-    Ji[2][0] = c02 * id;
-    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
-    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
-    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
-    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
-    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
-    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
-    w = cW[qx] * cW[qy] * cW[qz] * det;
+  // physical gradient from reference derivatives d[0..2]: sum_k d[k] Ji[k][j]
+  __device__ __forceinline__ float phys(const float d0, const float d1, const float d2, int j) const {
+    return d0 * Ji[0][j] + d1 * Ji[1][j] + d2 * Ji[2][j];
   }
+  // reference component k of J^-1 applied to a physical vector
+  __device__ __forceinline__ float ref(const float e0, const float e1, const float e2, int k) const {
+    return Ji[k][0] * e0 + Ji[k][1] * e1 + Ji[k][2] * e2;
+  }
+};
+struct JBox {
+  float s[3];  // (J^-1)[k][k]
+  __device__ __forceinline__ float phys(const float d0, const float d1, const float d2, int j) const {
+    return (j == 0 ? d0 : j == 1 ? d1 : d2) * s[j];
+  }
+  __device__ __forceinline__ float ref(const float e0, const float e1, const float e2, int k) const {
+    return s[k] * (k == 0 ? e0 : k == 1 ? e1 : e2);
+  }
+};
+
+template <int MODE, int NF, int FO, class JM>
+__device__ __forceinline__ void pointwise_core(const ResidualArgs& A, float* CF, int q, const JM& M,
+                                               float w, float F[NF][4], const float PQ[4][4],
+                                               float aT, float dT) {
   float v[3], gv[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     v[i] = F[FO + 1 + i][0];
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      gv[i][j] = F[FO + 1 + i][1] * Ji[0][j] + F[FO + 1 + i][2] * Ji[1][j] + F[FO + 1 + i][3] * Ji[2][j];
+      gv[i][j] = M.phys(F[FO + 1 + i][1], F[FO + 1 + i][2], F[FO + 1 + i][3], j);
   }
   float conv[3];
 #pragma unroll
@@ -288,16 +284,13 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
     const float dd0 = F[FO][1] - PQ[0][1], dd1 = F[FO][2] - PQ[0][2], dd3 = F[FO][3] - PQ[0][3];
     float gdp[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) gdp[j] = dd0 * Ji[0][j] + dd1 * Ji[1][j] + dd3 * Ji[2][j];
+    for (int j = 0; j < 3; ++j) gdp[j] = M.phys(dd0, dd1, dd3, j);
     const bool use_d = A.convection && dT != 0.f;
     float g[3] = {0.f, 0.f, 0.f}, pvr[3] = {0.f, 0.f, 0.f};
     if (use_d) {
-      float pv[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) pv[i] = PQ[1 + i][0];
       // pvr = J^-1 pi v; (pi v . grad) pi v_i = sum_m d(pi v_i)/dxi_m pvr_m
 #pragma unroll
-      for (int kk = 0; kk < 3; ++kk) pvr[kk] = Ji[kk][0] * pv[0] + Ji[kk][1] * pv[1] + Ji[kk][2] * pv[2];
+      for (int kk = 0; kk < 3; ++kk) pvr[kk] = M.ref(PQ[1][0], PQ[2][0], PQ[3][0], kk);
 #pragma unroll
       for (int i = 0; i < 3; ++i)
         g[i] = conv[i] - (PQ[1 + i][1] * pvr[0] + PQ[1 + i][2] * pvr[1] + PQ[1 + i][3] * pvr[2]);
@@ -308,7 +301,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
     for (int j = 0; j < 3; ++j) E[j] = aT * w * gdp[j];
     CFW(CA + 0) = w * div;
 #pragma unroll
-    for (int kk = 0; kk < 3; ++kk) CFW(CB + kk) = Ji[kk][0] * E[0] + Ji[kk][1] * E[1] + Ji[kk][2] * E[2];
+    for (int kk = 0; kk < 3; ++kk) CFW(CB + kk) = M.ref(E[0], E[1], E[2], kk);
     const float hn = 0.5f * A.nu * w;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -320,8 +313,7 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 #pragma unroll
       for (int j = 0; j < 3; ++j) Fi[j] = hn * gv[i][j] + dg * v[j] - (i == j ? w * p : 0.f);
 #pragma unroll
-      for (int kk = 0; kk < 3; ++kk)
-        CFW(CB + 3 * (1 + i) + kk) = Ji[kk][0] * Fi[0] + Ji[kk][1] * Fi[1] + Ji[kk][2] * Fi[2];
+      for (int kk = 0; kk < 3; ++kk) CFW(CB + 3 * (1 + i) + kk) = M.ref(Fi[0], Fi[1], Fi[2], kk);
     }
   } else {  // MODE_RHS (assembly.py:242-259, f = None)
     const float hn = -0.5f * A.nu * w;
@@ -333,16 +325,66 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
       CFW(CA + 1 + i) = w * (v[i] * ik - 0.5f * conv[i]);
 #pragma unroll
       for (int kk = 0; kk < 3; ++kk)
-        CFW(CB + 3 * (1 + i) + kk) =
-            hn * (Ji[kk][0] * gv[i][0] + Ji[kk][1] * gv[i][1] + Ji[kk][2] * gv[i][2]);
+        CFW(CB + 3 * (1 + i) + kk) = hn * M.ref(gv[i][0], gv[i][1], gv[i][2], kk);
     }
   }
 #undef CFW
 }
 
-template <int MODE, bool CACHED>
+// box: (1/hx, 1/hy, 1/hz, det J) of the cell; wq = the Gauss weight of point q
+template <int MODE, int GEO>
+__device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S, float* CF, int q,
+                                          float F[KLay<GEO>::NF][4], const float PQ[4][4],
+                                          float aT, float dT, const float4 box, float wq) {
+  using L = KLay<GEO>;
+  const int qx = q & 3, qy = (q >> 2) & 3, qz = q >> 4;
+  if constexpr (GEO == GEO_BOX) {
+    JBox M;
+    M.s[0] = box.x;
+    M.s[1] = box.y;
+    M.s[2] = box.z;
+    pointwise_core<MODE, L::NF, L::FO>(A, CF, q, M, wq * box.w, F, PQ, aT, dT);
+  } else {
+    JFull M;
+    float w;
+    if constexpr (GEO == GEO_CACHED) {
+      const float* G = S + L::oGQ;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) M.Ji[k][j] = G[(3 * k + j) * 64 + q];
+      w = G[9 * 64 + q];
+    } else {
+      float J[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) J[i][j] = F[i][1 + j];
+      const float c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      const float c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      const float c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      const float det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+      const float id = 1.0f / det;
+      M.Ji[0][0] = c00 * id;
+      M.Ji[1][0] = c01 * id;
+      M.Ji[2][0] = c02 * id;
+      M.Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+      M.Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+      M.Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+      M.Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+      M.Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+      M.Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+      w = cW[qx] * cW[qy] * cW[qz] * det;
+    }
+    pointwise_core<MODE, L::NF, L::FO>(A, CF, q, M, w, F, PQ, aT, dT);
+  }
+}
+
+template <int MODE, int GEO>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(ResidualArgs A) {
-  using L = KLay<CACHED>;
+  using L = KLay<GEO>;
+  constexpr bool CACHED = L::CACHED;          // 4 fields through the forward stages
+  constexpr bool STAGED = GEO == GEO_CACHED;  // per-point geometry block staged per cell
   constexpr int NF = L::NF;
   extern __shared__ __align__(16) float smem[];
   const int wib = threadIdx.x >> 5;
@@ -354,18 +396,21 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
   int idx_next = 0;  // node index of cell c + stride (lane t < 27)
   const uint32_t bar = smem_u32(S + L::oBar);
   uint32_t phase = 0;
-  if constexpr (CACHED) {
+  if constexpr (STAGED) {
     if (t == 0) {
       mbar_init(bar, 1);
       fence_async_smem();
     }
     __syncwarp();
   }
+  // Gauss weights of this lane's two points q = t and t + 32 (box form: w = wq det J)
+  const float wq_a = cW[t & 3] * cW[(t >> 2) & 3] * cW[t >> 4];
+  const float wq_b = cW[t & 3] * cW[(t >> 2) & 3] * cW[(t >> 4) + 2];
   if (c < A.n_cells) {
     const int node = t < 27 ? __ldg(A.cell_nodes + (int64_t)c * 27 + t) : 0;
-    load_raw<CACHED>(A, c, node, t, raw);
+    load_raw<GEO>(A, c, node, t, raw);
     if (c + stride < A.n_cells && t < 27) idx_next = __ldg(A.cell_nodes + (int64_t)(c + stride) * 27 + t);
-    if constexpr (CACHED) stage_geo(A, c, t, S + L::oGQ, bar);
+    if constexpr (STAGED) stage_geo(A, c, t, S + L::oGQ, bar);
   }
 
   for (; c < A.n_cells; c += stride) {
@@ -389,8 +434,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       vsq = raw.xv.y * raw.xv.y + raw.xv.z * raw.xv.z + raw.xv.w * raw.xv.w;
     }
     const float hT = raw.hT;
+    const float4 box = raw.gb;
     if (c + stride < A.n_cells) {  // issue the loads of the next cell (consumed next iteration)
-      load_raw<CACHED>(A, c + stride, idx_next, t, raw);
+      load_raw<GEO>(A, c + stride, idx_next, t, raw);
       if (c + 2 * stride < A.n_cells && t < 27)
         idx_next = __ldg(A.cell_nodes + (int64_t)(c + 2 * stride) * 27 + t);
     }
@@ -469,7 +515,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
           G[f][3] = cD[qz + 2][0] * vv0 + cD[qz + 2][1] * vv1 + cD[qz + 2][2] * vv2;
         }
       }
-      if constexpr (CACHED) {  // this cell's geometry block (staged one cell ahead)
+      if constexpr (STAGED) {  // this cell's geometry block (staged one cell ahead)
         mbar_wait(bar, phase);
         phase ^= 1;
       }
@@ -478,11 +524,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         pi_fields(S + oU + L::FO * 27,
                   CACHED ? reinterpret_cast<const float4*>(S + oVtx) : nullptr, yx & 3, yx >> 2,
                   qz, PQa, PQb);
-      pointwise<MODE, CACHED>(A, S, S + L::oCF, t, F, PQa, aT, dT);
-      pointwise<MODE, CACHED>(A, S, S + L::oCF, t + 32, G, PQb, aT, dT);
+      pointwise<MODE, GEO>(A, S, S + L::oCF, t, F, PQa, aT, dT, box, wq_a);
+      pointwise<MODE, GEO>(A, S, S + L::oCF, t + 32, G, PQb, aT, dT, box, wq_b);
     }
     __syncwarp();
-    if constexpr (CACHED) {
+    if constexpr (STAGED) {
       if (c + stride < A.n_cells) stage_geo(A, c + stride, t, S + L::oGQ, bar);
     }
     // ---------------- backward x, y, z in registers: lane (cp, qz), cp = (comp, part) ----------------
@@ -690,6 +736,22 @@ static int32_t check_level(const dnnmg_level_t* lv, const char* who) {
 int32_t launch_k2tc_elements(const dnnmg_level_t*, const float*, const float*, const float*,
                              const dnnmg_phys_t*, int, float*, cudaStream_t);
 
+template <int MODE, int GEO>
+static void launch_element_kernel(const ResidualArgs& A, cudaStream_t s) {
+  constexpr size_t smem = sizeof(float) * KLay<GEO>::kFloats * kWarpsPerBlock;
+  static uint64_t configured = 0;
+  if (first_use_on_device(configured))
+    cudaFuncSetAttribute(element_kernel<MODE, GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int blocks = (A.n_cells + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel<MODE, GEO>,
+                                                32 * kWarpsPerBlock, smem);
+  const int cap = kSMs * (per_sm > 0 ? per_sm : 1);
+  if (blocks > cap) blocks = cap;
+  element_kernel<MODE, GEO><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+}
+
 static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const float* aT,
                                const float* dT, const dnnmg_phys_t* ph, int mode, float* elem,
                                cudaStream_t s) {
@@ -713,44 +775,24 @@ static int32_t launch_elements(const dnnmg_level_t* lv, const float* x, const fl
   A.mode = mode;
   A.elem = reinterpret_cast<float4*>(elem);
   A.geo_q = lv->geo_q;
+  A.geo_box = reinterpret_cast<const float4*>(lv->geo_box);
   if (lv->n_cells == 0) return DNNMG_OK;
-  const bool cached = lv->geo_q != nullptr;
-  const size_t smem =
-      sizeof(float) * (cached ? KLay<true>::kFloats : KLay<false>::kFloats) * kWarpsPerBlock;
-  static uint64_t configured = 0;
-  if (first_use_on_device(configured)) {
-    cudaFuncSetAttribute(element_kernel<MODE_OPERATOR, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * KLay<false>::kFloats * kWarpsPerBlock));
-    cudaFuncSetAttribute(element_kernel<MODE_RHS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * KLay<false>::kFloats * kWarpsPerBlock));
-    cudaFuncSetAttribute(element_kernel<MODE_OPERATOR, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * KLay<true>::kFloats * kWarpsPerBlock));
-    cudaFuncSetAttribute(element_kernel<MODE_RHS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * KLay<true>::kFloats * kWarpsPerBlock));
-  }
-  int blocks = (lv->n_cells + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  int per_sm = 0;
-  if (cached)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel<MODE_OPERATOR, true>,
-                                                  32 * kWarpsPerBlock, smem);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_kernel<MODE_OPERATOR, false>,
-                                                  32 * kWarpsPerBlock, smem);
-  const int cap = kSMs * (per_sm > 0 ? per_sm : 1);
-  if (blocks > cap) blocks = cap;
+  // axis-aligned level: the box form; else the per-point cache when present
+  static const bool no_box = getenv("DNNMG_K2_NO_BOX") != nullptr;
+  if (no_box) A.geo_box = nullptr;
+  const int geo = A.geo_box ? GEO_BOX : lv->geo_q ? GEO_CACHED : GEO_NONE;
+#define DNNMG_K2_LAUNCH(M, G) \
+  launch_element_kernel<M, G>(A, s)
   if (mode == MODE_OPERATOR) {
-    if (cached)
-      element_kernel<MODE_OPERATOR, true><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
-    else
-      element_kernel<MODE_OPERATOR, false><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+    if (geo == GEO_BOX) DNNMG_K2_LAUNCH(MODE_OPERATOR, GEO_BOX);
+    else if (geo == GEO_CACHED) DNNMG_K2_LAUNCH(MODE_OPERATOR, GEO_CACHED);
+    else DNNMG_K2_LAUNCH(MODE_OPERATOR, GEO_NONE);
   } else {
-    if (cached)
-      element_kernel<MODE_RHS, true><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
-    else
-      element_kernel<MODE_RHS, false><<<blocks, 32 * kWarpsPerBlock, smem, s>>>(A);
+    if (geo == GEO_BOX) DNNMG_K2_LAUNCH(MODE_RHS, GEO_BOX);
+    else if (geo == GEO_CACHED) DNNMG_K2_LAUNCH(MODE_RHS, GEO_CACHED);
+    else DNNMG_K2_LAUNCH(MODE_RHS, GEO_NONE);
   }
+#undef DNNMG_K2_LAUNCH
   DNNMG_CHECK_LAUNCH("element_kernel");
   return DNNMG_OK;
 }
@@ -832,6 +874,58 @@ int32_t launch_level_geometry(const dnnmg_level_t* lv, float* geo, cudaStream_t 
   geometry_kernel<<<grid_for((lv->n_cells + 3) / 4, 1, 16), 128, 0, s>>>(lv->n_cells, lv->cell_nodes,
                                                                           lv->coords, geo);
   DNNMG_CHECK_LAUNCH("geometry_kernel");
+  return DNNMG_OK;
+}
+
+// ---- axis-aligned levels: one record per cell instead of the per-point cache --------------
+// box[c] = (1/hx, 1/hy, 1/hz, det J = hx hy hz) in fp64 -> fp32, hk = extent of the cell along
+// axis k (signed).  n_bad counts the cells whose 27 nodes are not the tri-quadratic lattice of
+// an axis-aligned box (|X_a - X_0 - (ix hx, iy hy, iz hz)/2| > 1e-12 |h|): the caller uses the
+// record only when it is 0, since then J is diagonal and constant over every cell and the
+// element kernel's box form equals the general one up to fp32 rounding of w.
+__global__ void __launch_bounds__(128) geometry_box_kernel(int n_cells, const int32_t* __restrict__ cn,
+                                                           const double* __restrict__ coords,
+                                                           float4* __restrict__ box,
+                                                           int32_t* __restrict__ n_bad) {
+  const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
+  for (int c = blockIdx.x * 4 + w; c < n_cells; c += gridDim.x * 4) {
+    const int32_t* row = cn + (int64_t)c * 27;
+    const int n0 = __ldg(row), nx = __ldg(row + 2), ny = __ldg(row + 6), nz = __ldg(row + 18);
+    double X0[3], h[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) X0[i] = __ldg(coords + 3 * (int64_t)n0 + i);
+    h[0] = __ldg(coords + 3 * (int64_t)nx + 0) - X0[0];
+    h[1] = __ldg(coords + 3 * (int64_t)ny + 1) - X0[1];
+    h[2] = __ldg(coords + 3 * (int64_t)nz + 2) - X0[2];
+    bool bad = false;
+    if (t < 27) {
+      const int n = __ldg(row + t);
+      const int l[3] = {t % 3, (t / 3) % 3, t / 9};
+      const double tol = 1e-12 * (fabs(h[0]) + fabs(h[1]) + fabs(h[2]));
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        bad |= !(fabs(__ldg(coords + 3 * (int64_t)n + i) - X0[i] - 0.5 * l[i] * h[i]) <= tol);
+    }
+    const double det = h[0] * h[1] * h[2];
+    bad |= !(det != 0.0);
+    const unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (t == 0) {
+      box[c] = make_float4((float)(1.0 / h[0]), (float)(1.0 / h[1]), (float)(1.0 / h[2]), (float)det);
+      if (any && n_bad) atomicAdd(n_bad, 1);
+    }
+  }
+}
+
+int32_t launch_level_geometry_box(const dnnmg_level_t* lv, float* box, int32_t* n_bad,
+                                  cudaStream_t s) {
+  DNNMG_REQUIRE(lv && lv->cell_nodes && lv->coords && box, DNNMG_ERR_ARG,
+                "level_geometry_box: null argument");
+  DNNMG_REQUIRE(((uintptr_t)box & 15) == 0, DNNMG_ERR_ARG, "level_geometry_box: unaligned output");
+  if (n_bad) cudaMemsetAsync(n_bad, 0, sizeof(int32_t), s);
+  if (lv->n_cells == 0) return DNNMG_OK;
+  geometry_box_kernel<<<grid_for((lv->n_cells + 3) / 4, 1, 16), 128, 0, s>>>(
+      lv->n_cells, lv->cell_nodes, lv->coords, reinterpret_cast<float4*>(box), n_bad);
+  DNNMG_CHECK_LAUNCH("geometry_box_kernel");
   return DNNMG_OK;
 }
 

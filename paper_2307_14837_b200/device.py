@@ -320,14 +320,18 @@ class DeviceLevel:
         self.affine = self.geo_kind > 0
         self.tc_geo = None
 
-    def struct(self, dof_mask=None, geometry=False, tc=None):
-        """tc: use the tensor-core element kernel (default: with the geometry cache present,
+    def struct(self, dof_mask=None, geometry=False, tc=None, box=None):
+        """geometry: with the per-mesh geometry -- the per-cell box record when every cell is an
+        axis-aligned box (box=False forces the per-point cache), else the per-point cache.
+        tc: use the tensor-core element kernel (default: with the geometry cache present,
         k2_tensor_cores)."""
         tc = geometry and k2_tensor_cores(self.geo_kind) if tc is None else tc
+        box = self.geometry_box() if (geometry and not tc and box is not False) else None
         lv = _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
                         ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx), ptr(dof_mask),
-                        ptr(self.geometry()) if (geometry or tc) else None, ptr(self.order),
-                        None, None, 0, ptr(self.vptr), ptr(self.vidx))
+                        ptr(self.geometry()) if ((geometry and box is None) or tc) else None,
+                        ptr(self.order), None, None, 0, ptr(self.vptr), ptr(self.vidx),
+                        ptr(box))
         if tc:
             lv.tc_const = ptr(k2tc_constants())
             lv.tc_geo = ptr(self.geometry_tc())
@@ -355,6 +359,23 @@ class DeviceLevel:
             _lib.call("dnnmg_level_geometry", ctypes.byref(self.struct()), ptr(self.geo_q),
                       stream_handle())
         return self.geo_q
+
+    def geometry_box(self):
+        """Per-cell (1/hx, 1/hy, 1/hz, det J) when every cell of the level is an axis-aligned
+        box with its Q2 nodes on the tri-quadratic lattice (checked on the device in fp64), else
+        None.  K2 then takes its box form: J^-1 diagonal and constant over a cell."""
+        if not hasattr(self, "geo_box"):
+            self.geo_box = None
+            if self.n_cells:
+                rec = torch.empty(self.n_cells * 4, dtype=torch.float32, device=device())
+                bad = torch.zeros(1, dtype=torch.int32, device=device())
+                lv = _lib.Level(self.n_nodes, self.n_cells, ptr(self.cell_nodes), ptr(self.coords),
+                                ptr(self.h_T), ptr(self.csr_ptr), ptr(self.csr_idx))
+                _lib.call("dnnmg_level_geometry_box", ctypes.byref(lv), ptr(rec), ptr(bad),
+                          stream_handle())
+                if int(bad.item()) == 0:
+                    self.geo_box = rec
+        return self.geo_box
 
     def scratch(self):
         """Element-vector scratch shared by the reference-API calls on this level

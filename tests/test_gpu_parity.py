@@ -393,7 +393,7 @@ def test_geometry_cache_matches_recomputed(name):
     ph = _lib.Phys(float(g["nu"]), float(g["k"]), float(g["alpha0"]), float(g["delta0"]), 1)
     out = []
     for geo in (False, True):
-        lv = lvl.struct(mask, geometry=geo)
+        lv = lvl.struct(mask, geometry=geo, box=False)
         r = torch.empty_like(xt)
         _lib.call("dnnmg_residual", ctypes.byref(lv), dv.ptr(xt), dv.ptr(b), None, None,
                   ctypes.byref(ph), dv.ptr(lvl.scratch()), dv.ptr(r), 1, dv.stream_handle())
@@ -403,6 +403,55 @@ def test_geometry_cache_matches_recomputed(name):
     # the cached geometry is formed in fp64: at least as close to the reference
     assert rel(out[1], g["r"]) < 2e-5, rel(out[1], g["r"])
     assert rel(out[1], g["r"]) <= 1.2 * rel(out[0], g["r"]) + 1e-9
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_box_geometry_matches_cached(name):
+    """K2's box form (levels of axis-aligned cells: per-cell (1/hx, 1/hy, 1/hz, det J), no
+    products with the zero off-diagonal entries of J^-1) against the per-point geometry cache
+    on the same level, residual and next-step RHS; a jittered level must not get the record."""
+    import ctypes
+    from paper_2307_14837_b200 import _lib, device as dv
+    g = load_golden(name)
+    h = product_hierarchy(g)
+    L, J = int(g["L"]), int(g["J"])
+    s = spmod.FeSpace(h, L + J)
+    lvl = dv.DeviceLevel.get(s)
+    box = lvl.geometry_box()
+    # the device check (27 nodes of every cell on the box lattice, fp64) on any level
+    rec = torch.empty(max(lvl.n_cells, 1) * 4, dtype=torch.float32, device="cuda")
+    bad = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    _lib.call("dnnmg_level_geometry_box", ctypes.byref(lvl.struct()), dv.ptr(rec), dv.ptr(bad),
+              dv.stream_handle())
+    if box is None:
+        assert int(bad.item()) > 0, (name, lvl.geo_kind, int(bad.item()))
+        assert not lvl.struct(None, geometry=True).geo_box
+        return
+    assert int(bad.item()) == 0
+    assert name != "jit"
+    X = np.asarray(s.nodes)[np.asarray(s.cell_nodes)]
+    hx = X[:, 2, 0] - X[:, 0, 0]
+    assert np.allclose(rec.cpu().numpy().reshape(-1, 4)[:, 0], 1.0 / hx, rtol=1e-6)
+    mask = dv.upload(dv.dof_mask_bits(g["mask"], s.n_nodes), np.uint8)
+    xt = torch.tensor(g["x_tilde"], dtype=torch.float32, device="cuda")
+    b = torch.tensor(g["b_prev"], dtype=torch.float32, device="cuda")
+    ph = _lib.Phys(float(g["nu"]), float(g["k"]), float(g["alpha0"]), float(g["delta0"]), 1)
+    res, rhs = [], []
+    for use_box in (False, True):
+        lv = lvl.struct(mask, geometry=True, tc=False, box=use_box)
+        assert bool(lv.geo_box) == use_box and bool(lv.geo_q) == (not use_box)
+        r = torch.empty_like(xt)
+        _lib.call("dnnmg_residual", ctypes.byref(lv), dv.ptr(xt), dv.ptr(b), None, None,
+                  ctypes.byref(ph), dv.ptr(lvl.scratch()), dv.ptr(r), 1, dv.stream_handle())
+        bn = torch.empty_like(xt)
+        _lib.call("dnnmg_rhs_next", ctypes.byref(lv), dv.ptr(xt), ctypes.byref(ph),
+                  dv.ptr(lvl.scratch()), dv.ptr(bn), dv.stream_handle())
+        torch.cuda.synchronize()
+        res.append(r.cpu().numpy().astype(float))
+        rhs.append(bn.cpu().numpy().astype(float))
+    assert rel(res[1], res[0]) < 2e-6, rel(res[1], res[0])
+    assert rel(rhs[1], rhs[0]) < 1e-6, rel(rhs[1], rhs[0])
+    assert rel(res[1], g["r"]) < 2e-5, rel(res[1], g["r"])
 
 
 @pytest.mark.parametrize("name", ["cfg0", "jit", "j2", "lvl1", "chan"])

@@ -85,6 +85,11 @@ typedef struct {
   const int32_t* owner_ptr;         /* [n_coarse_cells+1] or NULL */
   const int32_t* owner_node;        /* [n_fine_nodes] */
   const uint8_t* owner_code;        /* [n_fine_nodes] */
+  /* optional lattice form of the owner lists (takes precedence in K1): lat_node[C][25 pz +
+   * 5 py + px] = the fine node at position (px, py, pz) of the 5 x 5 x 5 lattice of the refined
+   * cell C when C is its first-appearance parent, else -1.  K1 then interpolates whole 1-D
+   * lines per lane with no per-node index decoding */
+  const int32_t* lat_node;          /* [n_coarse_cells][125] or NULL */
 } dnnmg_prolong_t;
 
 /* Restriction level l+1 -> l of a dual (RHS) vector: b_coarse = P^T b_fine
@@ -122,6 +127,11 @@ typedef struct {
                                     prolongation it is applied with (dnnmg_prolong_t.owner_node),
                                     read coalesced instead of gathered per owned node; NULL:
                                     gathered */
+  const int32_t* lat_node_bc;    /* optional [n_coarse_cells][125]: the lat_node table of the
+                                    prolongation this data is applied with, each owned entry
+                                    carrying bc_code[node] in bits 29-30 (node ids < 2^29), so
+                                    that K1's lattice form needs no Dirichlet-code load; NULL:
+                                    bc_code is gathered per node */
 } dnnmg_dirichlet_t;
 
 /* One fine level for assembly (assembly.py:65-108). */

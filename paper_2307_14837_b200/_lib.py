@@ -24,12 +24,12 @@ c_i32, c_i64, c_f32, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctyp
 class Prolong(ctypes.Structure):
     _fields_ = [("n_fine_nodes", c_i32), ("n_coarse_cells", c_i32),
                 ("coarse_cell_nodes", c_vp), ("fine_src", c_vp), ("owner_ptr", c_vp),
-                ("owner_node", c_vp), ("owner_code", c_vp)]
+                ("owner_node", c_vp), ("owner_code", c_vp), ("lat_node", c_vp)]
 
 
 class Dirichlet(ctypes.Structure):
     _fields_ = [("n_nodes", c_i32), ("bc_code", c_vp), ("bc_values", c_vp),
-                ("bc_code_owner", c_vp)]
+                ("bc_code_owner", c_vp), ("lat_node_bc", c_vp)]
 
 
 class Level(ctypes.Structure):

@@ -9,6 +9,8 @@
 // p = 2*o_k + a_k in {0..4} hits a coarse node (p even, weight 1) or a quarter
 // point (p odd, weights phi(p/4) = {3/8, 3/4, -1/8} or mirrored).  All weights
 // are dyadic, so they are exact in fp32.  Each node is one float4 (p, vx, vy, vz).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dnnmg {
@@ -223,6 +225,126 @@ __global__ void __launch_bounds__(32 * kProlongWarps) prolongate_owner_kernel(
   }
 }
 
+// v4: lattice form.  One warp per parent cell C; every interpolation stage is a set of whole
+// 1-D lines held in registers by one lane each (x: 9 lines, y: 15, z: the 25 columns of the
+// 5 x 5 x 5 lattice of the refined cell), so a line costs 3 shared loads and 2 three-tap
+// interpolations with compile-time weights, the lanes' roles are the same for every cell, and
+// a stage stores only its new (odd-position) values: the next stage reads an even position
+// from the array it came from through a per-lane base pointer.  The column lanes write their
+// five results straight to global memory: lat[C][25 pz + 5 py + px] is the fine node at that
+// lattice position when C is its first-appearance parent, else -1; with PACKED the node's
+// Dirichlet code sits in bits 29-30 (dnnmg_dirichlet_t.lat_node_bc).  K1 is bound by the L1
+// data pipe (ncu: 80-90 % l1tex, issue 45-63 %): v3 (owner lists, per-node index decoding, all
+// positions stored by every stage) took 54 us at config 3, staging the finished lattice in
+// shared memory for an owner-ordered (coalesced) write-out 52 us, this form 45 us and less.
+__device__ __forceinline__ float4 lerp_lo(const float4& a, const float4& b, const float4& c) {
+  float4 r;  // quarter point 1/4: (3/8, 3/4, -1/8), same operation order as lerp3
+  r.x = fmaf(-0.125f, c.x, fmaf(0.75f, b.x, 0.375f * a.x));
+  r.y = fmaf(-0.125f, c.y, fmaf(0.75f, b.y, 0.375f * a.y));
+  r.z = fmaf(-0.125f, c.z, fmaf(0.75f, b.z, 0.375f * a.z));
+  r.w = fmaf(-0.125f, c.w, fmaf(0.75f, b.w, 0.375f * a.w));
+  return r;
+}
+__device__ __forceinline__ float4 lerp_hi(const float4& a, const float4& b, const float4& c) {
+  float4 r;  // 3/4: (-1/8, 3/4, 3/8)
+  r.x = fmaf(0.375f, c.x, fmaf(0.75f, b.x, -0.125f * a.x));
+  r.y = fmaf(0.375f, c.y, fmaf(0.75f, b.y, -0.125f * a.y));
+  r.z = fmaf(0.375f, c.z, fmaf(0.75f, b.z, -0.125f * a.z));
+  r.w = fmaf(0.375f, c.w, fmaf(0.75f, b.w, -0.125f * a.w));
+  return r;
+}
+
+template <bool PACKED>
+__global__ void __launch_bounds__(32 * kProlongWarps) prolongate_lattice_kernel(
+    int n_coarse_cells, const int32_t* __restrict__ ctab, const int32_t* __restrict__ lat,
+    const float4* __restrict__ xc, float4* __restrict__ xf, const uint8_t* __restrict__ bc_code,
+    const float* __restrict__ bc_values) {
+  // cv[iz][iy][ix] 27 | X1[iz][iy][k] 18 (px = 2k+1) | X2[iz][k][px] 30 (py = 2k+1)
+  __shared__ float4 sm[kProlongWarps][27 + 18 + 30];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* cv = sm[w];
+  float4* X1 = cv + 27;
+  float4* X2 = X1 + 18;
+  // x line (iz, iy) = lane < 9
+  const float4* xs = cv + 3 * lane;
+  float4* xd = X1 + 2 * lane;
+  // y line (iz, px) = lane < 15: even px reads cv (stride 3), odd px reads X1 (stride 2)
+  const int y_iz = lane / 5, y_px = lane % 5;
+  const float4* ys = (y_px & 1) ? X1 + 6 * y_iz + (y_px >> 1) : cv + 9 * y_iz + (y_px >> 1);
+  const int y_st = (y_px & 1) ? 2 : 3;
+  float4* yd = X2 + 10 * y_iz + y_px;  // [k] stride 5
+  // z column (py, px) = lane < 25: [iz] from X2 (odd py), X1 (even py, odd px) or cv
+  const int z_py = lane / 5, z_px = lane % 5;
+  const float4* zs = (z_py & 1)   ? X2 + 5 * (z_py >> 1) + z_px
+                     : (z_px & 1) ? X1 + 2 * (z_py >> 1) + (z_px >> 1)
+                                  : cv + 3 * (z_py >> 1) + (z_px >> 1);
+  const int z_st = (z_py & 1) ? 10 : (z_px & 1) ? 6 : 9;
+  const int stride = gridDim.x * kProlongWarps;
+  int C = blockIdx.x * kProlongWarps + w;
+  float4 nxt = make_float4(0.f, 0.f, 0.f, 0.f);
+  int id_nxt[5] = {-1, -1, -1, -1, -1};
+  if (C < n_coarse_cells) {
+    if (lane < 27) nxt = __ldg(xc + __ldg(ctab + (int64_t)C * 27 + lane));
+    if (lane < 25) {
+#pragma unroll
+      for (int pz = 0; pz < 5; ++pz) id_nxt[pz] = __ldg(lat + (int64_t)C * 125 + 25 * pz + lane);
+    }
+  }
+  for (; C < n_coarse_cells; C += stride) {
+    if (lane < 27) cv[lane] = nxt;
+    int id[5];
+#pragma unroll
+    for (int pz = 0; pz < 5; ++pz) id[pz] = id_nxt[pz];
+    if (C + stride < n_coarse_cells) {  // next cell's loads in flight under this cell's stages
+      if (lane < 27) nxt = __ldg(xc + __ldg(ctab + (int64_t)(C + stride) * 27 + lane));
+      if (lane < 25) {
+#pragma unroll
+        for (int pz = 0; pz < 5; ++pz)
+          id_nxt[pz] = __ldg(lat + (int64_t)(C + stride) * 125 + 25 * pz + lane);
+      }
+    }
+    __syncwarp();
+    if (lane < 9) {
+      const float4 a = xs[0], b = xs[1], c = xs[2];
+      xd[0] = lerp_lo(a, b, c);
+      xd[1] = lerp_hi(a, b, c);
+    }
+    __syncwarp();
+    if (lane < 15) {
+      const float4 a = ys[0], b = ys[y_st], c = ys[2 * y_st];
+      yd[0] = lerp_lo(a, b, c);
+      yd[5] = lerp_hi(a, b, c);
+    }
+    __syncwarp();
+    if (lane < 25) {
+      const float4 a = zs[0], b = zs[z_st], c = zs[2 * z_st];
+      float4 v[5];
+      v[0] = a;
+      v[1] = lerp_lo(a, b, c);
+      v[2] = b;
+      v[3] = lerp_hi(a, b, c);
+      v[4] = c;
+#pragma unroll
+      for (int pz = 0; pz < 5; ++pz) {
+        if (id[pz] >= 0) {
+          const int n = PACKED ? (id[pz] & 0x1fffffff) : id[pz];
+          const int code = PACKED ? (id[pz] >> 29) : (bc_code ? (int)bc_code[n] : 0);
+          float4 acc = v[pz];
+          if (code == 1) {
+            acc.y = acc.z = acc.w = 0.f;
+          } else if (code == 2) {
+            acc.y = bc_values[3 * (int64_t)n];
+            acc.z = bc_values[3 * (int64_t)n + 1];
+            acc.w = bc_values[3 * (int64_t)n + 2];
+          }
+          xf[n] = acc;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float* x_fine,
                           const dnnmg_dirichlet_t* bc, cudaStream_t s) {
   DNNMG_REQUIRE(P && x_coarse && x_fine, DNNMG_ERR_ARG, "prolongate: null argument");
@@ -241,6 +363,20 @@ int32_t launch_prolongate(const dnnmg_prolong_t* P, const float* x_coarse, float
     owner_code = bc->bc_code_owner;
   }
   if (P->n_fine_nodes == 0) return DNNMG_OK;
+  static const bool no_lattice = getenv("DNNMG_K1_OWNER") != nullptr;
+  if (P->lat_node && !no_lattice) {
+    const int blocks = grid_for((P->n_coarse_cells + kProlongWarps - 1) / kProlongWarps, 1, 4);
+    const float4* xc = reinterpret_cast<const float4*>(x_coarse);
+    float4* xf = reinterpret_cast<float4*>(x_fine);
+    if (bc && bc->lat_node_bc)
+      prolongate_lattice_kernel<true><<<blocks, 32 * kProlongWarps, 0, s>>>(
+          P->n_coarse_cells, P->coarse_cell_nodes, bc->lat_node_bc, xc, xf, nullptr, vals);
+    else
+      prolongate_lattice_kernel<false><<<blocks, 32 * kProlongWarps, 0, s>>>(
+          P->n_coarse_cells, P->coarse_cell_nodes, P->lat_node, xc, xf, code, vals);
+    DNNMG_CHECK_LAUNCH("prolongate_lattice_kernel");
+    return DNNMG_OK;
+  }
   if (P->owner_ptr && P->owner_node && P->owner_code) {
     const int blocks = grid_for((P->n_coarse_cells + kProlongWarps - 1) / kProlongWarps, 1, 4);
     prolongate_owner_kernel<<<blocks, 32 * kProlongWarps, 0, s>>>(

@@ -166,6 +166,21 @@ def cell_diameters(vertices, cells, chunk=1 << 16):
     return out
 
 
+def lattice_table(src, n_coarse_cells):
+    """lat[C][25 pz + 5 py + px] = fine node whose first-appearance parent is C and whose
+    position in C's refined 5 x 5 x 5 lattice is (px, py, pz) (src = C*216 + o*27 + a: child
+    octant o, local Q2 node a; space.py:117-165), else -1."""
+    src = np.asarray(src, dtype=np.int64)
+    C, oa = src // 216, src % 216
+    o, a = oa // 27, oa % 27
+    px = 2 * (o & 1) + a % 3
+    py = 2 * ((o >> 1) & 1) + (a // 3) % 3
+    pz = 2 * (o >> 2) + a // 9
+    lat = np.full((n_coarse_cells, 125), -1, dtype=np.int64)
+    lat[C, 25 * pz + 5 * py + px] = np.arange(src.size)
+    return lat
+
+
 class DeviceProlong:
     """K1 tables for level -> level+1."""
 
@@ -187,8 +202,23 @@ class DeviceProlong:
         self.owner_order = order                      # host copy (owner-ordered bc codes)
         self.owner_node = upload(order, np.int32)
         self.owner_code = upload(src[order] % 216, np.uint8)
+        # lattice form: the owned fine node at every position of each parent's 5 x 5 x 5 lattice
+        self.lat_host = lattice_table(src, int(ctab.shape[0]))
+        self.lat_node = upload(self.lat_host, np.int32)
         self.struct = _lib.Prolong(self.n_fine, int(ctab.shape[0]), ptr(self.ctab), ptr(self.src),
-                                   ptr(self.owner_ptr), ptr(self.owner_node), ptr(self.owner_code))
+                                   ptr(self.owner_ptr), ptr(self.owner_node), ptr(self.owner_code),
+                                   ptr(self.lat_node))
+
+    def lattice_with_codes(self, code):
+        """lat_node with the Dirichlet code of every owned node in bits 29-30
+        (dnnmg_dirichlet_t.lat_node_bc), or None when the node ids do not leave room."""
+        if self.n_fine >= 1 << 29:
+            return None
+        lat = self.lat_host
+        out = lat.copy()
+        own = lat >= 0
+        out[own] = lat[own] | (np.asarray(code, dtype=np.int64)[lat[own]] << 29)
+        return out.astype(np.int32)
 
     @staticmethod
     def get(hierarchy, level):

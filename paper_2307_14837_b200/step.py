@@ -102,16 +102,25 @@ class CorrectionStep:
             # in place: a captured graph keeps reading the same buffers
             old.code.copy_(dv.upload(code, np.uint8))
             old.vals.copy_(dv.upload(vals, np.float32))
+            if not np.array_equal(self._code_host, code):  # (codes normally do not depend on t)
+                self._code_host = np.array(code, dtype=np.uint8)
+                old.code_owner.copy_(dv.upload(self._code_host[self.prolongs[-1].owner_order], np.uint8))
+                if old.lat_bc is not None:
+                    old.lat_bc.copy_(dv.upload(self.prolongs[-1].lattice_with_codes(code), np.int32))
             self._t = t
             return
         self.graph = None  # new buffers: a graph captured earlier would read stale ones
         self.bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
         self.bc.code = dv.upload(code, np.uint8)
+        self._code_host = np.array(code, dtype=np.uint8)
         # the codes in the owner order of the last prolongation (K1 reads them coalesced)
         self.bc.code_owner = dv.upload(np.asarray(code, np.uint8)[self.prolongs[-1].owner_order], np.uint8)
         self.bc.vals = None if vals is None else dv.upload(vals, np.float32)
+        # ... and packed into the lattice table of that prolongation (no code load at all)
+        lat = self.prolongs[-1].lattice_with_codes(code)
+        self.bc.lat_bc = None if lat is None else dv.upload(lat, np.int32)
         self.bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(self.bc.code), dv.ptr(self.bc.vals),
-                                        dv.ptr(self.bc.code_owner))
+                                        dv.ptr(self.bc.code_owner), dv.ptr(self.bc.lat_bc))
         self._t = t
 
     @property
@@ -143,8 +152,9 @@ class CorrectionStep:
             bc = dv.DeviceDirichlet.__new__(dv.DeviceDirichlet)
             bc.code, bc.vals = self.bc.code.clone(), self.bc.vals.clone()
             bc.code_owner = self.bc.code_owner
+            bc.lat_bc = self.bc.lat_bc
             bc.struct = _lib.Dirichlet(self.space.n_nodes, dv.ptr(bc.code), dv.ptr(bc.vals),
-                                       dv.ptr(bc.code_owner))
+                                       dv.ptr(bc.code_owner), dv.ptr(bc.lat_bc))
             t.bc = bc
         t.graph = None
         return t

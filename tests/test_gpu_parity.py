@@ -52,6 +52,52 @@ def test_prolongate_and_dirichlet(case):
     assert rel(xt.values, g["x_tilde"]) < 1e-7
 
 
+def test_prolongation_forms_bitwise(case):
+    """K1's table forms: the owner-list kernel and the lattice kernel (lat_node) write the same
+    bits, with the Dirichlet codes gathered, in owner order, or packed into the lattice table
+    (dnnmg_dirichlet_t.lat_node_bc); the per-fine-node kernel (fine_src only: products of the
+    three 1-D weights in one sum) agrees to fp32 rounding; every fine node is written exactly
+    once."""
+    import ctypes
+    from paper_2307_14837_b200 import _lib, device as dv
+    name, g, h, s, ps = case
+    L, J = int(g["L"]), int(g["J"])
+    P = dv.DeviceProlong.get(h, L + J - 1)
+    assert np.array_equal(np.sort(P.lat_host[P.lat_host >= 0]), np.arange(P.n_fine))
+    rng = np.random.default_rng(11)
+    xc = torch.tensor(rng.standard_normal(4 * P.n_coarse_nodes), dtype=torch.float32, device="cuda")
+    code, vals = dv.dirichlet_codes(s, float(g["t"]), product_bcs(g))
+    dcode = dv.upload(code, np.uint8)
+    dvals = None if vals is None else dv.upload(vals, np.float32)
+    downer = dv.upload(np.asarray(code, np.uint8)[P.owner_order], np.uint8)
+    dlat = dv.upload(P.lattice_with_codes(code), np.int32)
+    n_f, n_c = P.n_fine, P.lat_host.shape[0]
+    base = (dv.ptr(P.ctab), dv.ptr(P.src))
+    owner = (dv.ptr(P.owner_ptr), dv.ptr(P.owner_node), dv.ptr(P.owner_code))
+    forms = {"owner": _lib.Prolong(n_f, n_c, *base, *owner),
+             "lattice": _lib.Prolong(n_f, n_c, *base, *owner, dv.ptr(P.lat_node)),
+             "node": _lib.Prolong(n_f, n_c, *base)}
+    bcs = {"none": None,
+           "gathered": _lib.Dirichlet(n_f, dv.ptr(dcode), dv.ptr(dvals)),
+           "owner": _lib.Dirichlet(n_f, dv.ptr(dcode), dv.ptr(dvals), dv.ptr(downer)),
+           "packed": _lib.Dirichlet(n_f, dv.ptr(dcode), dv.ptr(dvals), dv.ptr(downer), dv.ptr(dlat))}
+    ref = {}
+    for fname, F in forms.items():
+        for bname, B in bcs.items():
+            out = torch.full((4 * n_f,), float("nan"), dtype=torch.float32, device="cuda")
+            _lib.call("dnnmg_prolongate", ctypes.byref(F), dv.ptr(xc), dv.ptr(out),
+                      None if B is None else ctypes.byref(B), dv.stream_handle())
+            torch.cuda.synchronize()
+            assert not torch.isnan(out).any(), (fname, bname)
+            key = "none" if bname == "none" else "bc"
+            if key not in ref:
+                ref[key] = out
+            if fname == "node":
+                assert rel(out.cpu().numpy(), ref[key].cpu().numpy()) < 1e-6, (fname, bname)
+            else:
+                assert torch.equal(out, ref[key]), (fname, bname)
+
+
 def test_stab(case):
     name, g, h, s, ps = case
     st = Assembler(s).stab(g["x_tilde"], float(g["nu"]), float(g["k"]))

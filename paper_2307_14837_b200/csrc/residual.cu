@@ -606,7 +606,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         const float keep = hi1 ? o[14 + k] : o[k];
         k14[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
       }
-      const float sgn = part ? -1.f : 1.f;
       float* out = S + oTZ + cp * 27 + (hi1 ? 14 : 0) + (hi0 ? 7 : 0);
       const int nvalid = (hi1 && hi0) ? 6 : 7;  // 27 = 7 + 7 + 7 + 6
 #pragma unroll
@@ -614,7 +613,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         const float send = hi0 ? k14[k] : k14[7 + k];
         const float keep = hi0 ? k14[7 + k] : k14[k];
         const float v = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-        if (k < nvalid) out[k] = sgn * v;
+        if (k < nvalid) out[k] = v;  // (part 1 enters with a minus sign: applied in the PI^T sums)
       }
     }
     __syncwarp();
@@ -631,7 +630,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       for (int m = 0; m < 8; ++m) {
         const int b0 = (m & 1) ? 1 : it0, b1 = (m & 2) ? 1 : it1, b2 = (m & 4) ? 1 : it2;
         const float wgt = ((m & 1) ? 0.5f : 1.f) * ((m & 2) ? 0.5f : 1.f) * ((m & 4) ? 0.5f : 1.f);
-        lps = fmaf(wgt, gp[b0 + 3 * b1 + 9 * b2], lps);
+        lps = fmaf(-wgt, gp[b0 + 3 * b1 + 9 * b2], lps);
       }
     }
     {

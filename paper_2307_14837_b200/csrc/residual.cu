@@ -98,7 +98,9 @@ struct KLay {
   static constexpr int oCF = oSY + NF * kSYF;
   static constexpr int oGQ = oCF + kNCF * kCFS;        // cached [J^-1 (9) | w][64]
   static constexpr int oBar = oGQ + 10 * 64;           // cached: the staging mbarrier (8 B)
-  static constexpr int kFloats = (oGQ + (GEO == GEO_CACHED ? 10 * 64 + 4 : 0) + 3) / 4 * 4;
+  // a block of zeros: the value-test array of the part-1 (LPS) lanes of the backward stage
+  static constexpr int oZero = (oGQ + (GEO == GEO_CACHED ? 10 * 64 + 4 : 0) + 3) / 4 * 4;
+  static constexpr int kFloats = oZero + kCFS + 32;
   static_assert(oTZ + 4 * 2 * 27 <= oCF && oCF % 4 == 0 && oGQ % 4 == 0, "layout");
 };
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
@@ -403,6 +405,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     }
     __syncwarp();
   }
+  for (int i = t; i < kCFS + 32; i += 32) S[L::oZero + i] = 0.f;
+  __syncwarp();
   // Gauss weights of this lane's two points q = t and t + 32 (box form: w = wq det J)
   const float wq_a = cW[t & 3] * cW[(t >> 2) & 3] * cW[t >> 4];
   const float wq_b = cW[t & 3] * cW[(t >> 2) & 3] * cW[(t >> 4) + 2];
@@ -440,19 +444,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       if (c + 2 * stride < A.n_cells && t < 27)
         idx_next = __ldg(A.cell_nodes + (int64_t)(c + 2 * stride) * 27 + t);
     }
-    // non-negative floats order like their bit patterns: one warp-wide integer max
-    const float vmag = sqrtf(__uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(vsq))));
-    float aT, dT;
-    if (A.alpha_in) {
-      aT = A.alpha_in[c];
-      dT = A.delta_in[c];
-    } else {  // stab at x (assembly.py:55-59, 169-178)
-      const float h = hT;
-      const float ih = frcp(h);
-      const float rden = frcp(fmaf(A.nu * ih, ih, fmaf(vmag, ih, A.ik)));
-      aT = A.alpha0 * rden;
-      dT = A.delta0 * rden;
-    }
+    // non-negative floats order like their bit patterns: one warp-wide integer max (its result
+    // and the reciprocals below are consumed in the pointwise phase: the dependent chain
+    // REDUX -> sqrt -> rcp -> rcp is placed under the forward z stage, whose loads and FMAs
+    // cover its latency; next to the gather it stalled every warp, 8 % of the samples)
+    const unsigned vsq_max = __reduce_max_sync(0xffffffffu, __float_as_uint(vsq));
     __syncwarp();
     // ---------------- forward x and y in registers: lane (f, qx) ----------------
     // x stage for this qx on the 9 (iz, iy) lines of field f, then the y stage for all four
@@ -492,6 +488,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     __syncwarp();
     // ---------------- forward z + pointwise: Gauss points q = t and t + 32 (same qy, qx) ----------------
     {
+      float aT, dT;
+      if (A.alpha_in) {
+        aT = A.alpha_in[c];
+        dT = A.delta_in[c];
+      } else {  // stab at x (assembly.py:55-59, 169-178)
+        const float vmag = sqrtf(__uint_as_float(vsq_max));
+        const float ih = frcp(hT);
+        const float rden = frcp(fmaf(A.nu * ih, ih, fmaf(vmag, ih, A.ik)));
+        aT = A.alpha0 * rden;
+        dT = A.delta0 * rden;
+      }
       const int yx = t & 15, qz = t >> 4;  // second point: qz + 2
       float F[NF][4], G[NF][4];
 #pragma unroll
@@ -544,7 +551,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       const int comp = cp >> 1, part = cp & 1;
       // part 0: A_c, B_c0..2; part 1: comp 0 -> B_00..02, comps 1..3 -> P_(c-1)0..2; part 1 has
       // no value test and enters with a minus sign
-      const float* c0 = S + L::oCF + (CA + comp) * kCFS + cfq(16 * qz);
+      // part 1 has no value test: its lanes read zeros, placed 8 banks away from the array the
+      // part-0 lanes of the same quarter-warp read (no select per loaded value, no conflict)
+      const float* c0 = part ? S + L::oZero + ((L::oCF + (CA + comp) * kCFS + 8 - L::oZero) & 31) +
+                                   cfq(16 * qz)
+                             : S + L::oCF + (CA + comp) * kCFS + cfq(16 * qz);
       const float* c1 = S + L::oCF +
                         (part == 0 || comp == 0 ? CB + 3 * comp : CP + 3 * (comp - 1)) * kCFS +
                         cfq(16 * qz);
@@ -557,11 +568,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         for (int ix = 0; ix < 3; ++ix) ua[iy][ix] = ub[iy][ix] = 0.f;
 #pragma unroll
       for (int qy = 0; qy < 4; ++qy) {
-        float4 l0 = *reinterpret_cast<const float4*>(c0 + 4 * qy);
+        const float4 l0 = *reinterpret_cast<const float4*>(c0 + 4 * qy);
         const float4 l1 = *reinterpret_cast<const float4*>(c1 + 4 * qy);
         const float4 l2 = *reinterpret_cast<const float4*>(c2 + 4 * qy);
         const float4 l3 = *reinterpret_cast<const float4*>(c3 + 4 * qy);
-        if (part) l0 = make_float4(0.f, 0.f, 0.f, 0.f);
         const float L0[4] = {l0.x, l0.y, l0.z, l0.w}, L1[4] = {l1.x, l1.y, l1.z, l1.w};
         const float L2[4] = {l2.x, l2.y, l2.z, l2.w}, L3[4] = {l3.x, l3.y, l3.z, l3.w};
 #pragma unroll

@@ -449,11 +449,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     // REDUX -> sqrt -> rcp -> rcp is placed under the forward z stage, whose loads and FMAs
     // cover its latency; next to the gather it stalled every warp, 8 % of the samples)
     const unsigned vsq_max = __reduce_max_sync(0xffffffffu, __float_as_uint(vsq));
+    const float ih = frcp(hT);  // (the chain is spread over the three regions between the warp
+    const float nuih = A.nu * ih;  //  barriers, which the compiler does not schedule across)
     __syncwarp();
     // ---------------- forward x and y in registers: lane (f, qx) ----------------
     // x stage for this qx on the 9 (iz, iy) lines of field f, then the y stage for all four
     // qy -> sy[f][kind*3 + iz][qy*4 + qx]; kind 0 = B_x B_y, 1 = B_x D_y, 2 = D_x B_y
     // (cached form: 4 fields x 4 qx x 2 halves of qy -> all 32 lanes)
+    const float sden = fmaf(nuih, ih, fmaf(sqrtf(__uint_as_float(vsq_max)), ih, A.ik));
+    float srcp;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(srcp) : "f"(sden));
     constexpr int QYH = CACHED ? 2 : 4;  // qy per lane
     if (t < (CACHED ? 32 : 4 * NF)) {
       const int f = CACHED ? t >> 3 : t >> 2, qx = CACHED ? (t >> 1) & 3 : t & 3;
@@ -493,9 +498,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         aT = A.alpha_in[c];
         dT = A.delta_in[c];
       } else {  // stab at x (assembly.py:55-59, 169-178)
-        const float vmag = sqrtf(__uint_as_float(vsq_max));
-        const float ih = frcp(hT);
-        const float rden = frcp(fmaf(A.nu * ih, ih, fmaf(vmag, ih, A.ik)));
+        const float rden = fmaf(fmaf(-sden, srcp, 1.0f), srcp, srcp);  // = frcp(sden)
         aT = A.alpha0 * rden;
         dT = A.delta0 * rden;
       }

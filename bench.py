@@ -25,11 +25,11 @@ kernels of the current one).
 `aux` times the rows around the step (next-step RHS, restriction, training-data
 rows + statistics, Vanka sweeps); they are not part of `value`.
 
---impl reference times the CPU oracle port of the reference (oracle/,
-float64 numpy, all host threads) on a bounded sample of the same workload.
-Multi-GPU (torchrun): the x-slab decomposition (slab.py), one config-sized slab
-per rank ("weak"), NCCL P2P halo exchange twice per step, timed on the device,
-max over ranks.
+--impl reference times the reference ITSELF (the unmodified package installed in
+baseline/_ref, float64 numpy, all host threads and one) on a bounded sample of the same
+workload.
+Multi-GPU (torchrun): the x-slab decomposition (slab.py) of the config-3 box, strong
+scaling, NCCL P2P halo exchange twice per step, timed on the device, max over ranks.
 """
 
 import argparse
@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-sample", default="16x8x8", help="coarse box of the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pipe-depth", type=int, default=2,
+                    help="device input/output buffers of the e2e host pipeline")
     ap.add_argument("--no-aux", action="store_true", help="skip the next-row aux timings")
     ap.add_argument("--mlp-sweep", action="store_true",
                     help="BASELINE config 4: isolated patch-MLP sweep (one JSON line)")
@@ -571,7 +573,8 @@ def run_slabs(args, rank, world, local):
                 entry["hbm_frac"] = entry["GB/s"] / peaks["hbm_gbs"]
             if "flops" in u:
                 entry["TFLOP/s"] = u["flops"] / (entry["ms"] / 1e3) / 1e12
-        roof = roofline_of(per_kernel, units, precision, peaks, peak_kind, st.level.n_cells)
+        roof = roofline_of(per_kernel, units, precision, peaks, peak_kind, st.level.n_cells,
+                           "box" if st.level.geometry_box() is not None else "general")
         cpu = None if args.no_cpu_baseline else cpu_baseline_entry(cfg, args)
         line = {
             "metric": METRIC, "value": n_total * args.steps / (ms / 1e3), "unit": UNIT,
@@ -709,8 +712,11 @@ def vanka_aux(step, steps, barrier, n_cells=(16, 8, 8)):
 # executed FP32 work of K2's element kernel per fine cell and lane, from its SASS mix at
 # config 3 (ncu smsp__sass_thread_inst_executed_op_{ffma,fmul,fadd}_pred_on / 32 / cells,
 # profiles/r1_kernels_cfg3_ncu.txt): FFMA 659.7, FMUL 271.8, FADD 85.4
-DRAM_TRAFFIC_FILE = "r1_dram_traffic.json"   # newest ncu DRAM capture (per round)
-K2_EXEC_FLOP_PER_CELL = 32 * (2 * 659.7 + 271.8 + 85.4)
+# (general form, per-point geometry cache); the box form of axis-aligned levels (config 3,
+# profiles/r2_kernels_cfg3_ncu.txt): FFMA 551.7, FMUL 273.9, FADD 85.4
+DRAM_TRAFFIC_FILE = "r2_dram_traffic.json"   # newest ncu DRAM capture (per round)
+K2_EXEC_FLOP_PER_CELL = {"general": 32 * (2 * 659.7 + 271.8 + 85.4),
+                         "box": 32 * (2 * 551.7 + 273.9 + 85.4)}
 
 
 def fp32_nominal_tflops(peaks):
@@ -718,7 +724,7 @@ def fp32_nominal_tflops(peaks):
     return 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
 
 
-def roofline_of(per_kernel, units, precision, peaks, peak_kind, n_cells=None):
+def roofline_of(per_kernel, units, precision, peaks, peak_kind, n_cells=None, k2_form="general"):
     """`roofline` of the dominant stage (largest event time) and the K2 FP32 roofline."""
     names = [n for n in per_kernel if n in units or n.startswith("K3K4")]
     dom = max(names, key=lambda n: per_kernel[n]["ms"])
@@ -743,11 +749,12 @@ def roofline_of(per_kernel, units, precision, peaks, peak_kind, n_cells=None):
     # SIMT peak at the max SM clock (no micro-benchmark number)
     if "K2_residual" in per_kernel and n_cells:
         pk = fp32_nominal_tflops(peaks)
-        ach2 = K2_EXEC_FLOP_PER_CELL * n_cells / (per_kernel["K2_residual"]["ms"] / 1e3) / 1e12
+        ach2 = K2_EXEC_FLOP_PER_CELL[k2_form] * n_cells / (per_kernel["K2_residual"]["ms"] / 1e3) / 1e12
         per_kernel["K2_residual"]["fp32_roofline"] = {
             "bound": "fp32 issue", "achieved": ach2, "peak": pk, "unit": "TFLOP/s",
             "frac": ach2 / pk,
             "peak_source": "nominal FP32: 148 SMs x 128 lanes x 2 x sm_max_mhz (MEASURED_PEAKS)",
+            "element_kernel_form": k2_form,
             "flop_source": "executed FFMA/FMUL/FADD per cell from the element kernel's SASS mix"}
     # DRAM traffic per launch of each stage from the committed ncu capture
     try:
@@ -904,7 +911,7 @@ def run_ours(args, rank, world, local):
         hb = [p[1].cpu().pin_memory() for p in pairs]
         hout = [torch.empty(step.x_corr.numel(), dtype=torch.float32).pin_memory()
                 for _ in range(S)]
-        pipe = HostPipeline(step)
+        pipe = HostPipeline(step, depth=args.pipe_depth)
         pipe.begin()
         for i in range(max(args.warmup, 2)):
             pipe.submit(hx[i % S], hb[i % S], hout[i % S])
@@ -948,7 +955,8 @@ def run_ours(args, rank, world, local):
         if "flops_ref_formulation" in u:
             entry["ref_formulation_TFLOP/s"] = u["flops_ref_formulation"] / (avg[j] / 1e3) / 1e12
         per_kernel[nm] = entry
-    roof = roofline_of(per_kernel, units, precision, peaks, peak_kind, step.level.n_cells)
+    roof = roofline_of(per_kernel, units, precision, peaks, peak_kind, step.level.n_cells,
+                       "box" if step.level.geometry_box() is not None else "general")
     cpu = None if args.no_cpu_baseline else cpu_baseline_entry(cfg, args)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

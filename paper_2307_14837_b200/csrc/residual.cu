@@ -94,6 +94,8 @@ template <int GEO>
 struct KLay {
   static constexpr bool CACHED = GEO != GEO_NONE;
   static constexpr int NF = CACHED ? 4 : kNF;         // Q2 fields through the forward stages
+  static constexpr int US = CACHED ? 28 : 27;         // field stride of u (28: rows 16-byte aligned,
+                                                      // the forward x-y stage reads them as float4)
   static constexpr int FO = NF - 4;                    // index of p among them
   static constexpr int oCF = oSY + NF * kSYF;
   static constexpr int oGQ = oCF + kNCF * kCFS;        // cached [J^-1 (9) | w][64]
@@ -422,14 +424,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     float vsq = 0.f;  // |v|^2 of this lane's node; vmax = sqrt(max |v|^2) (sqrt is monotone)
     if (t < 27) {
       if constexpr (!CACHED) {
-        S[oU + 0 * 27 + t] = float(raw.X[0] - raw.X0[0]);
-        S[oU + 1 * 27 + t] = float(raw.X[1] - raw.X0[1]);
-        S[oU + 2 * 27 + t] = float(raw.X[2] - raw.X0[2]);
+        S[oU + 0 * L::US + t] = float(raw.X[0] - raw.X0[0]);
+        S[oU + 1 * L::US + t] = float(raw.X[1] - raw.X0[1]);
+        S[oU + 2 * L::US + t] = float(raw.X[2] - raw.X0[2]);
       }
-      S[oU + (L::FO + 0) * 27 + t] = raw.xv.x;
-      S[oU + (L::FO + 1) * 27 + t] = raw.xv.y;
-      S[oU + (L::FO + 2) * 27 + t] = raw.xv.z;
-      S[oU + (L::FO + 3) * 27 + t] = raw.xv.w;
+      S[oU + (L::FO + 0) * L::US + t] = raw.xv.x;
+      S[oU + (L::FO + 1) * L::US + t] = raw.xv.y;
+      S[oU + (L::FO + 2) * L::US + t] = raw.xv.z;
+      S[oU + (L::FO + 3) * L::US + t] = raw.xv.w;
       if constexpr (CACHED) {   // vertex copy as float4 (pi fields)
         const int ix = t % 3, iy = (t / 3) % 3, iz = t / 9;
         if (ix != 1 && iy != 1 && iz != 1)
@@ -463,7 +465,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     if (t < (CACHED ? 32 : 4 * NF)) {
       const int f = CACHED ? t >> 3 : t >> 2, qx = CACHED ? (t >> 1) & 3 : t & 3;
       const int qy0 = CACHED ? 2 * (t & 1) : 0;
-      const float* u = S + oU + f * 27;
+      float u[28];
+      if constexpr (CACHED) {   // 7 vector loads instead of 27 scalar ones
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+          const float4 q4 = reinterpret_cast<const float4*>(S + oU + f * L::US)[k];
+          u[4 * k] = q4.x;
+          u[4 * k + 1] = q4.y;
+          u[4 * k + 2] = q4.z;
+          u[4 * k + 3] = q4.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 27; ++k) u[k] = S[oU + f * L::US + k];
+      }
       const float bx0 = cB[qx][0], bx1 = cB[qx][1], bx2 = cB[qx][2];
       const float dx0 = cD[qx][0], dx1 = cD[qx][1], dx2 = cD[qx][2];
       float aB[3][3], aD[3][3];
@@ -531,7 +546,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       }
       float PQa[4][4], PQb[4][4];
       if constexpr (MODE == MODE_OPERATOR)
-        pi_fields(S + oU + L::FO * 27,
+        pi_fields(S + oU + L::FO * L::US,
                   CACHED ? reinterpret_cast<const float4*>(S + oVtx) : nullptr, yx & 3, yx >> 2,
                   qz, PQa, PQb);
       pointwise<MODE, GEO>(A, S, S + L::oCF, t, F, PQa, aT, dT, box, wq_a);

@@ -79,9 +79,11 @@ constexpr int kNCF = 25;
 // backward LDS.128 is 4 wavefronts; with qz-stride 16 and no shift it was 8)
 constexpr int kCFS = 72;
 __host__ __device__ constexpr int cfq(int q) { return q + ((q >> 5) << 2); }
-constexpr int oTZ = oSY;              // tz[4][2][27] aliases sy (dead after the pointwise phase)
+constexpr int oTZ = oSY;              // tz[4][2][kTZS] aliases sy (dead after the pointwise phase)
+constexpr int kTZS = 28;              // row stride of tz: with 28 the backward stage's 32 output
+                                      // stores (row cp, offsets 0/7/14/21) hit 32 distinct banks
 constexpr int kCellFloats = (oCF + kNCF * kCFS + 3) / 4 * 4;
-static_assert(oTZ + 4 * 2 * 27 <= oCF, "tz must fit in sy");
+static_assert(oTZ + 4 * 2 * kTZS <= oCF, "tz must fit in sy");
 static_assert(oSY % 4 == 0 && oCF % 4 == 0, "float4 alignment");
 
 // Layout of the geometry-cached form: J^-1 and w per Gauss point come from a per-mesh
@@ -97,13 +99,18 @@ struct KLay {
   static constexpr int US = CACHED ? 28 : 27;         // field stride of u (28: rows 16-byte aligned,
                                                       // the forward x-y stage reads them as float4)
   static constexpr int FO = NF - 4;                    // index of p among them
-  static constexpr int oCF = oSY + NF * kSYF;
+  // start of field f in sy.  Cached forms: the forward x-y stage runs on lanes (f, qx, qy half),
+  // whose stores are 8 floats apart per half; fields 2 and 3 are shifted by 8 so that the eight
+  // (f, half) groups of a store hit eight distinct 4-bank groups (with the plain stride: 2-way
+  // conflicts on all 18 stores per lane)
+  __host__ __device__ static constexpr int sy(int f) { return f * kSYF + (CACHED && f >= 2 ? 8 : 0); }
+  static constexpr int oCF = oSY + NF * kSYF + (CACHED ? 8 : 0);
   static constexpr int oGQ = oCF + kNCF * kCFS;        // cached [J^-1 (9) | w][64]
   static constexpr int oBar = oGQ + 10 * 64;           // cached: the staging mbarrier (8 B)
   // a block of zeros: the value-test array of the part-1 (LPS) lanes of the backward stage
   static constexpr int oZero = (oGQ + (GEO == GEO_CACHED ? 10 * 64 + 4 : 0) + 3) / 4 * 4;
   static constexpr int kFloats = oZero + kCFS + 32;
-  static_assert(oTZ + 4 * 2 * 27 <= oCF && oCF % 4 == 0 && oGQ % 4 == 0, "layout");
+  static_assert(oTZ + 4 * 2 * kTZS <= oCF && oCF % 4 == 0 && oGQ % 4 == 0, "layout");
 };
 // coefficient arrays (numbered so that every backward load slot hits distinct banks)
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
@@ -490,7 +497,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
           aB[iz][iy] = fmaf(bx2, u2, fmaf(bx1, u1, bx0 * u0));
           aD[iz][iy] = fmaf(dx2, u2, fmaf(dx1, u1, dx0 * u0));
         }
-      float* dst = S + oSY + f * kSYF + qx;
+      float* dst = S + oSY + L::sy(f) + qx;
 #pragma unroll
       for (int qq = 0; qq < QYH; ++qq) {
         const int qy = qy0 + qq;
@@ -521,7 +528,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
       float F[NF][4], G[NF][4];
 #pragma unroll
       for (int f = 0; f < NF; ++f) {
-        const float* src = S + oSY + f * kSYF + yx;  // [(kind*3 + iz)*16]
+        const float* src = S + oSY + L::sy(f) + yx;  // [(kind*3 + iz)*16]
         const float vv0 = src[0], vv1 = src[16], vv2 = src[32];
         const float vd0 = src[48], vd1 = src[64], vd2 = src[80];
         const float dv0 = src[96], dv1 = src[112], dv2 = src[128];
@@ -634,7 +641,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
         const float keep = hi1 ? o[14 + k] : o[k];
         k14[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
       }
-      float* out = S + oTZ + cp * 27 + (hi1 ? 14 : 0) + (hi0 ? 7 : 0);
+      float* out = S + oTZ + cp * kTZS + (hi1 ? 14 : 0) + (hi0 ? 7 : 0);
       const int nvalid = (hi1 && hi0) ? 6 : 7;  // 27 = 7 + 7 + 7 + 6
 #pragma unroll
       for (int k = 0; k < 7; ++k) {
@@ -653,7 +660,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     if constexpr (MODE == MODE_OPERATOR) {
       const int comp = t >> 3, v = t & 7;
       const int it0 = (v & 1) ? 2 : 0, it1 = (v & 2) ? 2 : 0, it2 = (v & 4) ? 2 : 0;
-      const float* gp = S + oTZ + (comp * 2 + 1) * 27;
+      const float* gp = S + oTZ + (comp * 2 + 1) * kTZS;
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         const int b0 = (m & 1) ? 1 : it0, b1 = (m & 2) ? 1 : it1, b2 = (m & 4) ? 1 : it2;
@@ -669,7 +676,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
 #pragma unroll
       for (int comp = 0; comp < 4; ++comp) {
         const float l = __shfl_sync(0xffffffffu, lps, comp * 8 + (vid & 7));
-        e[comp] = t < 27 ? S[oTZ + (comp * 2) * 27 + t] + (vtx ? l : 0.f) : 0.f;
+        e[comp] = t < 27 ? S[oTZ + (comp * 2) * kTZS + t] + (vtx ? l : 0.f) : 0.f;
       }
       if (t < 27) A.elem[(int64_t)c * 27 + t] = make_float4(e[0], e[1], e[2], e[3]);
     }

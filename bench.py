@@ -866,12 +866,6 @@ def run_ours(args, rank, world, local):
                "note": "Alg. 1 lines 8-9 (next-step RHS, P^T restriction); outside the timed step"}
     except Exception as exc:  # pragma: no cover - auxiliary numbers only
         aux = {"error": str(exc)[:200]}
-    if not args.no_aux:
-        for key, fn in (("dataset_rows", dataset_aux), ("vanka", vanka_aux)):
-            try:
-                aux[key] = fn(step, args.steps, barrier)
-            except Exception as exc:  # pragma: no cover - auxiliary numbers only
-                aux[key] = {"error": str(exc)[:200]}
     # the same step replayed from CUDA graphs (one per input pair): removes launch gaps,
     # which dominate for the small configs
     graphs = []
@@ -934,6 +928,15 @@ def run_ours(args, rank, world, local):
                "d2h_bytes_per_step": int(hout[0].numel() * 4),
                "overlap": "H2D(i+1) | kernels(i) | D2H(i-1) on 3 streams (step.HostPipeline)"}
 
+    # the rows around the step (training-data rows + statistics, Vanka sweeps): after the e2e
+    # measurement -- their host-side setup (scipy / BLAS worker threads) otherwise competes with
+    # the thread that enqueues the pipelined copies (e2e 269 M instead of 295 M patches/s)
+    if not args.no_aux:
+        for key, fn in (("dataset_rows", dataset_aux), ("vanka", vanka_aux)):
+            try:
+                aux[key] = fn(step, args.steps, barrier)
+            except Exception as exc:  # pragma: no cover - auxiliary numbers only
+                aux[key] = {"error": str(exc)[:200]}
     if rank != 0:
         if world > 1:
             tdist.destroy_process_group()

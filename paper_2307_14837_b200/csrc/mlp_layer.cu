@@ -16,6 +16,8 @@
 // fp32 skip sum and writes both the fp32 skip state and the next layer's split operand
 // (or, for the head, Y).  Warp roles (320 threads): warps 0-7 epilogue (TMEM lane quadrant
 // x column half), warp 8 TMA producer, warp 9 MMA issuer.
+#include <cstdlib>
+
 #include "tc_common.cuh"
 
 namespace dnnmg {
@@ -439,6 +441,59 @@ int32_t mlp_layered_workspace_bytes(const dnnmg_mlp_t* m, int64_t n_rows, int64_
   return DNNMG_OK;
 }
 
+// The patch form with whole nodes per load: 4 consecutive operand columns are the 4 components
+// of one node (x~ or r, a float4 gather through the patch's node table) or 4 geometry values, so
+// a thread's HC columns take HC/4 table loads and HC/4 float4 loads instead of 2 HC dependent
+// scalar loads; mean / std are read as float4.  (Needs n_geo % 4 == 0 and 16-byte aligned x, r,
+// geom, mean, std.)  LANES_ROWS: consecutive lanes take consecutive rows of one column group
+// (their 16-byte operand stores form 128-byte runs of the canonical layout) instead of
+// consecutive column groups of one row.
+template <int MODE, bool LANES_ROWS>
+__global__ void __launch_bounds__(256) layer_input_patch4_kernel(PatchRows P, int64_t r0, int64_t n,
+                                                                 int64_t n_rows_pad, int n_in,
+                                                                 int n_kc,
+                                                                 const float* __restrict__ mean,
+                                                                 const float* __restrict__ std_,
+                                                                 uint8_t* __restrict__ out) {
+  using C = TcCfg<MODE>;
+  constexpr int KC = C::KC, HC = KC / 2;
+  constexpr uint32_t AST = kTcM * KC * C::ESZ * C::PARTS;
+  const int groups = n_kc * 2;
+  const int64_t total = n_rows_pad * groups;
+  const int nb = 4 * P.npp;
+  const float4* x4 = reinterpret_cast<const float4*>(P.x);
+  const float4* r4 = reinterpret_cast<const float4*>(P.r);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = LANES_ROWS ? i % n_rows_pad : i / groups;
+    const int g = (int)(LANES_ROWS ? i / n_rows_pad : i - r * groups);
+    const int col0 = g * HC;
+    const int64_t p = r0 + r;
+    float v[HC];
+#pragma unroll
+    for (int q = 0; q < HC / 4; ++q) {
+      const int col = col0 + 4 * q;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < n && col < n_in) {
+        if (col < nb) x = __ldg(x4 + __ldg(P.table + p * P.npp + (col >> 2)));
+        else if (col < 2 * nb) x = __ldg(r4 + __ldg(P.table + p * P.npp + ((col - nb) >> 2)));
+        else x = __ldg(reinterpret_cast<const float4*>(P.geom + p * P.n_geo + (col - 2 * nb)));
+        const float4 m = __ldg(reinterpret_cast<const float4*>(mean + col));
+        const float4 sd = __ldg(reinterpret_cast<const float4*>(std_ + col));
+        x = make_float4((x.x - m.x) / sd.x, (x.y - m.y) / sd.y, (x.z - m.z) / sd.z,
+                        (x.w - m.w) / sd.w);
+      }
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
+    }
+    const int64_t t = r / kTcM;
+    uint8_t* chunk = out + (t * n_kc + col0 / KC) * AST;
+    put_row<MODE>(chunk, (int)(r % kTcM), col0 % KC, v);
+  }
+}
+
 int32_t launch_mlp_layered_pack(const dnnmg_mlp_t* m, void* packed, cudaStream_t s) {
   DNNMG_REQUIRE(mlp_layered_supported(m), DNNMG_ERR_UNSUPPORTED,
                 "mlp: layered tensor-core mode needs n_hidden %% 32 == 0");
@@ -494,7 +549,17 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, const PatchRow
     const int tiles = (int)((n + kTcM - 1) / kTcM);
     const int kc0 = L.K[0] / C::KC;
     const int in_grid = grid_for((int64_t)tiles * kTcM * kc0 * 2, 256);
-    if (P)
+    const bool vec4 = P && P->n_geo % 4 == 0 && m->n_in % 4 == 0 &&
+                      (((uintptr_t)P->x | (uintptr_t)P->r | (uintptr_t)P->geom |
+                        (uintptr_t)m->in_mean | (uintptr_t)m->in_std) & 15) == 0;
+    static const int in_mode = getenv("DNNMG_LAYER_INPUT") ? atoi(getenv("DNNMG_LAYER_INPUT")) : 2;
+    if (vec4 && in_mode == 2)
+      layer_input_patch4_kernel<MODE, true><<<in_grid, 256, 0, s>>>(
+          *P, r0, n, (int64_t)tiles * kTcM, m->n_in, kc0, m->in_mean, m->in_std, abuf[0]);
+    else if (vec4 && in_mode == 1)
+      layer_input_patch4_kernel<MODE, false><<<in_grid, 256, 0, s>>>(
+          *P, r0, n, (int64_t)tiles * kTcM, m->n_in, kc0, m->in_mean, m->in_std, abuf[0]);
+    else if (P)
       layer_input_kernel<MODE, true><<<in_grid, 256, 0, s>>>(
           nullptr, *P, r0, n, (int64_t)tiles * kTcM, m->n_in, kc0, m->in_mean, m->in_std, abuf[0]);
     else

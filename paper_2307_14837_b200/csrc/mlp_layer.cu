@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
   uint64_t* acc_full = bars + 2 * NS;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // head epilogue: a padded 32 x GS staging tile per epilogue warp (after the barriers)
+  float* ystage = reinterpret_cast<float*>(smem + NS * STG + 8 * (2 * NS + 4) + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_items = (int64_t)A.n_tiles * A.n_nb;
   const bool seg2 = MODE == DNNMG_PREC_TF32X3 && A.n_kc * KC > 512;
@@ -195,11 +197,24 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
         }
         const int col0 = b * kLN + cc;          // layer column of v[0]
         if (A.head) {
-          if (live) {
+          // Y rows are n_out floats apart (375 or 81: not 16-byte aligned), and a lane holds one
+          // row: stored from the registers, every store instruction hit 32 sectors with 4 bytes
+          // each (the head took longer than a hidden layer).  The 32 x GS block goes through a
+          // padded shared-memory tile and leaves as 64- or 128-byte row segments.
+          float* st = ystage + (warp * 32) * (GS + 1);
 #pragma unroll
-            for (int e = 0; e < GS; ++e)
-              if (col0 + e < A.n_out) A.Y[grow * A.n_out + col0 + e] = v[e] * yu;
+          for (int e = 0; e < GS; ++e) st[lane * (GS + 1) + e] = v[e] * yu;
+          __syncwarp();
+          constexpr int RPI = 32 / GS;   // rows per store instruction
+          const int e = lane % GS;
+#pragma unroll 4
+          for (int rr = 0; rr < 32; rr += RPI) {
+            const int rl = rr + lane / GS;
+            const int64_t gr = (int64_t)t * kTcM + quad * 32 + rl;
+            if (gr < A.n_rows && col0 + e < A.n_out)
+              A.Y[gr * A.n_out + col0 + e] = st[rl * (GS + 1) + e];
           }
+          __syncwarp();
           continue;
         }
         float hv[GS];
@@ -526,7 +541,8 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, const PatchRow
   constexpr int NS = LCfg<MODE>::NS;
   constexpr size_t STG = (size_t)kTcM * C::KC * C::ESZ * C::PARTS +
                          (size_t)kLN * C::KC * C::ESZ * C::PARTS;
-  const size_t smem = NS * STG + 8 * (2 * NS + 4) + 16;
+  constexpr int GS = C::KC / 2 > 16 ? C::KC / 2 : 16;   // (as in the kernel's epilogue)
+  const size_t smem = NS * STG + 8 * (2 * NS + 4) + 16 + 8 * 32 * (GS + 1) * sizeof(float);
   const LayeredGeom L = layered_geom(m, n_rows);
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* abuf[2] = {base, base + L.a_bytes};

@@ -14,8 +14,8 @@
 // consumes it, so the producer is one bulk copy per K chunk; weights are pre-packed per
 // (K chunk, N block) the same way.  The fused epilogue applies BN + activation + the
 // fp32 skip sum and writes both the fp32 skip state and the next layer's split operand
-// (or, for the head, Y).  Warp roles (320 threads): warps 0-7 epilogue (TMEM lane quadrant
-// x column half), warp 8 TMA producer, warp 9 MMA issuer.
+// (or, for the head, Y).  Warp roles (576 threads): warps 0-15 epilogue (TMEM lane quadrant
+// x every fourth column step), warp 16 TMA producer, warp 17 MMA issuer.
 #include <cstdlib>
 
 #include "tc_common.cuh"
@@ -23,8 +23,14 @@
 namespace dnnmg {
 
 constexpr int kLN = 256;          // accumulator columns per work item
-constexpr int kLThreads = 320;
-constexpr int kLProd = 8, kLMma = 9;
+#ifndef DNNMG_LAYER_EPI_WARPS
+#define DNNMG_LAYER_EPI_WARPS 16
+#endif
+constexpr int kLEpi = DNNMG_LAYER_EPI_WARPS;   // epilogue warps: 4 per TMEM lane quadrant (the
+                                               // hidden layers are epilogue-latency-bound: with 2
+                                               // per quadrant the tensor pipe idled half the time)
+constexpr int kLThreads = 32 * (kLEpi + 2);
+constexpr int kLProd = kLEpi, kLMma = kLEpi + 1;
 constexpr int64_t kLChunkRows = 1 << 19;   // rows per pass (bounds the workspace)
 
 template <int MODE> struct LCfg { static constexpr int NS = 4; };
@@ -80,7 +86,7 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), 8);
+      mbar_init(smem_u32(&acc_empty[i]), kLEpi);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
     }
   } else {
     // ---------------- epilogue warps ----------------
-    const int quad = warp & 3, half = warp >> 2;
+    const int quad = warp & 3, part = warp >> 2;   // part: which GS-column steps of an item
     const int row = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     constexpr bool accurate = MODE == DNNMG_PREC_F16X3 || MODE == DNNMG_PREC_TF32X3;
@@ -183,8 +189,7 @@ __global__ void __launch_bounds__(kLThreads, 1) mlp_layer_kernel(LayerArgs A) {
         mbar_wait(smem_u32(&acc_full[buf]), (j >> 1) & 1);
       }
       tc_fence_after();
-      const int c0 = half * (nbw / 2);
-      for (int cc = c0; cc < c0 + nbw / 2; cc += GS) {
+      for (int cc = part * GS; cc < nbw; cc += (kLEpi / 4) * GS) {
         float v[GS];
 #pragma unroll
         for (int p = 0; p < GS / 16; ++p) tmem_ld16(tmem + lane_addr + buf * kLN + cc + 16 * p, v + 16 * p);
@@ -542,7 +547,7 @@ static int32_t layered_mode(const dnnmg_mlp_t* m, const float* X, const PatchRow
   constexpr size_t STG = (size_t)kTcM * C::KC * C::ESZ * C::PARTS +
                          (size_t)kLN * C::KC * C::ESZ * C::PARTS;
   constexpr int GS = C::KC / 2 > 16 ? C::KC / 2 : 16;   // (as in the kernel's epilogue)
-  const size_t smem = NS * STG + 8 * (2 * NS + 4) + 16 + 8 * 32 * (GS + 1) * sizeof(float);
+  const size_t smem = NS * STG + 8 * (2 * NS + 4) + 16 + kLEpi * 32 * (GS + 1) * sizeof(float);
   const LayeredGeom L = layered_geom(m, n_rows);
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* abuf[2] = {base, base + L.a_bytes};

@@ -144,3 +144,38 @@ def test_tile_tables_cover_node_table():
         assert np.array_equal(nodes[t][slot[128 * t:128 * t + len(rows)].astype(np.int64)], rows)
         assert np.all(np.diff(nodes[t][:count[t]]) > 0)
         assert count[t] == np.unique(rows).size
+
+
+def test_lattice_table_reproduces_prolongation(case):
+    """K1's lattice table (device.lattice_table: the owned fine node at every position of each
+    parent cell's 5 x 5 x 5 lattice) against the prolongation matrix that is pinned bit-exact
+    above: the tensor product of the 1-D quarter-point stencils at a node's lattice position, on
+    its parent's 27 nodes, is exactly that node's row of P; every fine node is owned once."""
+    from paper_2307_14837_b200 import device as dv
+    name, g, h = case
+    L, J = int(g["L"]), int(g["J"])
+    w1 = {0: {0: 1.0}, 1: {0: 0.375, 1: 0.75, 2: -0.125}, 2: {1: 1.0},
+          3: {0: -0.125, 1: 0.75, 2: 0.375}, 4: {2: 1.0}}
+    for l in range(L, L + J):
+        P = spmod.prolongation_matrix(h, l).tocsr()
+        ctab = h.scalar_nodes(l)[1]
+        src = spmod.prolongation_source(h, l)
+        lat = dv.lattice_table(src, ctab.shape[0])
+        assert lat.shape == (ctab.shape[0], 125)
+        owned = lat[lat >= 0]
+        assert np.array_equal(np.sort(owned), np.arange(P.shape[0]))
+        rng = np.random.default_rng(5)
+        cells = rng.choice(ctab.shape[0], size=min(40, ctab.shape[0]), replace=False)
+        for C in cells:
+            for pos in np.nonzero(lat[C] >= 0)[0]:
+                n = lat[C, pos]
+                px, py, pz = pos % 5, (pos // 5) % 5, pos // 25
+                row = {}
+                for iz, wz in w1[pz].items():
+                    for iy, wy in w1[py].items():
+                        for ix, wx in w1[px].items():
+                            m = ctab[C, 9 * iz + 3 * iy + ix]
+                            row[m] = row.get(m, 0.0) + wx * wy * wz
+                ref = dict(zip(P.indices[P.indptr[n]:P.indptr[n + 1]],
+                               P.data[P.indptr[n]:P.indptr[n + 1]]))
+                assert row == ref, (l, C, pos, n)

@@ -59,6 +59,18 @@ def global_level0_vertices(lo, hi, n_cells, jitter_seed=None):
     return V
 
 
+def global_is_box(V, n_cells, rtol=1e-13):
+    """True when the global level-0 vertices (x fastest) form an axis-aligned tensor grid:
+    every refined level then consists of axis-aligned boxes on every rank, and K2 may take its
+    box form on all of them (as the single domain does)."""
+    nx, ny, nz = (int(v) for v in n_cells)
+    X = np.asarray(V, dtype=float).reshape(nz + 1, ny + 1, nx + 1, 3)
+    tol = rtol * max(float(np.abs(X).max()), 1.0)
+    return bool(np.abs(X[..., 0] - X[0, 0, :, 0][None, None, :]).max() <= tol
+                and np.abs(X[..., 1] - X[0, :, 0, 1][None, :, None]).max() <= tol
+                and np.abs(X[..., 2] - X[:, 0, 0, 2][:, None, None]).max() <= tol)
+
+
 def global_cell_ids(lat, level, n0):
     """Global cell id of level-`level` cells with lattice index lat (n, 3) in a box of
     n0 = (NX, NY, NZ) level-0 cells: level-0 cells are numbered k, then i, j fastest
@@ -124,6 +136,7 @@ class SlabPartition:
         self.n_cells_global = self.n0
         self.a, self.b = slab_ranges(self.n0[0], world)[rank]
         V0 = global_level0_vertices(lo, hi, n_cells, jitter_seed)
+        self.global_box = global_is_box(V0, n_cells)
         self.h = meshmod.build_subbox(V0, n_cells, (self.a, self.b), lo, hi, channel_tags)
         for _ in range(L + J):
             meshmod.refine_uniform(self.h)
@@ -292,7 +305,10 @@ class SlabStep:
         bcs = bcs if bcs is not None else {meshmod.WALL: no_slip}
         self.step = CorrectionStep(part.h, part.L, part.J, model, nu, k, bcs=bcs, alpha0=alpha0,
                                    delta0=delta0, scale=scale, precision=precision,
-                                   patchset=part.patchset, t=t, mask=part.mask)
+                                   patchset=part.patchset, t=t, mask=part.mask,
+                                   # one element-kernel form on every rank (bitwise equal to the
+                                   # single domain): the box form only for an unjittered box
+                                   k2_box=None if getattr(part, "global_box", True) else False)
         dev = dv.device()
         self._keep = []
 

@@ -29,8 +29,12 @@ def constrained_mask(space, bcs):
 
 class CorrectionStep:
     def __init__(self, hierarchy, L, J, model, nu, k, bcs=None, alpha0=0.02, delta0=0.1,
-                 scale=1.0, precision="fp32", patchset=None, t=0.0, mask=None):
+                 scale=1.0, precision="fp32", patchset=None, t=0.0, mask=None, k2_box=None):
+        """k2_box: None = K2's box form whenever the fine level is axis-aligned (checked on the
+        device); False = never (the slab decomposition passes it for a jittered global mesh so
+        that every rank runs the same element-kernel form as the single domain)."""
         self.hierarchy, self.L, self.J = hierarchy, L, J
+        self.k2_box = k2_box
         self.bcs = bcs if bcs is not None else {meshmod.WALL: no_slip}
         self.scale = float(scale)
         self.nu, self.k = nu, k
@@ -42,7 +46,7 @@ class CorrectionStep:
         self.mask = constrained_mask(self.space, self.bcs) if mask is None else np.asarray(mask)
         self.mask_bits = dv.upload(dv.dof_mask_bits(self.mask, self.space.n_nodes), np.uint8)
         # K2 reads J^-1 and w from the per-mesh geometry cache (the mesh is fixed in time)
-        self.lv = self.level.struct(self.mask_bits, geometry=True)
+        self.lv = self.level.struct(self.mask_bits, geometry=True, box=self.k2_box)
         self.patchset = patchset if patchset is not None else meshmod.build_patches(hierarchy, L, J)
         self.ps = dv.DevicePatchSet.get(self.patchset)
         self.precision = precision
@@ -249,7 +253,7 @@ class CorrectionStep:
     def rhs_next(self, x, out=None):
         """Next-step fine RHS from a (corrected) fine state (assembly.py:242-259)."""
         out = torch.empty_like(self.x_tilde) if out is None else out
-        lv = self.level.struct(geometry=True)
+        lv = self.level.struct(geometry=True, box=self.k2_box)
         _lib.call("dnnmg_rhs_next", ctypes.byref(lv), dv.ptr(x), ctypes.byref(self.phys),
                   dv.ptr(self.elem), dv.ptr(out), dv.stream_handle())
         return out

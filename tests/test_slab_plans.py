@@ -84,3 +84,20 @@ def test_merge_plans_follow_global_order(n_cells, L, J, world):
             assert np.array_equal(theirs["remote_ids"], mine["own_ids"])
             assert np.array_equal(parts[r].fine_pos[mine["nodes"]],
                                   parts[r + 1].fine_pos[theirs["nodes"]])
+
+
+def test_global_box_predicate():
+    """Every rank decides from the global level-0 vertices whether K2 may take its box form, so
+    that all ranks run the element-kernel form of the single domain."""
+    from paper_2307_14837_b200 import slab
+    lo, hi = (0.0, 0.0, 0.0), (1.0, 0.5, 0.5)
+    assert slab.global_is_box(slab.global_level0_vertices(lo, hi, (4, 3, 2), None), (4, 3, 2))
+    assert not slab.global_is_box(slab.global_level0_vertices(lo, hi, (8, 2, 2), 31), (8, 2, 2))
+    # one cell across y and z: no interior vertex, nothing is jittered
+    assert slab.global_is_box(slab.global_level0_vertices(lo, hi, (8, 1, 1), 31), (8, 1, 1))
+    for world in (1, 2):
+        for rank in range(world):
+            p = slab.SlabPartition(lo, hi, (4, 2, 2), 0, 1, world, rank, jitter_seed=7)
+            assert p.global_box is False
+            p = slab.SlabPartition(lo, hi, (4, 2, 2), 0, 1, world, rank)
+            assert p.global_box is True

@@ -86,3 +86,42 @@ def test_layered_workspace_size_is_checked():
     rc = lib.dnnmg_mlp_forward_ws(ctypes.byref(m), dummy, rows, dummy, dummy, need.value - 1,
                                   None)
     assert rc == 1 and b"workspace" in lib.dnnmg_last_error()
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The ctypes mirror of every C-ABI struct (paper_2307_14837_b200/_lib.py, the binding a
+    reference maintainer would write) has the size and the field offsets a C compiler gives
+    include/dnnmg_b200.h: a field appended on one side only would shift every later one."""
+    import ctypes
+    pairs = {"dnnmg_prolong_t": _lib.Prolong, "dnnmg_restrict_t": _lib.Restrict,
+             "dnnmg_dirichlet_t": _lib.Dirichlet, "dnnmg_level_t": _lib.Level,
+             "dnnmg_phys_t": _lib.Phys, "dnnmg_patchset_t": _lib.PatchSet,
+             "dnnmg_mlp_t": _lib.Mlp, "dnnmg_csr_t": _lib.Csr, "dnnmg_vanka_t": _lib.Vanka,
+             "dnnmg_step_buffers_t": _lib.StepBuffers, "dnnmg_halo_plan_t": _lib.HaloPlan,
+             "dnnmg_slab_t": _lib.Slab}
+    src = open(HEADER).read()
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dnnmg_b200.h"',
+             'int main(void) {']
+    fields = {}
+    for cname in pairs:
+        body = re.search(r"typedef struct \{([^{}]*)\}\s*" + cname + ";",
+                         re.sub(r"/\*.*?\*/", "", src, flags=re.S)).group(1)
+        names = [re.search(r"(\w+)\s*(?:\[[^\]]*\])?\s*$", part.strip()).group(1)
+                 for d in body.split(";") if d.strip() for part in d.split(",")]
+        fields[cname] = names
+        lines.append(f'  printf("{cname} %zu", sizeof({cname}));')
+        for f in names:
+            lines.append(f'  printf(" %zu", offsetof({cname}, {f}));')
+        lines.append('  printf("\\n");')
+    lines += ['  return 0;', '}']
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(REPO, "include"), str(c), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    for row in out.strip().splitlines():
+        cname, size, *offs = row.split()
+        cls = pairs[cname]
+        assert ctypes.sizeof(cls) == int(size), cname
+        assert [f for f, _ in cls._fields_] == fields[cname], cname
+        assert [getattr(cls, f).offset for f, _ in cls._fields_] == [int(o) for o in offs], cname

@@ -116,7 +116,14 @@ struct KLay {
 constexpr int CA = 0;        // A[c]      value test           (c = 0..3)
 constexpr int CB = 4;        // B[c][k]   reference-gradient test
 constexpr int CP = 16;       // P[i][k] = delta*w*g_i (J^-1 pi v)_k: LPS Gpi test, comps 1..3
-constexpr int kWarpsPerBlock = 4;
+#ifndef DNNMG_K2_WPB
+#define DNNMG_K2_WPB 16
+#endif
+// warps per block of the element kernel.  Operator form (128 registers, 16 warps per SM either
+// way): one 16-warp block per SM instead of four 4-warp blocks, 0.827 -> 0.805 ms at config 3 (the
+// warps of one block stay in step and work on neighbouring cells); the RHS form (95-107
+// registers) keeps 4-warp blocks, of which five fit an SM (0.63 vs 0.70 ms at config 2).
+__host__ __device__ constexpr int k2_warps_per_block(int mode) { return mode == 1 ? 4 : DNNMG_K2_WPB; }
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
@@ -392,7 +399,9 @@ __device__ __forceinline__ void pointwise(const ResidualArgs& A, const float* S,
 }
 
 template <int MODE, int GEO>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(ResidualArgs A) {
+__global__ void __launch_bounds__(32 * k2_warps_per_block(MODE), 16 / k2_warps_per_block(MODE))
+    element_kernel(ResidualArgs A) {
+  constexpr int kWarpsPerBlock = k2_warps_per_block(MODE);
   using L = KLay<GEO>;
   constexpr bool CACHED = L::CACHED;          // 4 fields through the forward stages
   constexpr bool STAGED = GEO == GEO_CACHED;  // per-point geometry block staged per cell
@@ -401,8 +410,26 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
   const int wib = threadIdx.x >> 5;
   const int t = threadIdx.x & 31;
   float* S = smem + wib * L::kFloats;
-  const int stride = gridDim.x * kWarpsPerBlock;
-  int c = blockIdx.x * kWarpsPerBlock + wib;
+#ifdef DNNMG_K2_GRIDSTRIDE
+  constexpr bool kChunked = false;
+#else
+  // (measured: box form 0.805 -> 0.799 ms at config 3; general form 0.915 -> 0.917 at config 2)
+  constexpr bool kChunked = MODE == MODE_OPERATOR && GEO == GEO_BOX;
+#endif
+  int stride, c, c_end;
+  if constexpr (!kChunked) {
+    stride = gridDim.x * kWarpsPerBlock;
+    c = blockIdx.x * kWarpsPerBlock + wib;
+    c_end = A.n_cells;
+  } else {
+  // a block takes a contiguous range of cells and its warps walk it side by side: the cells in
+  // flight on an SM (and those of the next iterations) are neighbours in the numbering -- the
+  // eight children of a coarse cell, then its x neighbour -- and share their nodes in L1
+    stride = kWarpsPerBlock;
+    const int per_block = (A.n_cells + gridDim.x - 1) / gridDim.x;
+    c = blockIdx.x * per_block + wib;
+    c_end = min(A.n_cells, (int)(blockIdx.x + 1) * per_block);
+  }
   NodeRaw raw;
   int idx_next = 0;  // node index of cell c + stride (lane t < 27)
   const uint32_t bar = smem_u32(S + L::oBar);
@@ -419,14 +446,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
   // Gauss weights of this lane's two points q = t and t + 32 (box form: w = wq det J)
   const float wq_a = cW[t & 3] * cW[(t >> 2) & 3] * cW[t >> 4];
   const float wq_b = cW[t & 3] * cW[(t >> 2) & 3] * cW[(t >> 4) + 2];
-  if (c < A.n_cells) {
+  if (c < c_end) {
     const int node = t < 27 ? __ldg(A.cell_nodes + (int64_t)c * 27 + t) : 0;
     load_raw<GEO>(A, c, node, t, raw);
-    if (c + stride < A.n_cells && t < 27) idx_next = __ldg(A.cell_nodes + (int64_t)(c + stride) * 27 + t);
+    if (c + stride < c_end && t < 27) idx_next = __ldg(A.cell_nodes + (int64_t)(c + stride) * 27 + t);
     if constexpr (STAGED) stage_geo(A, c, t, S + L::oGQ, bar);
   }
 
-  for (; c < A.n_cells; c += stride) {
+  for (; c < c_end; c += stride) {
     // ---------------- gather (prefetched one cell ahead), stab ----------------
     float vsq = 0.f;  // |v|^2 of this lane's node; vmax = sqrt(max |v|^2) (sqrt is monotone)
     if (t < 27) {
@@ -448,9 +475,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     }
     const float hT = raw.hT;
     const float4 box = raw.gb;
-    if (c + stride < A.n_cells) {  // issue the loads of the next cell (consumed next iteration)
+    if (c + stride < c_end) {  // issue the loads of the next cell (consumed next iteration)
       load_raw<GEO>(A, c + stride, idx_next, t, raw);
-      if (c + 2 * stride < A.n_cells && t < 27)
+      if (c + 2 * stride < c_end && t < 27)
         idx_next = __ldg(A.cell_nodes + (int64_t)(c + 2 * stride) * 27 + t);
     }
     // non-negative floats order like their bit patterns: one warp-wide integer max (its result
@@ -561,7 +588,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) element_kernel(Residua
     }
     __syncwarp();
     if constexpr (STAGED) {
-      if (c + stride < A.n_cells) stage_geo(A, c + stride, t, S + L::oGQ, bar);
+      if (c + stride < c_end) stage_geo(A, c + stride, t, S + L::oGQ, bar);
     }
     // ---------------- backward x, y, z in registers: lane (cp, qz), cp = (comp, part) ----------------
     // tz[cp][iz][iy][ix] = sum_q test(q; ix, iy, iz) . coefficients(cp, q).  Each of the 32
@@ -772,6 +799,7 @@ int32_t launch_k2tc_elements(const dnnmg_level_t*, const float*, const float*, c
 
 template <int MODE, int GEO>
 static void launch_element_kernel(const ResidualArgs& A, cudaStream_t s) {
+  constexpr int kWarpsPerBlock = k2_warps_per_block(MODE);
   constexpr size_t smem = sizeof(float) * KLay<GEO>::kFloats * kWarpsPerBlock;
   static uint64_t configured = 0;
   if (first_use_on_device(configured))

@@ -80,6 +80,7 @@ constexpr int kNCF = 25;
 constexpr int kCFS = 72;
 __host__ __device__ constexpr int cfq(int q) { return q + ((q >> 5) << 2); }
 constexpr int oTZ = oSY;              // tz[4][2][kTZS] aliases sy (dead after the pointwise phase)
+constexpr int kTZ2 = 33;              // row stride of tz in the split backward form (4 rows)
 constexpr int kTZS = 28;              // row stride of tz: with 28 the backward stage's 32 output
                                       // stores (row cp, offsets 0/7/14/21) hit 32 distinct banks
 constexpr int kCellFloats = (oCF + kNCF * kCFS + 3) / 4 * 4;
@@ -590,6 +591,102 @@ __global__ void __launch_bounds__(32 * k2_warps_per_block(MODE), 16 / k2_warps_p
     if constexpr (STAGED) {
       if (c + stride < c_end) stage_geo(A, c + stride, t, S + L::oGQ, bar);
     }
+    constexpr int kTZO = MODE == MODE_RHS ? kTZ2 : 2 * kTZS;   // row stride of the direct-test rows
+    float lps = 0.f;
+    if constexpr (MODE == MODE_RHS) {
+    // ---------------- backward, RHS form: the direct test on all 32 lanes ----------------
+    // The RHS form has no LPS part, so instead of lanes (comp, part, qz) with idle part-1 lanes
+    // lane (comp, qz, h) contracts the two qy lines 2h, 2h+1 of plane qz for all three ix (x
+    // stage), those qy (y stage), adds its share of the qz sum to all 27 outputs, and the eight
+    // (qz, h) partials of a component are combined by a three-step shuffle reduce-scatter into
+    // tz[comp][27]: rhs_next 0.613 -> 0.558 ms at config 3, 0.710 -> 0.632 ms at config 2.  (For
+    // the operator form the same split, with the LPS test as a direct trilinear contraction,
+    // executed 3 % fewer instructions but ran 3 % slower in the step -- DESIGN.md, dead ends.)
+    {
+      const int comp = t >> 3, g = t & 7, qz = g >> 1, hq = g & 1;
+      const bool b2 = (g & 4) != 0, b1 = (g & 2) != 0, b0 = (g & 1) != 0;
+      const int qoff = cfq(16 * qz) + 8 * hq;   // first Gauss point of this lane's two lines
+      {
+        const float* c0 = S + L::oCF + (CA + comp) * kCFS + qoff;
+        const float* c1 = S + L::oCF + (CB + 3 * comp) * kCFS + qoff;
+        const float* c2 = c1 + kCFS;
+        const float* c3 = c1 + 2 * kCFS;
+        float ua[3][3], ub[3][3];  // [iy][ix]
+#pragma unroll
+        for (int iy = 0; iy < 3; ++iy)
+#pragma unroll
+          for (int ix = 0; ix < 3; ++ix) ua[iy][ix] = ub[iy][ix] = 0.f;
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int qy = 2 * hq + qq;
+          const float by[3] = {cB[qy][0], cB[qy][1], cB[qy][2]};
+          const float dy[3] = {cD[qy][0], cD[qy][1], cD[qy][2]};
+          const float4 l0 = *reinterpret_cast<const float4*>(c0 + 4 * qq);
+          const float4 l1 = *reinterpret_cast<const float4*>(c1 + 4 * qq);
+          const float4 l2 = *reinterpret_cast<const float4*>(c2 + 4 * qq);
+          const float4 l3 = *reinterpret_cast<const float4*>(c3 + 4 * qq);
+          const float L0[4] = {l0.x, l0.y, l0.z, l0.w}, L1[4] = {l1.x, l1.y, l1.z, l1.w};
+          const float L2[4] = {l2.x, l2.y, l2.z, l2.w}, L3[4] = {l3.x, l3.y, l3.z, l3.w};
+#pragma unroll
+          for (int ix = 0; ix < 3; ++ix) {
+            float t0 = cB[0][ix] * L0[0], t1 = cB[0][ix] * L2[0], t2 = cB[0][ix] * L3[0];
+#pragma unroll
+            for (int qx = 1; qx < 4; ++qx) t0 = fmaf(cB[qx][ix], L0[qx], t0);
+#pragma unroll
+            for (int qx = 0; qx < 4; ++qx) t0 = fmaf(cD[qx][ix], L1[qx], t0);
+#pragma unroll
+            for (int qx = 1; qx < 4; ++qx) {
+              t1 = fmaf(cB[qx][ix], L2[qx], t1);
+              t2 = fmaf(cB[qx][ix], L3[qx], t2);
+            }
+#pragma unroll
+            for (int iy = 0; iy < 3; ++iy) {
+              ua[iy][ix] = fmaf(by[iy], t0, fmaf(dy[iy], t1, ua[iy][ix]));
+              ub[iy][ix] = fmaf(by[iy], t2, ub[iy][ix]);
+            }
+          }
+        }
+        const float bz[3] = {cB[qz][0], cB[qz][1], cB[qz][2]};
+        const float dz[3] = {cD[qz][0], cD[qz][1], cD[qz][2]};
+        float o[28];
+#pragma unroll
+        for (int iz = 0; iz < 3; ++iz)
+#pragma unroll
+          for (int iy = 0; iy < 3; ++iy)
+#pragma unroll
+            for (int ix = 0; ix < 3; ++ix)
+              o[9 * iz + 3 * iy + ix] = fmaf(bz[iz], ua[iy][ix], dz[iz] * ub[iy][ix]);
+        o[27] = 0.f;
+        // reduce-scatter over the eight lanes of this component: lane bit 2 picks the half
+        // [0,14) / [14,28), bit 1 the quarter [0,7) / [7,14) of it, bit 0 [0,4) / [4,8) of that
+        float k14[14];
+#pragma unroll
+        for (int k = 0; k < 14; ++k) {
+          const float send = b2 ? o[k] : o[14 + k];
+          const float keep = b2 ? o[14 + k] : o[k];
+          k14[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        float k7[8];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+          const float send = b1 ? k14[k] : k14[7 + k];
+          const float keep = b1 ? k14[7 + k] : k14[k];
+          k7[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        k7[7] = 0.f;
+        float* out = S + oTZ + comp * kTZ2 + (b2 ? 14 : 0) + (b1 ? 7 : 0) + (b0 ? 4 : 0);
+        const int nvalid = (b0 ? 3 : 4) - ((b2 && b1 && b0) ? 1 : 0);   // 27 = 4+3+4+3+4+3+4+2
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float send = b0 ? k7[k] : k7[4 + k];
+          const float keep = b0 ? k7[4 + k] : k7[k];
+          const float v = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+          if (k < nvalid) out[k] = v;
+        }
+      }
+    }
+    __syncwarp();
+    } else {
     // ---------------- backward x, y, z in registers: lane (cp, qz), cp = (comp, part) ----------------
     // tz[cp][iz][iy][ix] = sum_q test(q; ix, iy, iz) . coefficients(cp, q).  Each of the 32
     // lanes contracts the four (qy) lines of one qz plane for all three ix (x stage), then qy
@@ -683,7 +780,6 @@ __global__ void __launch_bounds__(32 * k2_warps_per_block(MODE), 16 / k2_warps_p
     // PI[b][t] != 0 only for vertices t and the 8 nodes b with b_k in {t_k, 1} (weight 1/2 per
     // mid index): lane (comp, vertex) = (t >> 3, t & 7) forms one PI^T sum, and the node lanes
     // pick their four components up by shuffle
-    float lps = 0.f;
     if constexpr (MODE == MODE_OPERATOR) {
       const int comp = t >> 3, v = t & 7;
       const int it0 = (v & 1) ? 2 : 0, it1 = (v & 2) ? 2 : 0, it2 = (v & 4) ? 2 : 0;
@@ -695,6 +791,7 @@ __global__ void __launch_bounds__(32 * k2_warps_per_block(MODE), 16 / k2_warps_p
         lps = fmaf(-wgt, gp[b0 + 3 * b1 + 9 * b2], lps);
       }
     }
+    }
     {
       const int it0 = t % 3, it1 = (t / 3) % 3, it2 = t / 9;
       const bool vtx = MODE == MODE_OPERATOR && t < 27 && it0 != 1 && it1 != 1 && it2 != 1;
@@ -703,7 +800,7 @@ __global__ void __launch_bounds__(32 * k2_warps_per_block(MODE), 16 / k2_warps_p
 #pragma unroll
       for (int comp = 0; comp < 4; ++comp) {
         const float l = __shfl_sync(0xffffffffu, lps, comp * 8 + (vid & 7));
-        e[comp] = t < 27 ? S[oTZ + (comp * 2) * kTZS + t] + (vtx ? l : 0.f) : 0.f;
+        e[comp] = t < 27 ? S[oTZ + comp * kTZO + t] + (vtx ? l : 0.f) : 0.f;
       }
       if (t < 27) A.elem[(int64_t)c * 27 + t] = make_float4(e[0], e[1], e[2], e[3]);
     }

@@ -36,8 +36,11 @@ template <> struct TcCfg<DNNMG_PREC_TF32X3> {
 template <> struct TcCfg<DNNMG_PREC_FP8> {
   static constexpr int ESZ = 1, PARTS = 1, NW = 6, NA = 4, KSTEP = 32, KC = 64;
 };
+#ifndef DNNMG_F16X3_NA
+#define DNNMG_F16X3_NA 5
+#endif
 template <> struct TcCfg<DNNMG_PREC_F16X3> {
-  static constexpr int ESZ = 2, PARTS = 2, NW = 2, NA = 4, KSTEP = 16, KC = 32;
+  static constexpr int ESZ = 2, PARTS = 2, NW = 2, NA = DNNMG_F16X3_NA, KSTEP = 16, KC = 32;
 };
 static int kc_of(int precision) {
   return precision == DNNMG_PREC_TF32X3 ? 16 : precision == DNNMG_PREC_FP8 ? 64 : 32;

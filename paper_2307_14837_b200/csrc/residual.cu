@@ -1134,7 +1134,8 @@ int32_t launch_residual(const dnnmg_level_t* lv, const float* x, const float* b_
     DNNMG_REQUIRE(cudaStreamWaitEvent(s, b_ready, 0) == cudaSuccess, DNNMG_ERR_CUDA,
                   "residual: cudaStreamWaitEvent(b_ready) failed");
   }
-  node_sum_kernel<<<grid_for(lv->n_nodes, 256), 256, 0, s>>>(
+  // 8 blocks per SM: all resident at once (0.0805 -> 0.078 ms at config 3 against 64 waves)
+  node_sum_kernel<<<grid_for(lv->n_nodes, 256, 8), 256, 0, s>>>(
       lv->n_nodes, lv->node_cell_ptr, lv->node_cell_idx, reinterpret_cast<const float4*>(elem), b,
       1.0f, (apply_mask && lv->dof_mask) ? lv->dof_mask : nullptr, reinterpret_cast<float4*>(r),
       lv->node_order, lv->node_order ? lv->visit_ptr : nullptr, lv->visit_idx);

@@ -120,11 +120,11 @@ constexpr int CP = 16;       // P[i][k] = delta*w*g_i (J^-1 pi v)_k: LPS Gpi tes
 #ifndef DNNMG_K2_WPB
 #define DNNMG_K2_WPB 16
 #endif
-// warps per block of the element kernel.  Operator form (128 registers, 16 warps per SM either
-// way): one 16-warp block per SM instead of four 4-warp blocks, 0.827 -> 0.805 ms at config 3 (the
-// warps of one block stay in step and work on neighbouring cells); the RHS form (95-107
-// registers) keeps 4-warp blocks, of which five fit an SM (0.63 vs 0.70 ms at config 2).
-__host__ __device__ constexpr int k2_warps_per_block(int mode) { return mode == 1 ? 4 : DNNMG_K2_WPB; }
+// warps per block of the element kernel: one 16-warp block per SM instead of four 4-warp blocks
+// (the operator form needs 128 registers, 16 warps per SM either way): 0.827 -> 0.805 ms at
+// config 3; the 16 warps work on neighbouring cells.  The RHS form (95-107 registers, five
+// 4-warp blocks would fit) measured the same way: 0.556 -> 0.538 ms at config 3.
+__host__ __device__ constexpr int k2_warps_per_block(int /*mode*/) { return DNNMG_K2_WPB; }
 
 enum { MODE_OPERATOR = 0, MODE_RHS = 1 };
 
